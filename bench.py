@@ -1,0 +1,400 @@
+"""GEM data-parallel core benchmark (BASELINE.json: Qwen3-235B-shaped trace).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+
+One timed step = the statistics phase over the whole synthetic router trace
+(94 layers x 2^24 tokens x top-8 int16 ids, 25.2 GB resident in HBM):
+K1 ids->histograms, K2 step co-activation Gram, K3 stats finalize, K3b classes.
+`value` = trace tokens/s (whole job). Secondary numbers on the same line:
+candidate mappings/s (10k candidate [94,128] mappings scored on the full
+trace) and time-to-mapping (statistics + GEM-Place search of all 94 layers on
+all 16,384 steps, 32 runs per layer). Multi-GPU: token-range shards, one NCCL
+all-reduce of the exact integer statistics (colsum, active counts, Gram).
+Inputs exceed L2 (126 MB) by 200x, so no explicit L2 flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "trace tokens/s (stats) + candidate mappings/s; time-to-mapping, Qwen3-235B"
+
+CONFIGS = {
+    # name: (L, N, k, E, B, G, C)
+    "mixtral": (32, 65536, 2, 8, 1024, 8, 10000),
+    "olmoe": (16, 1 << 20, 8, 64, 1024, 8, 10000),
+    "qwen3-30b": (48, 1 << 22, 8, 128, 1024, 8, 10000),
+    "qwen3-235b": (94, 1 << 24, 8, 128, 1024, 8, 10000),
+    "deepseek-v3": (58, 1 << 24, 8, 256, 1024, 32, 10000),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", default="qwen3-235b", choices=sorted(CONFIGS))
+    ap.add_argument("--candidates", type=int, default=None, help="override C (candidate mappings)")
+    ap.add_argument("--no-search", action="store_true", help="skip the time-to-mapping leg")
+    ap.add_argument("--no-candidates", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--search-steps", type=int, default=None, help="search window (default: all steps)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+
+class Clocks:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes/launch of the dominant kernel from the committed ncu capture, if any."""
+    p = ROOT / "profiles" / "ncu_topk_hist.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_19945_b200 as gem
+    from paper_2605_19945_b200 import _device, _lib, ingest
+    from paper_2605_19945_b200 import mapping as gm
+    from paper_2605_19945_b200 import search as gs
+    from paper_2605_19945_b200.trace import DeviceStats, finalize_stats
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L, N, k, E, B, G, C = CONFIGS[args.config]
+    if args.candidates:
+        C = args.candidates
+    T = N // B
+    spec = ingest.TopkTraceSpec(num_layers=L, num_tokens=N, top_k=k, num_experts=E, tokens_per_step=B, seed=0)
+    # token-range shard of this rank (step aligned)
+    steps_per = -(-T // world)
+    t0, t1 = rank * steps_per, min(T, (rank + 1) * steps_per)
+    n_local = (t1 - t0) * B
+    ids = ingest.generate_topk_ids(spec, dtype=torch.int16, token_offset=t0 * B, num_tokens=n_local)
+    hist = torch.empty((L, t1 - t0, E), dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    kev = []  # (start, end) events around K1 per timed step
+
+    def stats_step(timed: bool):
+        colsum = torch.zeros((L, E), dtype=torch.int64, device="cuda")
+        active = torch.zeros((L, E), dtype=torch.int32, device="cuda")
+        dropped = torch.zeros((L,), dtype=torch.int64, device="cuda")
+        gram = torch.zeros((L, E, E), dtype=torch.int64, device="cuda")
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        _lib.call("gem_topk_hist", ids.data_ptr(), 2, L, n_local, k, B, E, hist.data_ptr(), colsum.data_ptr(),
+                  active.data_ptr(), dropped.data_ptr(), stream.cuda_stream)
+        if timed:
+            e1.record(stream)
+            kev.append((e0, e1))
+        _lib.call("gem_step_gram", hist.data_ptr(), L, t1 - t0, E, gram.data_ptr(), stream.cuda_stream)
+        if world > 1:
+            for t in (colsum, active, gram):
+                dist.all_reduce(t)
+        ds = DeviceStats(colsum, active, gram, T)
+        mu, af, corr = finalize_stats(ds, with_corr=True)
+        cls = ingest.classify_device(colsum, active, gram, T)
+        return mu, af, corr, cls
+
+    for _ in range(args.warmup):
+        stats_step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            out = stats_step(True)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    k1_ms = sum(a.elapsed_time(b) for a, b in kev) / len(kev)
+    tokens_per_s = N / (ms / 1e3)
+    result = {
+        "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int16 ids / int32+int64 counts / f64 stats", "data": "synthetic",
+        "config": {"workload": f"{args.config}: stats phase over the full router trace", "layers": L,
+                   "tokens": N, "top_k": k, "experts": E, "tokens_per_step": B, "steps_per_layer": T,
+                   "virtual_gpus": G, "id_dtype": "int16", "l2": "inputs 25 GB >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"token-range shards x{world}, NCCL all-reduce of integer stats"},
+        "gpu_launches": 4 * args.steps,
+        "clocks": clk.summary(),
+    }
+    # roofline of the dominant kernel (K1)
+    algo_bytes = L * n_local * k * 2 + L * (t1 - t0) * E * 4
+    peak, peak_src = peaks()
+    achieved = algo_bytes / (k1_ms / 1e3) / 1e9
+    result["roofline"] = {"kernel": "topk_hist_kernel (K1)", "bound": "hbm", "achieved": achieved, "peak": peak,
+                          "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(),
+                          "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": k1_ms,
+                          "kernel_share_of_step": k1_ms / ms, "peak_source": peak_src}
+
+    # ---- e2e through the public API with host (pinned) ids
+    if not args.no_e2e and world == 1:
+        host_ids = torch.empty(ids.shape, dtype=ids.dtype, pin_memory=True)
+        host_ids.copy_(ids)
+        dev_ids = torch.empty_like(ids)
+        torch.cuda.synchronize()
+
+        def e2e_step():
+            dev_ids.copy_(host_ids, non_blocking=True)
+            st = ingest.trace_statistics(dev_ids, B, E)
+            res = (st.mean_utilization.to("cpu", non_blocking=True), st.classes.cls.to("cpu", non_blocking=True))
+            torch.cuda.current_stream().synchronize()
+            return res
+
+        e2e_step()
+        reps = max(1, min(3, args.steps))
+        s0 = time.perf_counter()
+        for _ in range(reps):
+            e2e_step()
+        e2e_s = (time.perf_counter() - s0) / reps
+        result["e2e"] = {"value": N / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(ids.numel() * 2),
+                         "d2h_bytes_per_step": int(L * E * 8 + L * E), "ms_per_step": e2e_s * 1e3,
+                         "path": "ingest.trace_statistics(ids from pinned host memory)"}
+        del host_ids, dev_ids
+
+    # ---- candidate mappings/s (C candidates x all layers, full trace)
+    if not args.no_candidates and world == 1:
+        profile = gem.generate_profile(gem.VariabilitySetupSpec(num_gpus=G, setup="moderate", tile_size=64,
+                                                                max_tokens=B * k, rng_seed=0))
+        rng = np.random.default_rng(0)
+        base = np.repeat(np.arange(G, dtype=np.int8), E // G)
+        cand = np.empty((C, L, E), dtype=np.int8)
+        for c in range(C):
+            cand[c] = np.stack([rng.permutation(base) for _ in range(L)])
+        cand_d = torch.from_numpy(cand).cuda()
+        nmax = B * k
+        layer_scores = torch.empty((C, L), dtype=torch.float64, device="cuda")
+        gm.score_candidates_device(hist, nmax, profile, cand_d[:64].contiguous(), layer_scores[:64])
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        total, _ = gm.score_candidates_device(hist, nmax, profile, cand_d, layer_scores)
+        c1.record()
+        torch.cuda.synchronize()
+        cms = c0.elapsed_time(c1)
+        best = int(torch.argmin(total).item())
+        result["candidates"] = {"value": C / (cms / 1e3), "unit": "candidate mappings/s", "ms": cms,
+                                "candidates": C, "layers": L, "steps": T, "best_index": best,
+                                "best_score": float(total[best].item())}
+        del cand_d, layer_scores
+
+    # ---- time-to-mapping: stats + search of every layer (full trace)
+    if not args.no_search and world == 1:
+        profile = gem.generate_profile(gem.VariabilitySetupSpec(num_gpus=G, setup="moderate", tile_size=64,
+                                                                max_tokens=B * k, rng_seed=0))
+        cfg = gem.SearchConfig(rng_seed=0)
+        Tw = args.search_steps or T
+        hwin = hist[:, :Tw].contiguous()
+        torch.cuda.synchronize()
+        s0 = time.perf_counter()
+        mu, af, corr, cls = stats_step(False)
+        results = gs.search_hist(hwin, B * k, profile, cfg, mean_util=None if Tw != T else mu.cpu().numpy())
+        torch.cuda.synchronize()
+        ttm = time.perf_counter() - s0
+        swaps = [r.swap_count for res in results for r in res.per_restart]
+        result["time_to_mapping"] = {"value": ttm, "unit": "s", "steps_searched": Tw, "runs": len(swaps),
+                                     "swaps_median": float(np.median(swaps)), "swaps_max": int(max(swaps)),
+                                     "aggregate_score": gs.aggregate_score(results)}
+
+    if not args.no_cpu and world == 1 and rank == 0:
+        try:
+            result["cpu_baseline"] = cpu_stats_baseline(spec, ids)
+        except Exception as exc:  # the baseline is reported, never required
+            result["cpu_baseline"] = {"error": repr(exc)}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# CPU side: reference compute_stats (oracle/_ref, gemap 0.1.0) + a bincount
+# restatement of id ingestion (the reference has no id ingestion)
+
+
+def _cpu_layer(args):
+    ids_l, B, E = args
+    import numpy as np
+
+    from oracle import oracle as o
+
+    gemap = o.import_reference()
+    n = ids_l.shape[0]
+    step = (np.arange(n) // B).repeat(ids_l.shape[1])
+    T = -(-n // B)
+    hist = np.bincount(step * E + ids_l.ravel().astype(np.int64), minlength=T * E).reshape(T, E)
+    st = gemap.compute_stats(gemap.ExpertTrace(hist))
+    return float(st.mean_utilization[0])
+
+
+def cpu_stats_run(ids_np, B, E, cores):
+    """Reference statistics for every layer of ids_np [l, n, k] on `cores` processes -> seconds."""
+    from concurrent.futures import ProcessPoolExecutor
+
+    work = [(ids_np[l], B, E) for l in range(ids_np.shape[0])]
+    s0 = time.perf_counter()
+    if cores > 1:
+        with ProcessPoolExecutor(max_workers=cores) as ex:
+            list(ex.map(_cpu_layer, work))
+    else:
+        for w in work:
+            _cpu_layer(w)
+    return time.perf_counter() - s0
+
+
+def cpu_stats_baseline(spec, ids_dev):
+    """Bounded sample: `layers` full layers (all 2^24 tokens) of the same trace."""
+    cores = os.cpu_count() or 1
+    layers = min(spec.num_layers, max(2, min(cores, 8)))
+    ids_np = ids_dev[:layers].cpu().numpy()
+    secs = cpu_stats_run(ids_np, spec.tokens_per_step, spec.num_experts, min(cores, layers))
+    tokens_equiv = spec.num_tokens * layers / spec.num_layers
+    return {"value": tokens_equiv / secs, "unit": "tokens/s", "cores": min(cores, layers), "kind": "reference",
+            "sample": f"{layers} of {spec.num_layers} layers x {spec.num_tokens} tokens: np.bincount ingestion "
+                      f"(restatement) + reference gemap.compute_stats (oracle/_ref), {secs:.2f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import oracle as o
+
+    if o.import_reference() is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (reference build) missing"}))
+        return
+    L, N, k, E, B, G, C = CONFIGS[args.config]
+    T = N // B
+    # the same synthetic ids, generated by the CPU twin of the device generator
+    from paper_2605_19945_b200.ingest import TopkTraceSpec, _prob_u32, planted_layout
+
+    spec = TopkTraceSpec(num_layers=L, num_tokens=N, top_k=k, num_experts=E, tokens_per_step=B, seed=0)
+    cores = os.cpu_count() or 1
+    layers = min(L, max(1, min(cores, 4)))
+    sample_tokens = min(N, 1 << 21)
+    w, r = planted_layout(spec)
+    ids = o.gen_topk(layers, sample_tokens, k, B, E, w[:layers], r[:layers], _prob_u32(0.85), _prob_u32(0.17), 3, 0)
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        cpu_stats_run(ids[:, : B * 16], B, E, min(cores, layers))
+    times = [cpu_stats_run(ids, B, E, min(cores, layers)) for _ in range(max(1, min(args.steps, 3)))]
+    secs = float(np.median(times))
+    value = sample_tokens * layers / L / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1,
+        "steps": len(times), "warmup": 1, "ms_per_step": secs * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64 counts / f64 stats", "data": "synthetic",
+        "config": {"workload": f"{args.config}: stats phase (bounded CPU sample)", "layers": L, "tokens": N,
+                   "top_k": k, "experts": E},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": min(cores, layers), "kind": "reference",
+                         "sample": f"{layers} layers x {sample_tokens} tokens; np.bincount ingestion restatement + "
+                                   "reference gemap.compute_stats (Cython build in oracle/_ref)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,250 @@
+"""CUDA kernels vs the CPU oracle and the reference golden vectors (bit-exact
+for every integer and every score; Pearson within 1e-12 absolute)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from _golden import curves_args, f, fl, profile as golden_profile, vectors
+from conftest import balanced_assignment, mixed_profile, random_counts, staircase_profile
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2605_19945_b200 as gem  # noqa: E402
+from paper_2605_19945_b200 import ingest, kernels  # noqa: E402
+
+
+# --------------------------------------------------------------------- curves
+
+def test_curve_eval_golden():
+    be = kernels.active()
+    for case in vectors()["curves"]:
+        p = golden_profile(gem, case["profile"])
+        ns = np.asarray(case["counts"], dtype=np.int64)
+        for g, want in enumerate(case["cost"]):
+            assert np.array_equal(p.curves[g].cost_many(ns), fl(want))
+            xs = np.concatenate([c.token_counts for c in p.curves])
+            ys = np.concatenate([c.latencies for c in p.curves])
+            off = np.concatenate(([0], np.cumsum([c.num_samples for c in p.curves]))).astype(np.int64)
+            dl = np.asarray([c.dense_limit for c in p.curves], dtype=np.int64)
+            assert np.array_equal(be.eval_curve_packed(xs, ys, off, dl, g, ns), fl(want))
+
+
+# -------------------------------------------------------------- ingestion (K1)
+
+@pytest.mark.parametrize("dtype", [torch.int16, torch.int32])
+@pytest.mark.parametrize("shape", [(3, 5000, 8, 256, 64), (2, 1000, 2, 100, 7), (1, 777, 3, 50, 300),
+                                   (2, 40000, 8, 9000, 16)])
+def test_topk_hist_random_ids(oracle, dtype, shape):
+    L, N, k, B, E = shape
+    rng = np.random.default_rng(sum(shape))
+    ids = rng.integers(-2, E + 2, (L, N, k)).astype(np.int16 if dtype == torch.int16 else np.int32)
+    h = ingest.ids_to_histograms(torch.from_numpy(ids).cuda(), B, E, check_dropped=False)
+    want, dropped = oracle.topk_hist(ids, B, E)
+    assert np.array_equal(h.hist.cpu().numpy(), want)
+    assert np.array_equal(h.dropped.cpu().numpy(), dropped)
+    assert np.array_equal(h.colsum.cpu().numpy(), want.sum(axis=1))
+    assert np.array_equal(h.active.cpu().numpy(), (want > 0).sum(axis=1))
+
+
+def test_topk_hist_unaligned_view(oracle):
+    rng = np.random.default_rng(9)
+    base = rng.integers(0, 32, (1, 4097, 3)).astype(np.int16)
+    ids = torch.from_numpy(base).cuda()[:, 1:, :].contiguous()
+    h = ingest.ids_to_histograms(ids, 64, 32)
+    want, _ = oracle.topk_hist(base[:, 1:, :].copy(), 64, 32)
+    assert np.array_equal(h.hist.cpu().numpy(), want)
+
+
+def test_dropped_ids_raise():
+    ids = torch.tensor([[[0, 1], [5, 2]]], dtype=torch.int16).cuda()
+    with pytest.raises(gem.ValidationError):
+        ingest.ids_to_histograms(ids, 2, 4)
+
+
+@pytest.mark.parametrize("dtype", [torch.int16, torch.int32])
+def test_generator_matches_oracle(oracle, dtype):
+    spec = ingest.TopkTraceSpec(num_layers=3, num_tokens=5000, top_k=4, num_experts=24, tokens_per_step=300, seed=11)
+    ids = ingest.generate_topk_ids(spec, dtype=dtype)
+    w, r = ingest.planted_layout(spec)
+    want = oracle.gen_topk(3, 5000, 4, 300, 24, w, r, ingest._prob_u32(0.85), ingest._prob_u32(0.17), 3, 11,
+                           id_bytes=2 if dtype == torch.int16 else 4)
+    assert np.array_equal(ids.cpu().numpy(), want)
+    part = ingest.generate_topk_ids(spec, dtype=dtype, token_offset=1234, num_tokens=2000)
+    assert np.array_equal(part.cpu().numpy(), want[:, 1234:3234])
+
+
+# ------------------------------------------------------- statistics (K2, K3)
+
+def test_stats_and_classes_match_oracle(oracle):
+    spec = ingest.TopkTraceSpec(num_layers=3, num_tokens=200 * 512, top_k=8, num_experts=64, tokens_per_step=512,
+                                seed=5)
+    ids = ingest.generate_topk_ids(spec)
+    st = ingest.trace_statistics(ids, 512, 64)
+    hist = st.hist.hist.cpu().numpy().astype(np.int64)
+    for l in range(3):
+        mu, af, corr = oracle.stats(hist[l])
+        assert np.array_equal(st.mean_utilization[l].cpu().numpy(), mu)
+        assert np.array_equal(st.active_fraction[l].cpu().numpy(), af)
+        c = st.correlation[l].cpu().numpy()
+        assert np.allclose(c, corr, rtol=0, atol=1e-12)
+        assert np.array_equal(c, c.T)
+        g = st.gram[l].cpu().numpy()
+        want_g = oracle.gram(hist[l])
+        iu = np.triu_indices(64)
+        assert np.array_equal(g[iu], want_g[iu])
+        cls, grp = oracle.classify(hist[l])
+        assert np.array_equal(st.classes.cls[l].cpu().numpy(), cls)
+        assert np.array_equal(st.classes.group[l].cpu().numpy(), grp)
+
+
+def test_planted_groups_recovered():
+    spec = ingest.TopkTraceSpec(num_layers=2, num_tokens=400 * 1024, top_k=8, num_experts=128, seed=3)
+    st = ingest.trace_statistics(ingest.generate_topk_ids(spec), 1024, 128)
+    _, role = ingest.planted_layout(spec)
+    for l in range(2):
+        cls = st.classes.cls[l].cpu().numpy()
+        grp = st.classes.group[l].cpu().numpy()
+        for g in range(spec.num_groups):
+            members = np.flatnonzero(role[l] == 2 + g)
+            assert all(cls[m] == ingest.CLASS_TEMPORAL for m in members)
+            assert len({int(grp[m]) for m in members}) == 1 and grp[members[0]] == members.min()
+        for e in np.flatnonzero(role[l] == 1):
+            assert cls[e] == ingest.CLASS_CONSISTENT
+
+
+def test_compute_stats_golden():
+    for case in vectors()["scoring"]:
+        tr = gem.ExpertTrace(np.asarray(case["tokens"], dtype=np.int64))
+        st = gem.compute_stats(tr)
+        assert np.array_equal(st.mean_utilization, fl(case["mean_utilization"]))
+        assert np.array_equal(st.active_fraction, fl(case["active_fraction"]))
+        want = np.array([fl(r) for r in case["correlation"]])
+        assert np.allclose(st.correlation, want, rtol=0, atol=1e-12)
+        assert np.array_equal(st.correlation, st.correlation.T)
+        assert gem.eplb_mapping(st, len(case["profile"])).assignment.tolist() == case["eplb"]
+
+
+# ------------------------------------------------------------ scoring (K4, K5)
+
+def test_score_and_replay_golden():
+    for case in vectors()["scoring"]:
+        tr = gem.ExpertTrace(np.asarray(case["tokens"], dtype=np.int64))
+        p = golden_profile(gem, case["profile"])
+        m = gem.ExpertMapping(np.asarray(case["assignment"]), p.num_gpus)
+        assert gem.score_mapping(tr, p, m) == f(case["score"])
+        rep = gem.replay(tr, p, m)
+        assert [s.straggler_latency for s in rep.step_costs] == list(fl(case["step_max"]))
+        assert [s.straggler_gpu for s in rep.step_costs] == case["straggler"]
+        assert list(rep.per_gpu_busy_time) == list(fl(case["busy"]))
+        assert list(rep.per_gpu_total_tokens) == case["gpu_tokens"]
+        assert rep.total_score == f(case["score"])
+        assert {k: f(v) for k, v in case["percentiles"].items()} == rep.percentiles
+
+
+def test_score_candidates_batch_matches_oracle(oracle):
+    from paper_2605_19945_b200 import mapping as gm
+    from paper_2605_19945_b200 import _device
+
+    rng = np.random.default_rng(77)
+    L, T, E, G, C = 3, 50, 32, 4, 300
+    tok = np.stack([random_counts(rng, T, E, high=200) for _ in range(L)])
+    p = staircase_profile(gem, rng, G, tile=64, tiles=128)
+    cand = np.stack([[balanced_assignment(rng, E, G) for _ in range(L)] for _ in range(C)])
+    hist, nmax = _device.counts_to_device_int32(tok)
+    total, per_layer = gm.score_candidates_device(hist, nmax, p, torch.from_numpy(cand.astype(np.int8)).cuda())
+    total, per_layer = total.cpu().numpy(), per_layer.cpu().numpy()
+    cv = oracle.Curves.from_profile(p)
+    for c in range(0, C, 7):
+        want_l = [oracle.score(tok[l], cand[c, l], cv) for l in range(L)]
+        assert per_layer[c].tolist() == want_l
+        s = 0.0
+        for v in want_l:
+            s = s + v
+        assert total[c] == s
+
+
+# ------------------------------------------------------ protocol (tier 1 ABI)
+
+def test_protocol_golden():
+    be = kernels.active()
+    assert be.BACKEND == "cuda"
+    for case in vectors()["protocol"]:
+        tok = np.asarray(case["tokens"], dtype=np.int64)
+        p = golden_profile(gem, case["profile"])
+        a = np.asarray(case["assignment"], dtype=np.int64)
+        xs = np.concatenate([c.token_counts for c in p.curves])
+        ys = np.concatenate([c.latencies for c in p.curves])
+        off = np.concatenate(([0], np.cumsum([c.num_samples for c in p.curves]))).astype(np.int64)
+        dl = np.asarray([c.dense_limit for c in p.curves], dtype=np.int64)
+        G = p.num_gpus
+        loads = np.zeros((tok.shape[0], G), dtype=np.int64)
+        for g in range(G):
+            loads[:, g] = tok[:, a == g].sum(axis=1)
+        lat = np.stack([be.eval_curve_packed(xs, ys, off, dl, g, loads[:, g]) for g in range(G)], axis=1)
+        found, i, j, cand = be.best_swap(tok, a, loads, lat, xs, ys, off, dl)
+        want = case["best_swap"]
+        assert (found, i, j) == (want[0], want[1], want[2]) and cand == f(want[3])
+        if case["pair"]:
+            got = be.swap_candidate_score(tok, a, loads, lat, xs, ys, off, dl, *case["pair"])
+            assert got == f(case["pair_score"])
+
+
+# ------------------------------------------------------------ search (K6-K8)
+
+def test_search_golden():
+    for case in vectors()["search"]:
+        tr = gem.ExpertTrace(np.asarray(case["tokens"], dtype=np.int64))
+        p = golden_profile(gem, case["profile"])
+        res = gem.search(tr, p, gem.SearchConfig(restarts=case["restarts"], rng_seed=case["seed"]))
+        assert res.best_score == f(case["best_score"])
+        assert res.best_mapping.assignment.tolist() == case["best_assignment"]
+        assert res.provenance == case["provenance"]
+        for got, want in zip(res.per_restart, case["records"]):
+            assert got.provenance == want["provenance"]
+            assert got.swap_count == want["swaps"]
+            assert list(got.trajectory) == list(fl(want["trajectory"]))
+        st = gem.compute_stats(tr)
+        init = gem.initial_mapping(st, 1, tr, p, np.random.default_rng(case["seed"] ^ 1))
+        assert init.assignment.tolist() == case["initial_1"]
+
+
+@pytest.mark.parametrize("G,E,T", [(2, 8, 16), (4, 16, 40), (8, 64, 128), (3, 12, 1), (8, 8, 30)])
+def test_search_matches_oracle(oracle, G, E, T):
+    rng = np.random.default_rng(G * 1000 + E + T)
+    tok = random_counts(rng, T, E, high=300)
+    p = mixed_profile(gem, rng, G) if E < 64 else staircase_profile(gem, rng, G, tile=64, tiles=256)
+    res = gem.search(gem.ExpertTrace(tok), p, gem.SearchConfig(restarts=5, rng_seed=E))
+    want = oracle.search(tok, oracle.Curves.from_profile(p), restarts=5, rng_seed=E)
+    assert res.best_score == want["best_score"]
+    assert res.best_mapping.assignment.tolist() == want["best_assignment"].tolist()
+    assert [r.trajectory for r in res.per_restart] == [tuple(r["trajectory"]) for r in want["records"]]
+
+
+def test_search_layers_matches_per_layer(oracle):
+    rng = np.random.default_rng(4)
+    traces = [gem.ExpertTrace(random_counts(rng, 24, 16, high=100)) for _ in range(5)]
+    p = staircase_profile(gem, rng, 4)
+    cfg = gem.SearchConfig(restarts=3, rng_seed=9)
+    batched = gem.search_layers(traces, p, cfg)
+    cv = oracle.Curves.from_profile(p)
+    for tr, res in zip(traces, batched):
+        want = oracle.search(tr.tokens, cv, restarts=3, rng_seed=9)
+        assert res.best_score == want["best_score"]
+        assert res.best_mapping.assignment.tolist() == want["best_assignment"].tolist()
+
+
+def test_refine_matches_oracle(oracle):
+    rng = np.random.default_rng(12)
+    for _ in range(10):
+        tok = random_counts(rng, 20, 12, high=200)
+        p = mixed_profile(gem, rng, 3)
+        a = balanced_assignment(rng, 12, 3)
+        got, swaps = gem.refine(gem.ExpertMapping(a, 3), gem.ExpertTrace(tok), p, gem.SearchConfig())
+        wa, _, wswaps, _ = oracle.refine(tok, a, oracle.Curves.from_profile(p), 1e-3, 120)
+        assert swaps == wswaps and got.assignment.tolist() == wa.tolist()

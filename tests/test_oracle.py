@@ -1,0 +1,147 @@
+"""The CPU oracle is pinned to the reference: golden vectors generated from the
+real `gemap` (tests/golden/make_golden.py) must be reproduced bit for bit."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from _golden import curves_args, f, fl, vectors
+
+
+def test_philox_known_answers(oracle):
+    # Random123 Philox4x32-10 KATs
+    assert [hex(v) for v in oracle.philox4x32_10([0, 0, 0, 0], [0, 0])] == \
+        ["0x6627e8d5", "0xe169c58d", "0xbc57ac4c", "0x9b00dbd8"]
+    assert [hex(v) for v in oracle.philox4x32_10([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2)] == \
+        ["0x408f276d", "0x41c83b0e", "0xa20bc7c6", "0x6d5451fd"]
+    assert [hex(v) for v in oracle.philox4x32_10([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344],
+                                                 [0xA4093822, 0x299F31D0])] == \
+        ["0xd16cfe09", "0x94fdcceb", "0x5001e420", "0x24126ea1"]
+
+
+def test_curve_eval_matches_reference(oracle):
+    for case in vectors()["curves"]:
+        cv = oracle.Curves(curves_args(case["profile"]))
+        ns = np.asarray(case["counts"], dtype=np.int64)
+        for g, want in enumerate(case["cost"]):
+            assert np.array_equal(cv.eval(g, ns), fl(want))
+
+
+def test_scoring_replay_stats_match_reference(oracle):
+    for case in vectors()["scoring"]:
+        tok = np.asarray(case["tokens"], dtype=np.int64)
+        cv = oracle.Curves(curves_args(case["profile"]))
+        a = np.asarray(case["assignment"], dtype=np.int64)
+        assert oracle.score(tok, a, cv) == f(case["score"])
+        rep = oracle.replay(tok, a, cv)
+        assert np.array_equal(rep["step_max"], fl(case["step_max"]))
+        assert rep["straggler"].tolist() == case["straggler"]
+        assert np.array_equal(rep["busy"], fl(case["busy"]))
+        assert rep["gpu_tokens"].tolist() == case["gpu_tokens"]
+        assert rep["total"] == f(case["score"])
+        mu, af, corr = oracle.stats(tok)
+        assert np.array_equal(mu, fl(case["mean_utilization"]))
+        assert np.array_equal(af, fl(case["active_fraction"]))
+        want_corr = np.array([fl(r) for r in case["correlation"]])
+        assert np.allclose(corr, want_corr, rtol=0, atol=1e-12)
+        assert np.array_equal(np.diag(corr), np.ones(tok.shape[1]))
+        assert oracle.eplb_assignment(mu, cv.G).tolist() == case["eplb"]
+
+
+def test_protocol_matches_reference(oracle):
+    for case in vectors()["protocol"]:
+        tok = np.asarray(case["tokens"], dtype=np.int64)
+        cv = oracle.Curves(curves_args(case["profile"]))
+        a = np.asarray(case["assignment"], dtype=np.int64)
+        loads = oracle.load_matrix(tok, a, cv.G)
+        lat = oracle.latency_matrix(cv, loads)
+        found, i, j, cand = oracle.best_swap(tok, a, loads, lat, cv)
+        want = case["best_swap"]
+        assert (found, i, j) == (want[0], want[1], want[2])
+        assert cand == f(want[3])
+        if case["pair"]:
+            assert oracle.swap_candidate_score(tok, a, loads, lat, cv, *case["pair"]) == f(case["pair_score"])
+
+
+def test_search_matches_reference(oracle):
+    for case in vectors()["search"]:
+        tok = np.asarray(case["tokens"], dtype=np.int64)
+        cv = oracle.Curves(curves_args(case["profile"]))
+        res = oracle.search(tok, cv, restarts=case["restarts"], rng_seed=case["seed"])
+        assert res["best_score"] == f(case["best_score"])
+        assert res["best_assignment"].tolist() == case["best_assignment"]
+        assert res["provenance"] == case["provenance"]
+        for got, want in zip(res["records"], case["records"]):
+            assert got["provenance"] == want["provenance"]
+            assert got["swap_count"] == want["swaps"]
+            assert list(got["trajectory"]) == list(fl(want["trajectory"]))
+        mu = oracle.mean_utilization(tok)
+        order = oracle.restart_order(mu, 1, np.random.default_rng(case["seed"] ^ 1), 0.2)
+        assert oracle.greedy(tok, order, cv).tolist() == case["initial_1"]
+
+
+def test_lockstep_fixture(oracle, data_dir):
+    import json
+
+    tr = np.asarray(json.loads((data_dir / "lockstep_trace.json").read_text())["tokens"], dtype=np.int64)
+    pj = json.loads((data_dir / "lockstep_profile.json").read_text())
+    cv = oracle.Curves([([s[0] for s in c["samples"]], [s[1] for s in c["samples"]], c["dense_limit"])
+                        for c in pj["curves"]])
+    a = np.asarray(json.loads((data_dir / "lockstep_mapping.json").read_text())["assignment"])
+    rep = oracle.replay(tr, a, cv)
+    assert rep["loads"][0].tolist() == [3, 6]
+    assert rep["step_max"].tolist() == [5.0, 4.0, 4.0]
+    assert rep["total"] == 13.0 and oracle.score(tr, a, cv) == 13.0
+    assert int(rep["straggler"][0]) == 1
+
+
+def test_topk_hist_is_bincount(oracle):
+    rng = np.random.default_rng(5)
+    ids = rng.integers(-3, 40, (3, 1000, 4)).astype(np.int16)
+    hist, dropped = oracle.topk_hist(ids, 128, 37)
+    T = -(-1000 // 128)
+    for l in range(3):
+        flat = ids[l].astype(np.int64)
+        step = np.repeat(np.arange(1000) // 128, 4).reshape(1000, 4)
+        ok = (flat >= 0) & (flat < 37)
+        want = np.bincount((step * 37 + flat)[ok], minlength=T * 37).reshape(T, 37)
+        assert np.array_equal(hist[l], want)
+        assert dropped[l] == int((~ok).sum())
+
+
+def test_classify_planted_structure(oracle):
+    # two perfectly co-bursting experts, one consistent expert, background
+    rng = np.random.default_rng(3)
+    T = 400
+    tok = np.zeros((T, 8), dtype=np.int64)
+    burst = rng.random(T) < 0.2
+    tok[:, 0] = np.where(burst, 30 + rng.integers(0, 3, T), 0)
+    tok[:, 3] = np.where(burst, 29 + rng.integers(0, 3, T), 0)
+    tok[:, 5] = np.where(rng.random(T) < 0.9, 10, 0)
+    tok[:, [1, 2, 4, 6, 7]] = 5 + rng.integers(0, 3, (T, 5))
+    cls, grp = oracle.classify(tok)
+    assert cls[0] == 2 and cls[3] == 2 and grp[0] == 0 and grp[3] == 0
+    assert cls[5] == 1
+    assert all(cls[e] == 1 for e in (1, 2, 4, 6, 7))
+    assert all(grp[e] == -1 for e in (1, 2, 4, 5, 6, 7))
+
+
+def test_gen_topk_properties(oracle):
+    L, N, k, B, E = 2, 3000, 4, 100, 16
+    rng = np.random.default_rng(1)
+    weight = rng.integers(1, 1000, (L, E)).astype(np.uint32)
+    role = np.zeros((L, E), dtype=np.int8)
+    role[:, 0] = 1
+    role[:, [1, 2]] = 2
+    ids = oracle.gen_topk(L, N, k, B, E, weight, role, int(0.85 * 2**32), int(0.17 * 2**32), 3, 42)
+    assert ids.min() >= 0 and ids.max() < E
+    assert all(len(set(row)) == k for row in ids.reshape(-1, k).tolist())  # distinct per token
+    # sharding by token offset reproduces the same ids
+    part = oracle.gen_topk(L, 1300, k, B, E, weight, role, int(0.85 * 2**32), int(0.17 * 2**32), 3, 42,
+                           token_offset=1700)
+    assert np.array_equal(part, ids[:, 1700:])
+    # group members burst together: both zero or both non-zero nearly always
+    hist, _ = oracle.topk_hist(ids, B, E)
+    both = (hist[0][:, 1] > 0) == (hist[0][:, 2] > 0)
+    assert both.mean() > 0.9
