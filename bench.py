@@ -132,7 +132,7 @@ def run_ours(args):
     import paper_2605_19945_b200 as gem
     from paper_2605_19945_b200 import _device, _lib, ingest
     from paper_2605_19945_b200 import mapping as gm
-    from paper_2605_19945_b200 import search as gs
+    from paper_2605_19945_b200.search import aggregate_score, search_hist
     from paper_2605_19945_b200.trace import DeviceStats, finalize_stats
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -280,13 +280,13 @@ def run_ours(args):
         torch.cuda.synchronize()
         s0 = time.perf_counter()
         mu, af, corr, cls = stats_step(False)
-        results = gs.search_hist(hwin, B * k, profile, cfg, mean_util=None if Tw != T else mu.cpu().numpy())
+        results = search_hist(hwin, B * k, profile, cfg, mean_util=None if Tw != T else mu.cpu().numpy())
         torch.cuda.synchronize()
         ttm = time.perf_counter() - s0
         swaps = [r.swap_count for res in results for r in res.per_restart]
         result["time_to_mapping"] = {"value": ttm, "unit": "s", "steps_searched": Tw, "runs": len(swaps),
                                      "swaps_median": float(np.median(swaps)), "swaps_max": int(max(swaps)),
-                                     "aggregate_score": gs.aggregate_score(results)}
+                                     "aggregate_score": aggregate_score(results)}
 
     if not args.no_cpu and world == 1 and rank == 0:
         try:

@@ -1,0 +1,278 @@
+// K1: router top-k ids -> per-step expert histograms (sm_100a).
+//
+// The reference starts from counts (trace.py:24-45); this is the ingestion
+// step that produces them. Bytes dominate: every id is read once (int16/int32,
+// 128-bit streaming loads) and every histogram cell is written once, so the
+// kernel is sized against HBM bandwidth.
+//
+// Counting: each warp owns a work unit of up to kHistStepsPerUnit consecutive
+// steps of one layer and keeps 32 lane-private sub-histograms in shared
+// memory, laid out bin-major / lane-minor (word = bin*32 + lane), so lane L
+// always touches bank L: increments never conflict and never contend, and a
+// shared atomic without return carries no dependency chain. Both int16 ids of
+// a 32-bit word are clamped with one __vminu2 to an overflow row (which counts
+// ids outside [0,E)), so the inner loop is branch-free: ~3.5 instructions per
+// id. Once per step the rows are reduced with conflict-free 128-bit reads and
+// written coalesced; per-expert totals and active-step counts accumulate in
+// registers and are flushed with one atomic per expert per unit. E > 160 uses
+// u16x2 counters (two bins per word) to halve shared memory.
+#include <cstdlib>
+
+#include "gem_common.cuh"
+
+namespace gem {
+
+constexpr int kHistWarps = 4;
+constexpr int kHistStepsPerUnit = 32;
+constexpr int kHistUnroll = 8;  // 128-bit loads in flight per lane (x2 with double buffering)
+
+// ---- wide layout (E <= kWideMaxE): one u32 counter per (bin, lane),
+//      word = bin*32 + lane; row E is the overflow row for ids >= E.
+constexpr int kWideMaxE = 160;
+
+// count the ids held in one 16-byte vector (int16: 8 ids, int32: 4 ids)
+template <typename IdT>
+__device__ __forceinline__ void count_vec_wide(uint32_t* cnt_lane, const uint4& v, uint32_t E, uint32_t Epair) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (sizeof(IdT) == 2) {
+      const uint32_t m = __vminu2(w[c], Epair);  // clamp both halves to the overflow row E
+      atomicAdd(cnt_lane + ((m & 0xffffu) << 5), 1u);
+      atomicAdd(cnt_lane + ((m >> 16) << 5), 1u);
+    } else {
+      atomicAdd(cnt_lane + (min(w[c], E) << 5), 1u);
+    }
+  }
+}
+
+// ---- packed layout (any E): two u16 counters per word,
+//      word = (bin>>1)*32 + lane; bin E (rounded to its pair) is the overflow bin.
+template <typename IdT>
+__device__ __forceinline__ void count_vec_packed(uint32_t* cnt_lane, const uint4& v, uint32_t E, uint32_t Epair) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (sizeof(IdT) == 2) {
+      const uint32_t m = __vminu2(w[c], Epair);
+      const uint32_t lo = m & 0xffffu, hi = m >> 16;
+      atomicAdd(cnt_lane + ((lo >> 1) << 5), 1u << ((lo & 1) << 4));
+      atomicAdd(cnt_lane + ((hi >> 1) << 5), 1u << ((hi & 1) << 4));
+    } else {
+      const uint32_t b = min(w[c], E);
+      atomicAdd(cnt_lane + ((b >> 1) << 5), 1u << ((b & 1) << 4));
+    }
+  }
+}
+
+template <typename IdT, bool WIDE>
+__device__ __forceinline__ void count_vec(uint32_t* cnt_lane, const uint4& v, uint32_t E, uint32_t Epair) {
+  if (WIDE) count_vec_wide<IdT>(cnt_lane, v, E, Epair);
+  else count_vec_packed<IdT>(cnt_lane, v, E, Epair);
+}
+
+template <bool WIDE>
+__device__ __forceinline__ void count_scalar(uint32_t* cnt_lane, uint32_t id, uint32_t E) {
+  const uint32_t b = min(id, E);
+  if (WIDE) atomicAdd(cnt_lane + (b << 5), 1u);
+  else atomicAdd(cnt_lane + ((b >> 1) << 5), 1u << ((b & 1) << 4));
+}
+
+// One warp = one work unit = up to kHistStepsPerUnit consecutive steps of one
+// layer. MAXR = histogram rows owned per lane in the reduction (rows/32).
+template <typename IdT, bool WIDE, int MAXR>
+__global__ void __launch_bounds__(kHistWarps * 32)
+topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B, int E, int64_t T,
+                 int32_t* __restrict__ hist, int64_t* __restrict__ colsum, int32_t* __restrict__ active,
+                 int64_t* __restrict__ dropped_out) {
+  extern __shared__ __align__(16) uint32_t hsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // counter rows: WIDE: E bins + 1 overflow row; packed: ceil((E+1)/2) pair rows
+  const int rows = WIDE ? E + 1 : (E + 2) / 2;
+  uint32_t* cnt = hsm + (size_t)warp * rows * 32;
+  uint32_t* cnt_lane = cnt + lane;
+  for (int w = lane; w < rows * 32; w += 32) cnt[w] = 0;
+  __syncwarp();
+  const uint32_t uE = (uint32_t)E;
+  const uint32_t Epair = uE | (uE << 16);
+  const int hrows = WIDE ? E : E / 2;  // reduced rows that hold real bins (packed: full pairs)
+
+  const int64_t units_per_layer = (T + kHistStepsPerUnit - 1) / kHistStepsPerUnit;
+  const int64_t total_units = L * units_per_layer;
+  const int64_t gwarp = (int64_t)blockIdx.x * kHistWarps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kHistWarps;
+  constexpr int BINS = WIDE ? 1 : 2;
+
+  for (int64_t unit = gwarp; unit < total_units; unit += nwarps) {
+    const int64_t l = unit / units_per_layer;
+    const int64_t t_begin = (unit % units_per_layer) * kHistStepsPerUnit;
+    const int64_t t_end = imin64(t_begin + kHistStepsPerUnit, T);
+    uint32_t csum[MAXR * BINS], act[MAXR * BINS];
+#pragma unroll
+    for (int q = 0; q < MAXR * BINS; ++q) { csum[q] = 0; act[q] = 0; }
+    uint32_t dropped = 0;
+
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      const int64_t tok0 = t * B;
+      const int64_t tok1 = imin64(tok0 + B, N);
+      const IdT* p = ids + (l * N + tok0) * k;
+      const int64_t cntn = (tok1 - tok0) * k;  // ids in this step
+      constexpr int per_vec = 16 / sizeof(IdT);
+      int64_t done = 0;
+      if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+        const int64_t nvec = cntn / per_vec;
+        const uint4* pv = reinterpret_cast<const uint4*>(p);
+        const int64_t nfull = nvec / (kHistUnroll * 32);  // full batches for the whole warp
+        if (nfull > 0) {
+          uint4 cur[kHistUnroll], nxt[kHistUnroll];
+#pragma unroll
+          for (int u = 0; u < kHistUnroll; ++u) cur[u] = __ldcs(pv + lane + u * 32);
+          for (int64_t bt = 0; bt < nfull; ++bt) {
+            const bool more = bt + 1 < nfull;
+            if (more) {
+              const uint4* q = pv + (bt + 1) * (kHistUnroll * 32) + lane;
+#pragma unroll
+              for (int u = 0; u < kHistUnroll; ++u) nxt[u] = __ldcs(q + u * 32);
+            }
+#pragma unroll
+            for (int u = 0; u < kHistUnroll; ++u) count_vec<IdT, WIDE>(cnt_lane, cur[u], uE, Epair);
+            if (more) {
+#pragma unroll
+              for (int u = 0; u < kHistUnroll; ++u) cur[u] = nxt[u];
+            }
+          }
+        }
+        for (int64_t v = nfull * (kHistUnroll * 32) + lane; v < nvec; v += 32)
+          count_vec<IdT, WIDE>(cnt_lane, __ldcs(pv + v), uE, Epair);
+        done = nvec * per_vec;
+      }
+      for (int64_t i = done + lane; i < cntn; i += 32) {
+        const uint32_t id = (sizeof(IdT) == 2) ? (uint32_t)(uint16_t)p[i] : (uint32_t)p[i];
+        count_scalar<WIDE>(cnt_lane, id, uE);
+      }
+      __syncwarp();
+      // Reduce the 32 lane-private columns of every row. Lane owns rows
+      // lane + 32q and reads them as 8 x 128-bit chunks, chunk (c+lane)&7 in
+      // iteration c (4 wavefronts per LDS.128: conflict-free), zeroing as it goes.
+      int32_t* hrow = hist + (l * T + t) * E;
+#pragma unroll
+      for (int q = 0; q < MAXR; ++q) {
+        const int row = lane + q * 32;
+        if (row < hrows) {
+          uint4* rp = reinterpret_cast<uint4*>(cnt + row * 32);
+          uint32_t s = 0;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int j = (c + lane) & 7;
+            const uint4 v = rp[j];
+            s += (v.x + v.y) + (v.z + v.w);
+            rp[j] = make_uint4(0u, 0u, 0u, 0u);
+          }
+          if (WIDE) {
+            hrow[row] = (int32_t)s;
+            csum[q] += s;
+            act[q] += (s > 0);
+          } else {
+            const uint32_t lo = s & 0xffffu, hi = s >> 16;
+            *reinterpret_cast<int2*>(hrow + 2 * row) = make_int2((int)lo, (int)hi);
+            csum[2 * q] += lo;
+            csum[2 * q + 1] += hi;
+            act[2 * q] += (lo > 0);
+            act[2 * q + 1] += (hi > 0);
+          }
+        }
+      }
+      // overflow: WIDE row E; packed: pair row E/2 (holds bin E-1 in its low
+      // half when E is odd, overflow in the high half; overflow alone when E is even)
+      {
+        const int orow = WIDE ? E : E / 2;
+        const uint32_t ov = cnt[orow * 32 + lane];
+        cnt[orow * 32 + lane] = 0;
+        if (WIDE || (E & 1) == 0) {
+          dropped += ov;
+        } else {
+          dropped += ov >> 16;
+          uint32_t lo = ov & 0xffffu;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) lo += __shfl_xor_sync(0xffffffffu, lo, o);
+          if (lane == 0) {
+            hrow[E - 1] = (int32_t)lo;
+            if (lo) {
+              atomicAdd((unsigned long long*)&colsum[l * E + E - 1], (unsigned long long)lo);
+              atomicAdd(&active[l * E + E - 1], 1);
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    // flush this unit's per-expert totals
+#pragma unroll
+    for (int q = 0; q < MAXR; ++q) {
+      const int row = lane + q * 32;
+      if (row >= hrows) continue;
+#pragma unroll
+      for (int bb = 0; bb < BINS; ++bb) {
+        const int bin = row * BINS + bb;
+        const uint32_t cs = csum[q * BINS + bb], ac = act[q * BINS + bb];
+        if (cs) atomicAdd((unsigned long long*)&colsum[l * E + bin], (unsigned long long)cs);
+        if (ac) atomicAdd(&active[l * E + bin], (int)ac);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dropped += __shfl_xor_sync(0xffffffffu, dropped, o);
+    if (lane == 0 && dropped) atomicAdd((unsigned long long*)&dropped_out[l], (unsigned long long)dropped);
+  }
+}
+
+template <typename IdT, bool WIDE, int MAXR>
+static int launch_hist_t(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int32_t* hist,
+                         int64_t* colsum, int32_t* active, int64_t* dropped, cudaStream_t st) {
+  const int rows = WIDE ? E + 1 : (E + 2) / 2;
+  const size_t smem = (size_t)kHistWarps * rows * 32 * sizeof(uint32_t);
+  auto kern = topk_hist_kernel<IdT, WIDE, MAXR>;
+  GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  GEM_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHistWarps * 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t units = L * ((T + kHistStepsPerUnit - 1) / kHistStepsPerUnit);
+  int64_t blocks = (int64_t)num_sms() * per_sm;
+  const int64_t need = (units + kHistWarps - 1) / kHistWarps;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  kern<<<(unsigned)blocks, kHistWarps * 32, smem, st>>>((const IdT*)ids, L, N, k, B, E, T, hist, colsum, active,
+                                                         dropped);
+  GEM_CHECK_LAUNCH("topk_hist_kernel");
+  return GEM_OK;
+}
+
+template <typename IdT>
+static int dispatch_hist(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int32_t* hist,
+                         int64_t* colsum, int32_t* active, int64_t* dropped, cudaStream_t st) {
+  if (E <= 64) return launch_hist_t<IdT, true, 2>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
+  if (E <= 128) return launch_hist_t<IdT, true, 4>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
+  if (E <= kWideMaxE) return launch_hist_t<IdT, true, 5>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
+  if (E <= 256) return launch_hist_t<IdT, false, 4>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
+  return launch_hist_t<IdT, false, 8>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
+}
+
+}  // namespace gem
+
+using namespace gem;
+
+extern "C" int gem_topk_hist(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k, int32_t B,
+                             int32_t E, int32_t* hist, int64_t* colsum, int32_t* active, int64_t* dropped,
+                             void* stream) {
+  GEM_REQUIRE(id_bytes == 2 || id_bytes == 4, "gem_topk_hist: id_bytes must be 2 or 4");
+  GEM_REQUIRE(L >= 1 && N >= 1 && k >= 1 && B >= 1 && E >= 1 && E <= 512,
+              "gem_topk_hist: bad shape L=%lld N=%lld k=%d B=%d E=%d (E <= 512)", (long long)L, (long long)N, k,
+              B, E);
+  GEM_REQUIRE(ids && hist && colsum && active && dropped, "gem_topk_hist: null pointer");
+  // a lane's u32 (wide) or u16 (packed) counter must not wrap within one step
+  GEM_REQUIRE(E <= kWideMaxE || (int64_t)B * k <= 65535,
+              "gem_topk_hist: E > %d needs at most 65535 ids per step", kWideMaxE);
+  const int64_t T = (N + B - 1) / B;
+  cudaStream_t st = as_stream(stream);
+  if (id_bytes == 2) return dispatch_hist<int16_t>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
+  return dispatch_hist<int32_t>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
+}

@@ -1,7 +1,7 @@
 // Trace ingestion and statistics on sm_100a.
 //
 //  K9 gem_gen_topk      synthetic router ids (Philox, integer-only)
-//  K1 gem_topk_hist     ids -> per-step histograms + per-expert totals
+//  (K1 gem_topk_hist lives in hist.cu)
 //     gem_hist_colstats counts -> per-expert totals (ExpertTrace input)
 //  K2 gem_step_gram     step-level co-activation Gram (Pearson statistics)
 //  K3 gem_stats_finalize / gem_classify
@@ -104,180 +104,6 @@ __global__ void gen_topk_kernel(int64_t N, int k, int B, int E, const uint32_t* 
       chosen[s] = pick;
       out[n * k + s] = (IdT)pick;
     }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K1: ids -> histograms
-// ---------------------------------------------------------------------------
-constexpr int kHistWarps = 8;
-constexpr int kHistMaxPairsPerLane = 8;  // E <= 512
-constexpr int kHistStepsPerUnit = 32;
-
-template <int PACK>
-struct LaneCounters;
-
-// PACK=2: two 16-bit counters per word; word index = (bin>>1)*32 + lane.
-template <>
-struct LaneCounters<2> {
-  static __device__ __forceinline__ uint32_t word(int bin, int lane) { return ((bin >> 1) << 5) + lane; }
-  static __device__ __forceinline__ uint32_t inc(int bin) { return 1u << ((bin & 1) << 4); }
-  static constexpr int bins_per_word = 2;
-};
-// PACK=1: one 32-bit counter per word; word index = bin*32 + lane.
-template <>
-struct LaneCounters<1> {
-  static __device__ __forceinline__ uint32_t word(int bin, int lane) { return (bin << 5) + lane; }
-  static __device__ __forceinline__ uint32_t inc(int) { return 1u; }
-  static constexpr int bins_per_word = 1;
-};
-
-template <int PACK>
-__device__ __forceinline__ void count_id(uint32_t* cnt, int lane, uint32_t id, uint32_t E,
-                                         uint32_t& dropped) {
-  if (id < E) {
-    atomicAdd(cnt + LaneCounters<PACK>::word((int)id, lane), LaneCounters<PACK>::inc((int)id));
-  } else {
-    ++dropped;
-  }
-}
-
-// one warp = one work unit = up to kHistStepsPerUnit consecutive steps of one layer
-template <typename IdT, int PACK>
-__global__ void __launch_bounds__(kHistWarps * 32)
-topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B, int E, int64_t T,
-                 int32_t* __restrict__ hist, int64_t* __restrict__ colsum, int32_t* __restrict__ active,
-                 int64_t* __restrict__ dropped_out) {
-  extern __shared__ uint32_t hsm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int words = (PACK == 2 ? (E + 1) / 2 : E);  // counter rows
-  uint32_t* cnt = hsm + (size_t)warp * words * 32;
-  for (int w = lane; w < words * 32; w += 32) cnt[w] = 0;
-  __syncwarp();
-
-  const int64_t units_per_layer = (T + kHistStepsPerUnit - 1) / kHistStepsPerUnit;
-  const int64_t total_units = L * units_per_layer;
-  const int64_t gwarp = (int64_t)blockIdx.x * kHistWarps + warp;
-  const int64_t nwarps = (int64_t)gridDim.x * kHistWarps;
-  const int rows_per_lane = (words + 31) / 32;
-
-  for (int64_t unit = gwarp; unit < total_units; unit += nwarps) {
-    const int64_t l = unit / units_per_layer;
-    const int64_t t_begin = (unit % units_per_layer) * kHistStepsPerUnit;
-    const int64_t t_end = imin64(t_begin + kHistStepsPerUnit, T);
-    uint32_t csum[kHistMaxPairsPerLane * 2];
-    uint32_t act[kHistMaxPairsPerLane * 2];
-#pragma unroll
-    for (int q = 0; q < kHistMaxPairsPerLane * 2; ++q) { csum[q] = 0; act[q] = 0; }
-    uint32_t dropped = 0;
-
-    for (int64_t t = t_begin; t < t_end; ++t) {
-      const int64_t tok0 = t * B;
-      const int64_t tok1 = imin64(tok0 + B, N);
-      const IdT* p = ids + (l * N + tok0) * k;
-      const int64_t cntn = (tok1 - tok0) * k;  // ids in this step
-      constexpr int per_vec = 16 / sizeof(IdT);
-      const bool vec_ok = ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
-      int64_t done = 0;
-      if (vec_ok) {
-        const int64_t nvec = cntn / per_vec;
-        const uint4* pv = reinterpret_cast<const uint4*>(p);
-        int64_t v = lane;
-        // 8 x 128-bit loads in flight per lane, then count
-        for (; v + 7 * 32 < nvec; v += 8 * 32) {
-          uint4 buf[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) buf[u] = __ldcs(pv + v + u * 32);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const uint32_t wv[4] = {buf[u].x, buf[u].y, buf[u].z, buf[u].w};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              if (sizeof(IdT) == 2) {
-                count_id<PACK>(cnt, lane, wv[c] & 0xffffu, (uint32_t)E, dropped);
-                count_id<PACK>(cnt, lane, wv[c] >> 16, (uint32_t)E, dropped);
-              } else {
-                count_id<PACK>(cnt, lane, wv[c], (uint32_t)E, dropped);
-              }
-            }
-          }
-        }
-        for (; v < nvec; v += 32) {
-          const uint4 b = __ldcs(pv + v);
-          const uint32_t wv[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            if (sizeof(IdT) == 2) {
-              count_id<PACK>(cnt, lane, wv[c] & 0xffffu, (uint32_t)E, dropped);
-              count_id<PACK>(cnt, lane, wv[c] >> 16, (uint32_t)E, dropped);
-            } else {
-              count_id<PACK>(cnt, lane, wv[c], (uint32_t)E, dropped);
-            }
-          }
-        }
-        done = nvec * per_vec;
-      }
-      for (int64_t i = done + lane; i < cntn; i += 32) {
-        const uint32_t id = (sizeof(IdT) == 2) ? (uint32_t)(uint16_t)p[i] : (uint32_t)p[i];
-        count_id<PACK>(cnt, lane, id, (uint32_t)E, dropped);
-      }
-      __syncwarp();
-      // reduce the 32 lane-private rows; lane owns rows lane, lane+32, ...
-      int32_t* hrow = hist + (l * T + t) * E;
-#pragma unroll
-      for (int q = 0; q < kHistMaxPairsPerLane; ++q) {
-        if (q >= rows_per_lane) break;
-        const int row = lane + q * 32;
-        if (row < words) {
-          uint32_t s = 0;
-#pragma unroll 8
-          for (int c = 0; c < 32; ++c) {
-            const uint32_t idx = (uint32_t)row * 32 + ((c + lane) & 31);
-            s += cnt[idx];
-            cnt[idx] = 0;
-          }
-          if (PACK == 2) {
-            const uint32_t lo = s & 0xffffu, hi = s >> 16;
-            const int b0 = row * 2;
-            hrow[b0] = (int32_t)lo;
-            if (b0 + 1 < E) hrow[b0 + 1] = (int32_t)hi;
-            csum[2 * q] += lo;
-            csum[2 * q + 1] += hi;
-            act[2 * q] += (lo > 0);
-            act[2 * q + 1] += (hi > 0);
-          } else {
-            hrow[row] = (int32_t)s;
-            csum[2 * q] += s;
-            act[2 * q] += (s > 0);
-          }
-        }
-      }
-      __syncwarp();
-    }
-    // flush this unit's per-expert totals
-#pragma unroll
-    for (int q = 0; q < kHistMaxPairsPerLane; ++q) {
-      if (q >= rows_per_lane) break;
-      const int row = lane + q * 32;
-      if (row < words) {
-        if (PACK == 2) {
-          const int b0 = row * 2;
-          if (csum[2 * q]) atomicAdd((unsigned long long*)&colsum[l * E + b0], (unsigned long long)csum[2 * q]);
-          if (act[2 * q]) atomicAdd(&active[l * E + b0], (int)act[2 * q]);
-          if (b0 + 1 < E) {
-            if (csum[2 * q + 1]) atomicAdd((unsigned long long*)&colsum[l * E + b0 + 1], (unsigned long long)csum[2 * q + 1]);
-            if (act[2 * q + 1]) atomicAdd(&active[l * E + b0 + 1], (int)act[2 * q + 1]);
-          }
-        } else {
-          if (csum[2 * q]) atomicAdd((unsigned long long*)&colsum[l * E + row], (unsigned long long)csum[2 * q]);
-          if (act[2 * q]) atomicAdd(&active[l * E + row], (int)act[2 * q]);
-        }
-      }
-    }
-    // dropped ids: warp-reduce then one atomic
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dropped += __shfl_xor_sync(0xffffffffu, dropped, o);
-    if (lane == 0 && dropped) atomicAdd((unsigned long long*)&dropped_out[l], (unsigned long long)dropped);
   }
 }
 
@@ -520,45 +346,6 @@ extern "C" int gem_gen_topk(int64_t L, int64_t N, int32_t k, int32_t B, int32_t 
                                                                     (int32_t*)ids);
   GEM_CHECK_LAUNCH("gen_topk_kernel");
   return GEM_OK;
-}
-
-template <typename IdT, int PACK>
-static int launch_hist(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int32_t* hist,
-                       int64_t* colsum, int32_t* active, int64_t* dropped, cudaStream_t st) {
-  const int words = PACK == 2 ? (E + 1) / 2 : E;
-  const size_t smem = (size_t)kHistWarps * words * 32 * sizeof(uint32_t);
-  auto kern = topk_hist_kernel<IdT, PACK>;
-  GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  GEM_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHistWarps * 32, smem));
-  if (per_sm < 1) per_sm = 1;
-  const int64_t units = L * ((T + kHistStepsPerUnit - 1) / kHistStepsPerUnit);
-  int64_t blocks = (int64_t)num_sms() * per_sm;
-  const int64_t need = (units + kHistWarps - 1) / kHistWarps;
-  if (blocks > need) blocks = need;
-  if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, kHistWarps * 32, smem, st>>>((const IdT*)ids, L, N, k, B, E, T, hist, colsum, active,
-                                                         dropped);
-  GEM_CHECK_LAUNCH("topk_hist_kernel");
-  return GEM_OK;
-}
-
-extern "C" int gem_topk_hist(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k, int32_t B,
-                             int32_t E, int32_t* hist, int64_t* colsum, int32_t* active, int64_t* dropped,
-                             void* stream) {
-  GEM_REQUIRE(id_bytes == 2 || id_bytes == 4, "gem_topk_hist: id_bytes must be 2 or 4");
-  GEM_REQUIRE(L >= 1 && N >= 1 && k >= 1 && B >= 1 && E >= 1 && E <= 512,
-              "gem_topk_hist: bad shape L=%lld N=%lld k=%d B=%d E=%d (E <= 512)", (long long)L, (long long)N, k, B,
-              E);
-  GEM_REQUIRE(ids && hist && colsum && active && dropped, "gem_topk_hist: null pointer");
-  const int64_t T = (N + B - 1) / B;
-  const bool pack2 = (int64_t)B * k <= 65535;  // a step's total fits a 16-bit lane counter sum
-  cudaStream_t st = as_stream(stream);
-  if (id_bytes == 2)
-    return pack2 ? launch_hist<int16_t, 2>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st)
-                 : launch_hist<int16_t, 1>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
-  return pack2 ? launch_hist<int32_t, 2>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st)
-               : launch_hist<int32_t, 1>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
 }
 
 extern "C" int gem_hist_colstats(const int32_t* hist, int64_t L, int64_t T, int32_t E, int64_t* colsum,
