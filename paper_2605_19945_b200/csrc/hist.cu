@@ -81,7 +81,7 @@ __device__ __forceinline__ void count_scalar(uint32_t* cnt_lane, uint32_t id, ui
 // One warp = one work unit = up to kHistStepsPerUnit consecutive steps of one
 // layer. MAXR = histogram rows owned per lane in the reduction (rows/32).
 template <typename IdT, bool WIDE, int MAXR>
-__global__ void __launch_bounds__(kHistWarps * 32)
+__global__ void __launch_bounds__(kHistWarps * 32, WIDE ? 3 : 2)
 topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B, int E, int64_t T,
                  int32_t* __restrict__ hist, int64_t* __restrict__ colsum, int32_t* __restrict__ active,
                  int64_t* __restrict__ dropped_out) {
@@ -111,7 +111,72 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
 #pragma unroll
     for (int q = 0; q < MAXR * BINS; ++q) { csum[q] = 0; act[q] = 0; }
     uint32_t dropped = 0;
+    bool t_end_done = false;
 
+    // ---- fast path (wide layout): the unit's ids are one contiguous block, so
+    // stream it in 4 KB warp batches with the next batch always in flight
+    // (also across step boundaries) and keep CUMULATIVE lane counters: the
+    // per-step reduction only reads, and hist = row sum - previous row sum.
+    const int64_t step_bytes = (int64_t)B * k * (int64_t)sizeof(IdT);
+    const IdT* ubase = ids + (l * N + t_begin * B) * k;
+    if (WIDE && step_bytes % (kHistUnroll * 32 * 16) == 0 && t_end * B <= N &&
+        (reinterpret_cast<uintptr_t>(ubase) & 15) == 0) {
+      const int bps = (int)(step_bytes / (kHistUnroll * 32 * 16));  // batches per step
+      const int64_t nb = (t_end - t_begin) * bps;
+      const uint4* pv = reinterpret_cast<const uint4*>(ubase) + lane;
+      uint32_t prev[MAXR];
+#pragma unroll
+      for (int q = 0; q < MAXR; ++q) prev[q] = 0;
+      uint4 cur[kHistUnroll], nxt[kHistUnroll];
+#pragma unroll
+      for (int u = 0; u < kHistUnroll; ++u) cur[u] = __ldcs(pv + u * 32);
+      int in_step = 0;
+      int64_t t = t_begin;
+      for (int64_t bt = 0; bt < nb; ++bt) {
+        if (bt + 1 < nb) {
+          const uint4* q = pv + (bt + 1) * (kHistUnroll * 32);
+#pragma unroll
+          for (int u = 0; u < kHistUnroll; ++u) nxt[u] = __ldcs(q + u * 32);
+        }
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; ++u) count_vec<IdT, WIDE>(cnt_lane, cur[u], uE, Epair);
+        if (++in_step == bps) {
+          in_step = 0;
+          __syncwarp();
+          int32_t* hrow = hist + (l * T + t) * E;
+#pragma unroll
+          for (int q = 0; q < MAXR; ++q) {
+            const int row = lane + q * 32;
+            if (row < hrows) {
+              const uint4* rp = reinterpret_cast<const uint4*>(cnt + row * 32);
+              uint32_t sum = 0;
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const uint4 v = rp[(c + lane) & 7];
+                sum += (v.x + v.y) + (v.z + v.w);
+              }
+              const uint32_t h = sum - prev[q];
+              prev[q] = sum;
+              hrow[row] = (int32_t)h;
+              act[q] += (h > 0);
+            }
+          }
+          __syncwarp();
+          ++t;
+        }
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; ++u) cur[u] = nxt[u];
+      }
+#pragma unroll
+      for (int q = 0; q < MAXR; ++q) csum[q] = prev[q];
+      // dropped ids of the whole unit sit in the overflow row; reset all counters
+      dropped += cnt[E * 32 + lane];
+      __syncwarp();
+      for (int w = lane; w < rows * 32; w += 32) cnt[w] = 0;
+      __syncwarp();
+      t_end_done = true;
+    }
+    if (!t_end_done)
     for (int64_t t = t_begin; t < t_end; ++t) {
       const int64_t tok0 = t * B;
       const int64_t tok1 = imin64(tok0 + B, N);
