@@ -320,14 +320,19 @@ def _cpu_layer(args):
     return float(st.mean_utilization[0])
 
 
+def _single_thread_env():
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"
+
+
 def cpu_stats_run(ids_np, B, E, cores):
-    """Reference statistics for every layer of ids_np [l, n, k] on `cores` processes -> seconds."""
+    """Reference statistics for every layer of ids_np [l, n, k], one process per layer -> seconds."""
     from concurrent.futures import ProcessPoolExecutor
 
     work = [(ids_np[l], B, E) for l in range(ids_np.shape[0])]
     s0 = time.perf_counter()
     if cores > 1:
-        with ProcessPoolExecutor(max_workers=cores) as ex:
+        with ProcessPoolExecutor(max_workers=cores, initializer=_single_thread_env) as ex:
             list(ex.map(_cpu_layer, work))
     else:
         for w in work:
@@ -336,15 +341,18 @@ def cpu_stats_run(ids_np, B, E, cores):
 
 
 def cpu_stats_baseline(spec, ids_dev):
-    """Bounded sample: `layers` full layers (all 2^24 tokens) of the same trace."""
-    cores = os.cpu_count() or 1
-    layers = min(spec.num_layers, max(2, min(cores, 8)))
-    ids_np = ids_dev[:layers].cpu().numpy()
-    secs = cpu_stats_run(ids_np, spec.tokens_per_step, spec.num_experts, min(cores, layers))
-    tokens_equiv = spec.num_tokens * layers / spec.num_layers
-    return {"value": tokens_equiv / secs, "unit": "tokens/s", "cores": min(cores, layers), "kind": "reference",
-            "sample": f"{layers} of {spec.num_layers} layers x {spec.num_tokens} tokens: np.bincount ingestion "
-                      f"(restatement) + reference gemap.compute_stats (oracle/_ref), {secs:.2f} s"}
+    """Bounded sample: `cores` layer-slices of 4096 steps (4M tokens) each, one process per core."""
+    cores = min(os.cpu_count() or 1, 16)
+    steps = min(spec.num_steps, 4096)
+    n = steps * spec.tokens_per_step
+    layers = min(spec.num_layers, cores)
+    ids_np = ids_dev[:layers, :n].cpu().numpy()
+    secs = cpu_stats_run(ids_np, spec.tokens_per_step, spec.num_experts, layers)
+    tokens_equiv = n * layers / spec.num_layers
+    return {"value": tokens_equiv / secs, "unit": "tokens/s", "cores": layers, "kind": "reference",
+            "sample": f"{layers} layers x {n} tokens ({steps} steps), one process per layer: np.bincount "
+                      f"ingestion (restatement; the reference has none) + reference gemap.compute_stats "
+                      f"(oracle/_ref Cython build), {secs:.2f} s"}
 
 
 def run_reference(args):
@@ -360,15 +368,16 @@ def run_reference(args):
         return
     L, N, k, E, B, G, C = CONFIGS[args.config]
     T = N // B
-    # the same synthetic ids, generated by the CPU twin of the device generator
-    from paper_2605_19945_b200.ingest import TopkTraceSpec, _prob_u32, planted_layout
-
-    spec = TopkTraceSpec(num_layers=L, num_tokens=N, top_k=k, num_experts=E, tokens_per_step=B, seed=0)
-    cores = os.cpu_count() or 1
-    layers = min(L, max(1, min(cores, 4)))
-    sample_tokens = min(N, 1 << 21)
-    w, r = planted_layout(spec)
-    ids = o.gen_topk(layers, sample_tokens, k, B, E, w[:layers], r[:layers], _prob_u32(0.85), _prob_u32(0.17), 3, 0)
+    # same-shape synthetic ids: Zipf(1.1)-popular experts, sampled with numpy (the
+    # CPU arm must not run our kernels, and the reference's cost does not depend
+    # on which ids are drawn, only on how many)
+    cores = min(os.cpu_count() or 1, 16)
+    layers = min(L, cores)
+    sample_tokens = min(N, 4096 * B)
+    rng = np.random.default_rng(0)
+    p = 1.0 / np.power(np.arange(1, E + 1), 1.1)
+    p /= p.sum()
+    ids = np.stack([rng.choice(E, size=(sample_tokens, k), p=p).astype(np.int16) for _ in range(layers)])
     for _ in range(args.warmup if args.warmup < 2 else 1):
         cpu_stats_run(ids[:, : B * 16], B, E, min(cores, layers))
     times = [cpu_stats_run(ids, B, E, min(cores, layers)) for _ in range(max(1, min(args.steps, 3)))]

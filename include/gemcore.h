@@ -152,6 +152,9 @@ int gem_score_batch(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_
                     const int8_t* cand, int64_t C, const double* lut, int64_t nmax,
                     double* layer_scores, double* total, int32_t* err_flag, void* stream);
 
+/* total[c] = serial-in-l sum of layer_scores[c][0..L) (cli.py:427 aggregate order) */
+int gem_layer_sum(const double* layer_scores, int64_t C, int64_t L, double* total, void* stream);
+
 /* replay of one layer under one mapping (mapping.py:169-198): per-step GPU
  * loads [T,G] (int64), latencies [T,G], step max, straggler (lowest index),
  * total (serial), busy time per GPU (serial), token totals per GPU. */

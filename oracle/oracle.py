@@ -270,6 +270,19 @@ def classify(tokens, cons=(4, 5), corr=(4, 5)):
     return cls, grp
 
 
+def classify_from_stats(colsum, active, gram, T, cons=(4, 5), corr=(4, 5)):
+    """Classification from (already reduced) integer statistics of one layer."""
+    colsum = np.ascontiguousarray(colsum, dtype=np.int64)
+    active = np.ascontiguousarray(active, dtype=np.int64)
+    gram = np.ascontiguousarray(gram, dtype=np.int64)
+    E = colsum.size
+    cls = np.zeros(E, dtype=np.int8)
+    grp = np.zeros(E, dtype=np.int16)
+    if lib().or_classify(colsum, active, gram, int(T), E, cons[0], cons[1], corr[0], corr[1], cls, grp):
+        raise OverflowError("oracle classify: statistics out of exact range")
+    return cls, grp
+
+
 def restart_order(mean_util, restart_index, rng, noise_fraction):
     keys = np.asarray(mean_util, dtype=np.float64)
     if restart_index > 0:

@@ -212,6 +212,14 @@ extern "C" int gem_score_batch(const int32_t* hist, int64_t L, int64_t T, int32_
   return GEM_OK;
 }
 
+extern "C" int gem_layer_sum(const double* layer_scores, int64_t C, int64_t L, double* total, void* stream) {
+  GEM_REQUIRE(layer_scores && total && C >= 0 && L >= 1, "gem_layer_sum: bad arguments");
+  if (C == 0) return GEM_OK;
+  layer_sum_kernel<<<grid_for(C, 256), 256, 0, as_stream(stream)>>>(layer_scores, C, L, total);
+  GEM_CHECK_LAUNCH("layer_sum_kernel");
+  return GEM_OK;
+}
+
 extern "C" int gem_replay(const int32_t* hist, int64_t T, int32_t E, int32_t G, const int8_t* assign,
                           const double* lut, int64_t nmax, int64_t* loads, double* lat, double* step_max,
                           int32_t* straggler, double* total, double* busy, int64_t* gpu_tokens, int32_t* err_flag,
