@@ -169,7 +169,7 @@ def run_ours(args):
         if timed:
             e1.record(stream)
             kev.append((e0, e1))
-        _lib.call("gem_step_gram", hist.data_ptr(), L, t1 - t0, E, gram.data_ptr(), stream.cuda_stream)
+        _lib.call("gem_step_gram", hist.data_ptr(), L, t1 - t0, E, B * k, gram.data_ptr(), stream.cuda_stream)
         if world > 1:
             for t in (colsum, active, gram):
                 dist.all_reduce(t)

@@ -111,9 +111,23 @@ int gem_hist_colstats(const int32_t* hist, int64_t L, int64_t T, int32_t E,
                       int64_t* colsum, int32_t* active, void* stream);
 
 /* --- K2: step-level co-activation Gram, gram[l][a][b] = sum_t h_a h_b -----
- * int64, exact (callers guarantee sum fits int64). ACCUMULATED. */
-int gem_step_gram(const int32_t* hist, int64_t L, int64_t T, int32_t E, int64_t* gram,
-                  void* stream);
+ * int64, exact (callers guarantee sum fits int64). ACCUMULATED; the upper
+ * triangle a <= b is authoritative (128x128 / 64x64 tiles straddling the
+ * diagonal also fill some a > b cells).
+ * max_count: an upper bound on every hist value that the caller guarantees
+ * (for ids: tokens_per_step * top_k), or -1 if unknown. With E a multiple of
+ * 128 (<= 512) and 0 <= max_count <= 65535 the tensor-core kernel runs
+ * (gem_step_gram_path() == 1: tcgen05 kind::i8 on two u8 limbs, s32 TMEM
+ * accumulators, int64 combine), otherwise the CUDA-core kernel (path 0).
+ * Both are exact and give identical results. */
+int gem_step_gram(const int32_t* hist, int64_t L, int64_t T, int32_t E, int64_t max_count,
+                  int64_t* gram, void* stream);
+int gem_step_gram_path(int32_t E, int64_t max_count);
+/* the two implementations, callable directly (tests, kernel benchmarks) */
+int gem_step_gram_cc(const int32_t* hist, int64_t L, int64_t T, int32_t E, int64_t* gram,
+                     void* stream);
+int gem_step_gram_tc(const int32_t* hist, int64_t L, int64_t T, int32_t E, int64_t* gram,
+                     void* stream);
 
 /* --- K3: statistics finalisation (trace.py:87-114) -------------------------
  * mean_util = colsum/total, active_frac = active/T (IEEE, bit-exact);

@@ -358,7 +358,7 @@ extern "C" int gem_hist_colstats(const int32_t* hist, int64_t L, int64_t T, int3
   return GEM_OK;
 }
 
-extern "C" int gem_step_gram(const int32_t* hist, int64_t L, int64_t T, int32_t E, int64_t* gram, void* stream) {
+extern "C" int gem_step_gram_cc(const int32_t* hist, int64_t L, int64_t T, int32_t E, int64_t* gram, void* stream) {
   GEM_REQUIRE(L >= 1 && T >= 1 && E >= 1 && hist && gram, "gem_step_gram: bad arguments");
   GEM_REQUIRE(L <= 65535, "gem_step_gram: L too large");
   const int tiles = (E + kGramTile - 1) / kGramTile;
@@ -373,6 +373,19 @@ extern "C" int gem_step_gram(const int32_t* hist, int64_t L, int64_t T, int32_t 
   step_gram_kernel<<<grid, 256, 0, as_stream(stream)>>>(hist, T, E, t_per, gram);
   GEM_CHECK_LAUNCH("step_gram_kernel");
   return GEM_OK;
+}
+
+// K2 dispatcher: the tcgen05 kernel (gram_tc.cu) whenever its preconditions
+// hold (E a multiple of 128 up to 512; every count in [0, 65535], which the
+// caller vouches for through max_count), the CUDA-core kernel otherwise.
+extern "C" int gem_step_gram_path(int32_t E, int64_t max_count) {
+  return (E >= 128 && E <= 512 && E % 128 == 0 && max_count >= 0 && max_count <= 65535) ? 1 : 0;
+}
+
+extern "C" int gem_step_gram(const int32_t* hist, int64_t L, int64_t T, int32_t E, int64_t max_count, int64_t* gram,
+                             void* stream) {
+  if (gem_step_gram_path(E, max_count) == 1) return gem_step_gram_tc(hist, L, T, E, gram, stream);
+  return gem_step_gram_cc(hist, L, T, E, gram, stream);
 }
 
 extern "C" int gem_stats_finalize(const int64_t* colsum, const int32_t* active, const int64_t* gram, int64_t L,

@@ -117,7 +117,7 @@ class ShardedStats:
 def sharded_statistics(ids_local, plan: ShardPlan, ops, tokens_per_step: int, num_experts: int,
                        group=None) -> ShardedStats:
     hist, colsum, active = ops.topk_hist(ids_local, tokens_per_step, num_experts)
-    gram = ops.gram(hist)
+    gram = ops.gram(hist, tokens_per_step * ids_local.shape[-1])  # every count <= B*k
     allreduce_stats(colsum, active, gram, group)
     fin = ops.finalize(colsum, active, gram, plan.num_steps)
     return ShardedStats(hist, colsum, active, gram, fin)
@@ -159,10 +159,10 @@ class DeviceOps:
         h = ids_to_histograms(ids_local, B, E, check_dropped=False)
         return h.hist, h.colsum, h.active
 
-    def gram(self, hist):
+    def gram(self, hist, max_count=-1):
         from .ingest import step_coactivation
 
-        return step_coactivation(hist)
+        return step_coactivation(hist, max_count=max_count)
 
     def finalize(self, colsum, active, gram, T):
         from .ingest import classify_device

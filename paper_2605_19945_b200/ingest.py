@@ -130,6 +130,12 @@ class Histograms:
     active: torch.Tensor    # [L, E] int32
     dropped: torch.Tensor   # [L] int64 ids outside [0, E)
     tokens_per_step: int
+    top_k: int = -1         # ids per token (bounds every count by tokens_per_step * top_k)
+
+    @property
+    def max_count(self) -> int:
+        """Upper bound on every histogram cell (-1 = unknown)."""
+        return self.tokens_per_step * self.top_k if self.top_k > 0 else -1
 
     @property
     def num_layers(self) -> int:
@@ -172,7 +178,7 @@ def ids_to_histograms(ids: torch.Tensor, tokens_per_step: int, num_experts: int,
     dropped = _device.zeros((L,), torch.int64)
     _lib.call("gem_topk_hist", ptr(ids), ids.element_size(), L, N, k, tokens_per_step, num_experts, ptr(hist),
               ptr(colsum), ptr(active), ptr(dropped), stream())
-    h = Histograms(hist, colsum, active, dropped, tokens_per_step)
+    h = Histograms(hist, colsum, active, dropped, tokens_per_step, k)
     if check_dropped and int(dropped.sum().item()):
         raise ValidationError(f"{int(dropped.sum().item())} expert ids outside [0, {num_experts})")
     return h
@@ -182,12 +188,15 @@ def ids_to_histograms(ids: torch.Tensor, tokens_per_step: int, num_experts: int,
 # K2 + K3: statistics, co-activation, classification
 
 
-def step_coactivation(hist: torch.Tensor, gram: torch.Tensor | None = None) -> torch.Tensor:
-    """K2: G[l,a,b] = sum_t hist[l,t,a] * hist[l,t,b] (int64; upper triangle a<=b written)."""
+def step_coactivation(hist: torch.Tensor, gram: torch.Tensor | None = None, max_count: int = -1) -> torch.Tensor:
+    """K2: G[l,a,b] = sum_t hist[l,t,a] * hist[l,t,b] (int64; upper triangle a<=b authoritative).
+
+    max_count bounds every count (-1 = unknown); with E % 128 == 0 and
+    max_count <= 65535 the Gram runs on the tensor cores (tcgen05 kind::i8)."""
     L, T, E = hist.shape
     if gram is None:
         gram = _device.zeros((L, E, E), torch.int64)
-    _lib.call("gem_step_gram", ptr(hist), L, T, E, ptr(gram), stream())
+    _lib.call("gem_step_gram", ptr(hist), L, T, E, max_count, ptr(gram), stream())
     return gram
 
 
@@ -246,7 +255,7 @@ def trace_statistics(ids: torch.Tensor, tokens_per_step: int, num_experts: int, 
 
 def statistics_from_histograms(h: Histograms, correlation: bool = True, classify: bool = True,
                                config: ClassifyConfig = ClassifyConfig()) -> TraceStatistics:
-    gram = step_coactivation(h.hist)
+    gram = step_coactivation(h.hist, max_count=h.max_count)
     ds = DeviceStats(h.colsum, h.active, gram, h.num_steps)
     mu, af, corr = finalize_stats(ds, with_corr=correlation)
     classes = classify_device(h.colsum, h.active, gram, h.num_steps, config) if classify else None

@@ -58,7 +58,7 @@ class OracleOps:
         h = torch.from_numpy(hist.astype(np.int32))
         return h, torch.from_numpy(hist.sum(axis=1)), torch.from_numpy((hist > 0).sum(axis=1).astype(np.int32))
 
-    def gram(self, hist):
+    def gram(self, hist, max_count=-1):
         return torch.from_numpy(np.stack([self.o.gram(h.numpy()) for h in hist]))
 
     def finalize(self, colsum, active, gram, T):

@@ -103,6 +103,55 @@ def test_stats_and_classes_match_oracle(oracle):
         assert np.array_equal(st.classes.group[l].cpu().numpy(), grp)
 
 
+def _gram_np(h: np.ndarray) -> np.ndarray:
+    """exact int64 X^T X (object arithmetic is not needed: |entries| < 2^62 here)."""
+    h = h.astype(np.int64)
+    return h.T @ h
+
+
+@pytest.mark.parametrize("shape", [(2, 300, 128, 1024), (1, 16384 + 77, 128, 65535), (3, 1000, 256, 4096),
+                                   (1, 129, 256, 65535), (2, 40000, 128, 2048)])
+def test_step_gram_tensor_cores_vs_cuda_cores(shape):
+    """K2: tcgen05 kind::i8 limb kernel == CUDA-core kernel == exact numpy, bit for bit
+    (ragged T, T > one 16384-step s32 segment, counts up to the 65535 limb limit, E=256 off-diagonal blocks)."""
+    from paper_2605_19945_b200 import _lib
+
+    L, T, E, hi = shape
+    rng = np.random.default_rng(T + E)
+    h = rng.integers(0, hi + 1, (L, T, E)).astype(np.int32)
+    h[:, ::7, :] = 0
+    h[0, 0, :] = hi
+    hd = torch.from_numpy(h).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    g_tc = torch.zeros((L, E, E), dtype=torch.int64, device="cuda")
+    g_cc = torch.zeros((L, E, E), dtype=torch.int64, device="cuda")
+    _lib.call("gem_step_gram_tc", hd.data_ptr(), L, T, E, g_tc.data_ptr(), st)
+    _lib.call("gem_step_gram_cc", hd.data_ptr(), L, T, E, g_cc.data_ptr(), st)
+    assert _lib.lib().gem_step_gram_path(E, hi) == 1
+    iu = np.triu_indices(E)
+    a, b = g_tc.cpu().numpy(), g_cc.cpu().numpy()
+    for l in range(L):
+        want = _gram_np(h[l])
+        assert np.array_equal(a[l][iu], want[iu])
+        assert np.array_equal(b[l][iu], want[iu])
+
+
+def test_step_gram_accumulates_and_dispatches():
+    from paper_2605_19945_b200 import _lib
+
+    rng = np.random.default_rng(1)
+    h = torch.from_numpy(rng.integers(0, 100, (1, 500, 128)).astype(np.int32)).cuda()
+    g = ingest.step_coactivation(h, max_count=100)
+    g = ingest.step_coactivation(h, gram=g, max_count=100)  # accumulates
+    want = 2 * _gram_np(h[0].cpu().numpy())
+    iu = np.triu_indices(128)
+    assert np.array_equal(g[0].cpu().numpy()[iu], want[iu])
+    assert _lib.lib().gem_step_gram_path(128, -1) == 0
+    assert _lib.lib().gem_step_gram_path(128, 65536) == 0
+    assert _lib.lib().gem_step_gram_path(64, 100) == 0
+    assert _lib.lib().gem_step_gram_path(256, 8192) == 1
+
+
 def test_planted_groups_recovered():
     spec = ingest.TopkTraceSpec(num_layers=2, num_tokens=400 * 1024, top_k=8, num_experts=128, seed=3)
     st = ingest.trace_statistics(ingest.generate_topk_ids(spec), 1024, 128)

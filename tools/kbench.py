@@ -64,9 +64,10 @@ def bench_gram(args):
     hist = torch.randint(0, 1024, (L, T, E), dtype=torch.int32, device="cuda")
     gram = torch.zeros((L, E, E), dtype=torch.int64, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
-    ms = timed(lambda: _lib.call("gem_step_gram", hist.data_ptr(), L, T, E, gram.data_ptr(), st), args.reps, args.warm)
     macs = L * T * E * E
-    print(json.dumps({"kernel": "step_gram", "ms": ms, "GMACps": macs / ms / 1e6, "hbm_GBps": L * T * E * 4 / ms / 1e6}))
+    for fn in ("gem_step_gram_cc", "gem_step_gram_tc"):
+        ms = timed(lambda: _lib.call(fn, hist.data_ptr(), L, T, E, gram.data_ptr(), st), args.reps, args.warm)
+        print(json.dumps({"kernel": fn, "ms": ms, "GMACps": macs / ms / 1e6, "hbm_GBps": L * T * E * 4 / ms / 1e6}))
 
 
 def bench_score(args):
