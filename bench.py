@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--search-steps", type=int, default=None, help="search window (default: all steps)")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the sharded (torch.distributed) code path even on one GPU")
     return ap.parse_args()
 
 
@@ -61,26 +63,71 @@ def parse():
 
 
 class Clocks:
-    def __init__(self, index: int):
+    """SM clock and throttle reasons sampled every 5 ms through NVML while the
+    timed region runs (nvidia-smi as a fallback when NVML is unavailable)."""
+
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+               "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
+
+    def __init__(self, index: int, period: float = 0.005):
         self.index = index
-        self.samples = []
+        self.period = period
+        self.samples = []  # (sm_mhz, reason bitmask)
+        self.max_mhz = None
+        self.source = None
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_handle(self):
+        """The NVML handle of torch's cuda:index, matched by UUID (NVML and CUDA orders can differ)."""
+        import pynvml
+
+        pynvml.nvmlInit()
+        try:
+            import torch
+
+            want = str(torch.cuda.get_device_properties(self.index).uuid)
+            for i in range(pynvml.nvmlDeviceGetCount()):
+                h = pynvml.nvmlDeviceGetHandleByIndex(i)
+                u = pynvml.nvmlDeviceGetUUID(h)
+                u = u.decode() if isinstance(u, bytes) else str(u)
+                if u.lower().removeprefix("gpu-") == want.lower():
+                    return pynvml, h
+        except Exception:
+            pass
+        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
     def __enter__(self):
-        def run():
+        try:
+            nv, h = self._nvml_handle()
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.source = "nvml"
+
+            def sample():
+                return (nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+        except Exception:
+            self.source = "nvidia-smi"
             q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+            def sample():
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip().split(",")
+                self.max_mhz = float(out[1])
+                mask = sum(1 << i for i in range(4) if out[2 + i].strip().lower() == "active")
+                return float(out[0]), ("smi", mask)
+
+        def run():
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
+                    self.samples.append(sample())
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(self.period)
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
@@ -93,13 +140,22 @@ class Clocks:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"]}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no clock samples"], "samples": 0}
+        sm = sorted(float(s[0]) for s in self.samples)
+        reasons = set()
+        if self.source == "nvml":
+            import pynvml
+
+            for _, mask in self.samples:
+                for name, attr in self.REASONS.items():
+                    if mask & getattr(pynvml, attr, 0):
+                        reasons.add(name)
+        else:
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for _, (_, mask) in self.samples:
+                reasons.update(names[i] for i in range(4) if mask >> i & 1)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(self.samples), "source": self.source}
 
 
 # ---------------------------------------------------------------------------
@@ -131,6 +187,7 @@ def run_ours(args):
 
     import paper_2605_19945_b200 as gem
     from paper_2605_19945_b200 import _device, _lib, ingest
+    from paper_2605_19945_b200 import dist as dist_mod
     from paper_2605_19945_b200 import mapping as gm
     from paper_2605_19945_b200.search import aggregate_score, search_hist
     from paper_2605_19945_b200.trace import DeviceStats, finalize_stats
@@ -139,8 +196,11 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    use_dist = world > 1 or args.force_dist
+    if use_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
     L, N, k, E, B, G, C = CONFIGS[args.config]
     if args.candidates:
         C = args.candidates
@@ -170,7 +230,7 @@ def run_ours(args):
             e1.record(stream)
             kev.append((e0, e1))
         _lib.call("gem_step_gram", hist.data_ptr(), L, t1 - t0, E, B * k, gram.data_ptr(), stream.cuda_stream)
-        if world > 1:
+        if use_dist:
             for t in (colsum, active, gram):
                 dist.all_reduce(t)
         ds = DeviceStats(colsum, active, gram, T)
@@ -181,7 +241,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         stats_step(False)
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -192,7 +252,7 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
+    if use_dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -219,8 +279,12 @@ def run_ours(args):
                           "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": k1_ms,
                           "kernel_share_of_step": k1_ms / ms, "peak_source": peak_src}
 
-    # ---- e2e through the public API with host (pinned) ids
-    if not args.no_e2e and world == 1:
+    plan = dist_mod.ShardPlan(world, rank, L, T)
+    ops = dist_mod.DeviceOps()
+
+    # ---- e2e through the public API with host (pinned) ids: every step copies
+    #      this rank's id shard host->device and reads the per-expert results back
+    if not args.no_e2e:
         host_ids = torch.empty(ids.shape, dtype=ids.dtype, pin_memory=True)
         host_ids.copy_(ids)
         dev_ids = torch.empty_like(ids)
@@ -228,65 +292,112 @@ def run_ours(args):
 
         def e2e_step():
             dev_ids.copy_(host_ids, non_blocking=True)
-            st = ingest.trace_statistics(dev_ids, B, E)
-            res = (st.mean_utilization.to("cpu", non_blocking=True), st.classes.cls.to("cpu", non_blocking=True))
+            if use_dist:
+                ss = dist_mod.sharded_statistics(dev_ids, plan, ops, B, E)
+                mu, cls = ss.finalized[0], ss.finalized[3]
+            else:
+                st = ingest.trace_statistics(dev_ids, B, E)
+                mu, cls = st.mean_utilization, st.classes.cls
+            res = (mu.to("cpu", non_blocking=True), cls.to("cpu", non_blocking=True))
             torch.cuda.current_stream().synchronize()
             return res
 
         e2e_step()
         reps = max(1, min(3, args.steps))
-        s0 = time.perf_counter()
+        torch.cuda.synchronize()
+        if use_dist:
+            dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
         for _ in range(reps):
             e2e_step()
-        e2e_s = (time.perf_counter() - s0) / reps
+        a1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = torch.tensor([a0.elapsed_time(a1) / reps], device="cuda")
+        if use_dist:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e_s = float(e2e_ms.item()) / 1e3
         result["e2e"] = {"value": N / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(ids.numel() * 2),
                          "d2h_bytes_per_step": int(L * E * 8 + L * E), "ms_per_step": e2e_s * 1e3,
-                         "path": "ingest.trace_statistics(ids from pinned host memory)"}
+                         "bytes_are": "per rank" if use_dist else "whole job",
+                         "path": ("dist.sharded_statistics" if use_dist else "ingest.trace_statistics")
+                         + "(ids copied from pinned host memory every step)"}
         del host_ids, dev_ids
 
-    # ---- candidate mappings/s (C candidates x all layers, full trace)
-    if not args.no_candidates and world == 1:
-        profile = gem.generate_profile(gem.VariabilitySetupSpec(num_gpus=G, setup="moderate", tile_size=64,
-                                                                max_tokens=B * k, rng_seed=0))
+    # ---- candidate mappings/s (C candidates x all layers, full trace) and
+    #      time-to-mapping (stats + GEM-Place search of every layer, full trace).
+    #      Multi-GPU: histogram rows go to the layer owners (one all-to-all),
+    #      layers are searched / scored where they live, results all-gathered.
+    profile = gem.generate_profile(gem.VariabilitySetupSpec(num_gpus=G, setup="moderate", tile_size=64,
+                                                            max_tokens=B * k, rng_seed=0))
+
+    def owned_hist():
+        return dist_mod.exchange_hist(hist, plan) if use_dist else hist
+
+    def dev_time(fn):
+        """CUDA-event time of fn() on this rank, max over ranks (ms)."""
+        torch.cuda.synchronize()
+        if use_dist:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        out = fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b)], device="cuda")
+        if use_dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return out, float(t.item())
+
+    if not args.no_candidates:
         rng = np.random.default_rng(0)
         base = np.repeat(np.arange(G, dtype=np.int8), E // G)
-        cand = np.empty((C, L, E), dtype=np.int8)
-        for c in range(C):
-            cand[c] = np.stack([rng.permutation(base) for _ in range(L)])
-        cand_d = torch.from_numpy(cand).cuda()
+        cand = rng.permuted(np.broadcast_to(base, (C * L, E)), axis=1).reshape(C, L, E)
+        cand_d = torch.from_numpy(np.ascontiguousarray(cand)).cuda()
+        hist_own = owned_hist()
         nmax = B * k
-        layer_scores = torch.empty((C, L), dtype=torch.float64, device="cuda")
-        gm.score_candidates_device(hist, nmax, profile, cand_d[:64].contiguous(), layer_scores[:64])
-        torch.cuda.synchronize()
-        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        c0.record()
-        total, _ = gm.score_candidates_device(hist, nmax, profile, cand_d, layer_scores)
-        c1.record()
-        torch.cuda.synchronize()
-        cms = c0.elapsed_time(c1)
+        l0, l1 = plan.layer_range()
+
+        def score_all():
+            if use_dist:
+                return dist_mod.sharded_candidate_scores(hist_own, plan, ops, profile, cand_d, nmax)
+            return gm.score_candidates_device(hist_own, nmax, profile, cand_d)
+
+        score_all()  # warm-up (LUT build, module load)
+        (total, _), cms = dev_time(score_all)
         best = int(torch.argmin(total).item())
         result["candidates"] = {"value": C / (cms / 1e3), "unit": "candidate mappings/s", "ms": cms,
                                 "candidates": C, "layers": L, "steps": T, "best_index": best,
-                                "best_score": float(total[best].item())}
-        del cand_d, layer_scores
+                                "best_score": float(total[best].item()),
+                                "sharding": f"layers {l0}..{l1 - 1} on this rank of {world}" if use_dist
+                                else "single GPU"}
+        del cand_d
 
-    # ---- time-to-mapping: stats + search of every layer (full trace)
-    if not args.no_search and world == 1:
-        profile = gem.generate_profile(gem.VariabilitySetupSpec(num_gpus=G, setup="moderate", tile_size=64,
-                                                                max_tokens=B * k, rng_seed=0))
+    if not args.no_search:
         cfg = gem.SearchConfig(rng_seed=0)
         Tw = args.search_steps or T
-        hwin = hist[:, :Tw].contiguous()
-        torch.cuda.synchronize()
-        s0 = time.perf_counter()
-        mu, af, corr, cls = stats_step(False)
-        results = search_hist(hwin, B * k, profile, cfg, mean_util=None if Tw != T else mu.cpu().numpy())
-        torch.cuda.synchronize()
-        ttm = time.perf_counter() - s0
-        swaps = [r.swap_count for res in results for r in res.per_restart]
-        result["time_to_mapping"] = {"value": ttm, "unit": "s", "steps_searched": Tw, "runs": len(swaps),
-                                     "swaps_median": float(np.median(swaps)), "swaps_max": int(max(swaps)),
-                                     "aggregate_score": aggregate_score(results)}
+
+        def ttm():
+            st = stats_step(False)
+            h = owned_hist()
+            if Tw != T:
+                h = h[:, :Tw].contiguous()
+            if use_dist:
+                return dist_mod.sharded_search(h, plan, ops, profile, cfg, B * k), None
+            mu = st[0].cpu().numpy() if Tw == T else None
+            return None, search_hist(h, B * k, profile, cfg, mean_util=mu)
+
+        (shm, results), tms = dev_time(ttm)
+        info = {"value": tms / 1e3, "unit": "s", "steps_searched": Tw, "layers": L,
+                "runs_per_layer": cfg.restarts + 2, "timing": "CUDA events on the launching stream, max over ranks",
+                "includes": "K1..K3b statistics, all-to-all to layer owners (N>1), greedy + refinement of every run"}
+        if results is not None:
+            swaps = [r.swap_count for res in results for r in res.per_restart]
+            info.update({"runs": len(swaps), "swaps_median": float(np.median(swaps)), "swaps_max": int(max(swaps)),
+                         "aggregate_score": aggregate_score(results)})
+        else:
+            info["aggregate_score"] = shm.aggregate
+        result["time_to_mapping"] = info
 
     if not args.no_cpu and world == 1 and rank == 0:
         try:
@@ -295,7 +406,7 @@ def run_ours(args):
             result["cpu_baseline"] = {"error": repr(exc)}
     if rank == 0:
         print(json.dumps(result), flush=True)
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
 

@@ -36,8 +36,22 @@ struct SearchWs {
   int32_t* run_i;      // [R]
   int32_t* run_j;      // [R]
   int32_t* run_active; // [R]
-  int32_t* counters;   // [4]: active count, mismatch, range
+  int32_t* run_list;   // [R] compacted indices of the active runs
+  int32_t* counters;   // [4]: active count, mismatch, range, list length
+  // screened scan (K6 v3)
+  double* loc_min;     // [R][NP] approximate minimum of each (run, GPU pair) tile
+  int32_t* loc_cnt;    // [R][NP] pairs inside the tile's window (may exceed kLocK)
+  double* loc_cand;    // [R][NP][kLocK]
+  int32_t* loc_flat;   // [R][NP][kLocK]
+  int32_t* cand_flat;  // [R][kCandK] pairs to evaluate exactly
+  int32_t* cand_n;     // [R]
+  int32_t* need_exact; // [R] window overflow -> exact full scan of the run
+  double* cand_exact;  // [R][kCandK]
+  const float* lut32;  // [G][nmax+1] fp32 rounding of the latency table (set by the driver)
 };
+
+constexpr int kLocK = 8;
+constexpr int kCandK = 32;
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -56,7 +70,17 @@ static size_t carve(SearchWs* ws, void* base, int64_t R, int64_t T, int G) {
   w.run_i = (int32_t*)take((size_t)R * 4);
   w.run_j = (int32_t*)take((size_t)R * 4);
   w.run_active = (int32_t*)take((size_t)R * 4);
+  w.run_list = (int32_t*)take((size_t)R * 4);
   w.counters = (int32_t*)take(16);
+  w.loc_min = (double*)take((size_t)R * NP * 8);
+  w.loc_cnt = (int32_t*)take((size_t)R * NP * 4);
+  w.loc_cand = (double*)take((size_t)R * NP * kLocK * 8);
+  w.loc_flat = (int32_t*)take((size_t)R * NP * kLocK * 4);
+  w.cand_flat = (int32_t*)take((size_t)R * kCandK * 4);
+  w.cand_n = (int32_t*)take((size_t)R * 4);
+  w.need_exact = (int32_t*)take((size_t)R * 4);
+  w.cand_exact = (double*)take((size_t)R * kCandK * 8);
+  w.lut32 = nullptr;
   if (ws) *ws = w;
   return off;
 }
@@ -206,10 +230,10 @@ init_score_kernel(int64_t T, int G, const double* __restrict__ lut, int64_t nmax
 __global__ void __launch_bounds__(kSearchThreads)
 best_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, const double* __restrict__ lut,
                  int64_t nmax, const int32_t* __restrict__ run_layer, const int8_t* __restrict__ assign,
-                 SearchWs ws) {
+                 SearchWs ws, const int32_t* __restrict__ filter) {
   extern __shared__ unsigned char bsm[];
   const int64_t r = blockIdx.x;
-  if (!ws.run_active[r]) return;
+  if (!ws.run_active[r] || (filter && !filter[r])) return;
   const int NP = G * (G - 1) / 2;
   // pair index -> (a, b), a < b
   int p = blockIdx.y, a = 0;
@@ -321,10 +345,325 @@ best_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, cons
   }
 }
 
-__global__ void reduce_pairs_kernel(int64_t R, int G, int E, SearchWs ws) {
+
+// ---------------------------------------------------------------------------
+// K6 v3: screened best-swap scan.
+//
+// The reference picks the pair with the smallest EXACT serial-fp64 candidate
+// score (lowest i*E+j on ties). Evaluating every pair exactly is bound by the
+// two latency-table gathers per pair-step; the fp64 table rows of two GPUs do
+// not fit shared memory next to the staging buffers, and from L1 a random
+// gather costs a wavefront per line. So the scan runs in two passes:
+//
+//  1. approximate pass (this kernel): the fp32 rounding of the table rows a
+//     and b lives in shared memory (2 x (nmax+1) x 4 B); each pair-step is
+//     m' = max(po', C'_a, C'_b) in fp32 (rounding is monotone, so m' is
+//     exactly fl32(m)) accumulated serially in fp64. Then
+//     |cand' - cand| <= 2^-24 cand + 2 T 2^-53 cand < 2^-22 cand, and the
+//     exact winner satisfies cand'(win) <= min' * (1+2^-22)/(1-2^-22)
+//     < min' * (1 + 2^-20) =: window. Every CTA keeps the pairs inside ITS
+//     window (a superset of the ones inside the run's window);
+//  2. the pairs inside the run's window (usually one or two) are evaluated
+//     exactly, exactly as v1 does, and the lexicographic (cand, flat) minimum
+//     is taken. A run whose window holds more than kCandK pairs (or a tile
+//     that overflowed kLocK) falls back to the exact v1 scan.
+// The selected pair and its score are therefore the reference's, bit for bit.
+//
+// CTA = (GPU pair a<b, RPC active runs). Every run places exactly n = E/G
+// experts on each GPU, so a (run, pair) tile has n*n expert pairs; a thread
+// owns one x (on a) and kSwapY consecutive y (on b): kSwapY independent
+// chains. Per t-chunk the CTA stages po' (max of the other GPUs' latencies),
+// l_a, l_b and the counts of the a- and b-experts for each of its runs.
+constexpr int kSwapY = 4;
+constexpr int kSwap3Threads = 256;
+constexpr int kSwap3TChunk = 64;
+constexpr double kWindow = 1.0 + 1.0 / 1048576.0;  // 1 + 2^-20
+
+struct Swap3Geom {
+  int n, ng, units_per_run, rpc;
+};
+
+__host__ __device__ inline Swap3Geom swap3_geom(int E, int G) {
+  Swap3Geom g;
+  g.n = E / G;
+  g.ng = (g.n + kSwapY - 1) / kSwapY;
+  g.units_per_run = g.n * g.ng;
+  g.rpc = kSwap3Threads / g.units_per_run;
+  if (g.rpc < 1) g.rpc = 1;
+  if (g.rpc > 16) g.rpc = 16;
+  return g;
+}
+
+__host__ __device__ inline size_t swap3_smem(int E, int G, int64_t nmax) {
+  const Swap3Geom g = swap3_geom(E, G);
+  const size_t lut = ((size_t)2 * (size_t)(nmax + 1) * 4 + 15) & ~size_t(15);
+  const size_t per_run_chunk = (size_t)kSwap3TChunk * (4 + 4 + 4 + 4 * (size_t)g.n + 4 * (size_t)g.ng * kSwapY);
+  return lut + (size_t)g.rpc * per_run_chunk + (size_t)g.rpc * (8 + 2 * g.n * 2) + 64;
+}
+
+__device__ __forceinline__ unsigned long long ord_bits(double v) {  // monotone for v >= 0 (and +inf)
+  return (unsigned long long)__double_as_longlong(v);
+}
+
+__global__ void __launch_bounds__(kSwap3Threads, 2)
+approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, int64_t nmax,
+                   const int32_t* __restrict__ run_layer, const int8_t* __restrict__ assign, int32_t n_active,
+                   SearchWs ws) {
+  extern __shared__ __align__(16) unsigned char s3[];
+  const Swap3Geom geo = swap3_geom(E, G);
+  const int n = geo.n, ng = geo.ng, RPC = geo.rpc;
+  const int NP = G * (G - 1) / 2;
+  const int slot0 = blockIdx.y * RPC;
+  if (slot0 >= n_active) return;
+  const int nruns = min(RPC, n_active - slot0);
+  int p = blockIdx.x, a = 0;
+  while (p >= G - 1 - a) { p -= G - 1 - a; ++a; }
+  const int b = a + 1 + p;
+  const int64_t width = nmax + 1;
+  const int nb_pad = ng * kSwapY;
+
+  float* lut_a = reinterpret_cast<float*>(s3);
+  float* lut_b = lut_a + width;
+  unsigned char* cur = s3 + (((size_t)2 * width * 4 + 15) & ~size_t(15));
+  int32_t* hA = reinterpret_cast<int32_t*>(cur);   cur += (size_t)RPC * kSwap3TChunk * n * 4;
+  int32_t* hB = reinterpret_cast<int32_t*>(cur);   cur += (size_t)RPC * kSwap3TChunk * nb_pad * 4;
+  float* po = reinterpret_cast<float*>(cur);       cur += (size_t)RPC * kSwap3TChunk * 4;
+  int32_t* la = reinterpret_cast<int32_t*>(cur);   cur += (size_t)RPC * kSwap3TChunk * 4;
+  int32_t* lb = reinterpret_cast<int32_t*>(cur);   cur += (size_t)RPC * kSwap3TChunk * 4;
+  unsigned long long* smin = reinterpret_cast<unsigned long long*>(cur);  cur += (size_t)RPC * 8;
+  int16_t* lists = reinterpret_cast<int16_t*>(cur);  // [RPC][2][n]
+
+  const int tid = threadIdx.x;
+  const float* la32 = ws.lut32 + (int64_t)a * width;
+  const float* lb32 = ws.lut32 + (int64_t)b * width;
+  for (int64_t i = tid; i < width; i += blockDim.x) {
+    lut_a[i] = __ldg(la32 + i);
+    lut_b[i] = __ldg(lb32 + i);
+  }
+  if (tid < RPC) smin[tid] = ord_bits(__longlong_as_double(0x7ff0000000000000LL));
+  // expert lists of the CTA's runs (ascending expert index on each GPU)
+  for (int w = tid >> 5; w < nruns; w += blockDim.x >> 5) {
+    const int lane = tid & 31;
+    const int r = ws.run_list[slot0 + w];
+    const int8_t* as = assign + (int64_t)r * E;
+    int base_a = 0, base_b = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      const int g = e < E ? as[e] : -1;
+      const unsigned ma = __ballot_sync(0xffffffffu, g == a), mb = __ballot_sync(0xffffffffu, g == b);
+      const unsigned below = (1u << lane) - 1u;
+      if (g == a) lists[(w * 2 + 0) * n + base_a + __popc(ma & below)] = (int16_t)e;
+      if (g == b) lists[(w * 2 + 1) * n + base_b + __popc(mb & below)] = (int16_t)e;
+      base_a += __popc(ma);
+      base_b += __popc(mb);
+    }
+  }
+  __syncthreads();
+
+  const int units_total = nruns * geo.units_per_run;
+  for (int pass0 = 0; pass0 < units_total; pass0 += blockDim.x) {
+    const int u = pass0 + tid;
+    const bool live = u < units_total;
+    const int s = live ? u / geo.units_per_run : 0;
+    const int ur = live ? u % geo.units_per_run : 0;
+    const int x = ur / ng, yg = ur % ng;
+    double acc[kSwapY];
+#pragma unroll
+    for (int q = 0; q < kSwapY; ++q) acc[q] = 0.0;
+
+    for (int64_t t0 = 0; t0 < T; t0 += kSwap3TChunk) {
+      const int tn = (int)imin64(kSwap3TChunk, T - t0);
+      __syncthreads();
+      for (int i = tid; i < nruns * tn; i += blockDim.x) {
+        const int ss = i / tn, tt = i % tn;
+        const int r = ws.run_list[slot0 + ss];
+        const int32_t* lrow = ws.loads + ((int64_t)r * T + t0 + tt) * G;
+        float m = __int_as_float(0xff800000);  // -inf when G == 2
+        for (int g = 0; g < G; ++g) {
+          if (g == a || g == b) continue;
+          const float v = __ldg(ws.lut32 + g * width + lrow[g]);
+          m = fmaxf(m, v);
+        }
+        po[ss * kSwap3TChunk + tt] = m;
+        la[ss * kSwap3TChunk + tt] = lrow[a];
+        lb[ss * kSwap3TChunk + tt] = lrow[b];
+      }
+      const int row_items = n + nb_pad;
+      for (int i = tid; i < nruns * tn * row_items; i += blockDim.x) {
+        const int ss = i / (tn * row_items);
+        const int rem = i % (tn * row_items);
+        const int tt = rem / row_items, c = rem % row_items;
+        const int r = ws.run_list[slot0 + ss];
+        const int32_t* hrow = hist + ((int64_t)run_layer[r] * T + t0 + tt) * E;
+        if (c < n) {
+          hA[(ss * kSwap3TChunk + tt) * n + c] = __ldg(hrow + lists[(ss * 2 + 0) * n + c]);
+        } else {
+          const int y = c - n;
+          hB[(ss * kSwap3TChunk + tt) * nb_pad + y] = y < n ? __ldg(hrow + lists[(ss * 2 + 1) * n + y]) : 0;
+        }
+      }
+      __syncthreads();
+      if (live) {
+        const float* pos = po + s * kSwap3TChunk;
+        const int32_t* las = la + s * kSwap3TChunk;
+        const int32_t* lbs = lb + s * kSwap3TChunk;
+        const int32_t* hAs = hA + (size_t)s * kSwap3TChunk * n + x;
+        const int32_t* hBs = hB + (size_t)s * kSwap3TChunk * nb_pad + yg * kSwapY;
+#pragma unroll 4
+        for (int tt = 0; tt < tn; ++tt) {
+          const int32_t hx = hAs[tt * n];
+          const int32_t ra = las[tt] - hx, rb = lbs[tt] + hx;
+          const float pm = pos[tt];
+          const int4 hy = *reinterpret_cast<const int4*>(hBs + tt * nb_pad);
+          const int32_t hys[4] = {hy.x, hy.y, hy.z, hy.w};
+#pragma unroll
+          for (int q = 0; q < kSwapY; ++q) {
+            const float m = fmaxf(fmaxf(pm, lut_a[ra + hys[q]]), lut_b[rb - hys[q]]);
+            acc[q] = dadd(acc[q], (double)m);
+          }
+        }
+      }
+    }
+    // tile minimum, then every pair inside the tile's window is recorded
+    if (live) {
+      double mn = acc[0];
+#pragma unroll
+      for (int q = 1; q < kSwapY; ++q)
+        if (yg * kSwapY + q < n) mn = fmin(mn, acc[q]);
+      atomicMin(&smin[s], ord_bits(mn));
+    }
+    __syncthreads();
+    if (live) {
+      const int r = ws.run_list[slot0 + s];
+      const int64_t tile = (int64_t)r * NP + blockIdx.x;
+      const double lim = __longlong_as_double((long long)smin[s]) * kWindow;
+      const int xe = lists[(s * 2 + 0) * n + x];
+#pragma unroll
+      for (int q = 0; q < kSwapY; ++q) {
+        const int yi = yg * kSwapY + q;
+        if (yi >= n || !(acc[q] <= lim)) continue;
+        const int ye = lists[(s * 2 + 1) * n + yi];
+        const int f = xe < ye ? xe * E + ye : ye * E + xe;
+        const int k = atomicAdd(&ws.loc_cnt[tile], 1);
+        if (k < kLocK) {
+          ws.loc_cand[tile * kLocK + k] = acc[q];
+          ws.loc_flat[tile * kLocK + k] = f;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < nruns) {
+    const int r = ws.run_list[slot0 + tid];
+    ws.loc_min[(int64_t)r * NP + blockIdx.x] = __longlong_as_double((long long)smin[tid]);
+  }
+}
+
+// per active run: the run's window over all GPU-pair tiles -> exact-candidate list
+__global__ void window_kernel(int32_t n_active, int G, SearchWs ws) {
+  const int NP = G * (G - 1) / 2;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_active; i += gridDim.x * blockDim.x) {
+    const int r = ws.run_list[i];
+    double gmin = __longlong_as_double(0x7ff0000000000000LL);
+    for (int p = 0; p < NP; ++p) gmin = fmin(gmin, ws.loc_min[(int64_t)r * NP + p]);
+    const double lim = gmin * kWindow;
+    int cnt = 0, overflow = 0;
+    for (int p = 0; p < NP; ++p) {
+      const int64_t tile = (int64_t)r * NP + p;
+      if (!(ws.loc_min[tile] <= lim)) continue;
+      const int c = ws.loc_cnt[tile];
+      if (c > kLocK) { overflow = 1; continue; }
+      for (int k = 0; k < c; ++k) {
+        if (!(ws.loc_cand[tile * kLocK + k] <= lim)) continue;
+        if (cnt < kCandK) ws.cand_flat[(int64_t)r * kCandK + cnt] = ws.loc_flat[tile * kLocK + k];
+        ++cnt;
+      }
+    }
+    if (cnt > kCandK) overflow = 1;
+    ws.cand_n[r] = overflow ? 0 : cnt;
+    ws.need_exact[r] = overflow;
+  }
+}
+
+// exact candidate score of one (run, expert pair): one warp, lanes evaluate 32
+// steps in parallel, the fp64 sum is one serial chain in t order (v1's terms).
+__global__ void exact_pairs_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G,
+                                   const double* __restrict__ lut, int64_t nmax,
+                                   const int32_t* __restrict__ run_layer, const int8_t* __restrict__ assign,
+                                   int32_t n_active, SearchWs ws) {
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int slot = warp_global / kCandK, k = warp_global % kCandK;
+  if (slot >= n_active) return;
+  const int r = ws.run_list[slot];
+  if (ws.need_exact[r] || k >= ws.cand_n[r]) return;
+  const int f = ws.cand_flat[(int64_t)r * kCandK + k];
+  const int i = f / E, j = f % E;
+  const int a = assign[(int64_t)r * E + i], b = assign[(int64_t)r * E + j];
+  const int64_t width = nmax + 1;
+  const int32_t* h = hist + (int64_t)run_layer[r] * T * E;
+  const int32_t* ld = ws.loads + (int64_t)r * T * G;
+  double sum = 0.0;
+  for (int64_t t0 = 0; t0 < T; t0 += 32) {
+    const int64_t t = t0 + lane;
+    double m = 0.0;
+    if (t < T) {
+      const int32_t* lrow = ld + t * G;
+      double po = __longlong_as_double(0xfff0000000000000LL);
+      for (int g = 0; g < G; ++g) {
+        if (g == a || g == b) continue;
+        const double v = __ldg(lut + g * width + lrow[g]);
+        po = v > po ? v : po;
+      }
+      const int32_t hi = h[t * E + i], hj = h[t * E + j];
+      const double va = __ldg(lut + a * width + (lrow[a] - hi + hj));
+      const double vb = __ldg(lut + b * width + (lrow[b] - hj + hi));
+      m = po;
+      m = va > m ? va : m;
+      m = vb > m ? vb : m;
+    }
+    const int tn = (int)imin64(32, T - t0);
+    for (int q = 0; q < tn; ++q) sum = dadd(sum, __shfl_sync(0xffffffffu, m, q));
+  }
+  if (lane == 0) ws.cand_exact[(int64_t)r * kCandK + k] = sum;
+}
+
+// per active run without overflow: lexicographic (exact cand, flat) minimum
+__global__ void select_pairs_kernel(int32_t n_active, int E, SearchWs ws) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_active; s += gridDim.x * blockDim.x) {
+    const int r = ws.run_list[s];
+    if (ws.need_exact[r]) continue;
+    double bc = __longlong_as_double(0x7ff0000000000000LL);
+    int bf = 0x7fffffff;
+    for (int k = 0; k < ws.cand_n[r]; ++k) {
+      const double c = ws.cand_exact[(int64_t)r * kCandK + k];
+      const int f = ws.cand_flat[(int64_t)r * kCandK + k];
+      if (c < bc || (c == bc && f < bf)) { bc = c; bf = f; }
+    }
+    const bool found = bf != 0x7fffffff;
+    ws.run_found[r] = found;
+    ws.run_i[r] = found ? bf / E : -1;
+    ws.run_j[r] = found ? bf % E : -1;
+    ws.run_cand[r] = bc;
+  }
+}
+
+// fp64 latency table -> its fp32 rounding (round to nearest: monotone)
+__global__ void lut_to_f32_kernel(const double* __restrict__ lut, int64_t n, float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __double2float_rn(lut[i]);
+}
+
+// compact the indices of active runs (order is irrelevant: runs are independent)
+__global__ void compact_runs_kernel(int64_t R, SearchWs ws) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x)
+    if (ws.run_active[r]) ws.run_list[atomicAdd(&ws.counters[3], 1)] = (int32_t)r;
+}
+
+__global__ void reduce_pairs_kernel(int64_t R, int G, int E, SearchWs ws, const int32_t* __restrict__ filter) {
   const int NP = G * (G - 1) / 2;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
-    if (!ws.run_active[r]) continue;
+    if (!ws.run_active[r] || (filter && !filter[r])) continue;
     double bc = __longlong_as_double(0x7ff0000000000000LL);
     int bf = 0x7fffffff;
     for (int p = 0; p < NP; ++p) {
@@ -416,18 +755,71 @@ static int check_search_args(const int32_t* hist, int64_t L, int64_t T, int32_t 
   return GEM_OK;
 }
 
-static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, const double* lut, int64_t nmax,
-                       int64_t R, const int32_t* run_layer, const int8_t* assign, const SearchWs& ws,
-                       cudaStream_t st) {
-  const int NP = G * (G - 1) / 2;
-  if (NP == 0) return GEM_OK;
+static int launch_exact_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, const double* lut, int64_t nmax,
+                             int64_t R, const int32_t* run_layer, const int8_t* assign, const SearchWs& ws,
+                             const int32_t* filter, cudaStream_t st) {
   const size_t smem = swap_smem(E);
   GEM_CHECK_CUDA(cudaFuncSetAttribute(best_swap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)R, (unsigned)NP);
-  best_swap_kernel<<<grid, kSearchThreads, smem, st>>>(hist, T, E, G, lut, nmax, run_layer, assign, ws);
+  dim3 grid((unsigned)R, (unsigned)(G * (G - 1) / 2));
+  best_swap_kernel<<<grid, kSearchThreads, smem, st>>>(hist, T, E, G, lut, nmax, run_layer, assign, ws, filter);
   GEM_CHECK_LAUNCH("best_swap_kernel");
-  reduce_pairs_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(R, G, E, ws);
+  reduce_pairs_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(R, G, E, ws, filter);
   GEM_CHECK_LAUNCH("reduce_pairs_kernel");
+  return GEM_OK;
+}
+
+// One best-swap scan over the active runs: screened (v3) when the two fp32
+// table rows fit shared memory, else the exact v1 scan for every active run.
+static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, const double* lut, int64_t nmax,
+                       int64_t R, int64_t n_active, const int32_t* run_layer, const int8_t* assign,
+                       const SearchWs& ws, cudaStream_t st) {
+  const int NP = G * (G - 1) / 2;
+  if (NP == 0 || n_active <= 0) return GEM_OK;
+  const size_t smem3 = swap3_smem(E, G, nmax);
+  int dev = 0, optin = 0;
+  GEM_CHECK_CUDA(cudaGetDevice(&dev));
+  GEM_CHECK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (ws.lut32 == nullptr || smem3 > (size_t)optin) {
+    return launch_exact_scan(hist, T, E, G, lut, nmax, R, run_layer, assign, ws, nullptr, st);
+  }
+  GEM_CHECK_CUDA(cudaMemsetAsync(ws.counters + 3, 0, 4, st));
+  compact_runs_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(R, ws);
+  GEM_CHECK_LAUNCH("compact_runs_kernel");
+  GEM_CHECK_CUDA(cudaMemsetAsync(ws.loc_cnt, 0, (size_t)R * NP * 4, st));
+  GEM_CHECK_CUDA(cudaFuncSetAttribute(approx_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  const Swap3Geom g = swap3_geom(E, G);
+  dim3 grid((unsigned)NP, (unsigned)((n_active + g.rpc - 1) / g.rpc));
+  approx_scan_kernel<<<grid, kSwap3Threads, smem3, st>>>(hist, T, E, G, nmax, run_layer, assign, (int32_t)n_active,
+                                                         ws);
+  GEM_CHECK_LAUNCH("approx_scan_kernel");
+  window_kernel<<<(unsigned)((n_active + 127) / 128), 128, 0, st>>>((int32_t)n_active, G, ws);
+  GEM_CHECK_LAUNCH("window_kernel");
+  const int64_t warps = n_active * kCandK;
+  exact_pairs_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(hist, T, E, G, lut, nmax, run_layer,
+                                                                           assign, (int32_t)n_active, ws);
+  GEM_CHECK_LAUNCH("exact_pairs_kernel");
+  select_pairs_kernel<<<(unsigned)((n_active + 127) / 128), 128, 0, st>>>((int32_t)n_active, E, ws);
+  GEM_CHECK_LAUNCH("select_pairs_kernel");
+  // runs whose window overflowed: the exact scan (CTAs of other runs exit at once)
+  return launch_exact_scan(hist, T, E, G, lut, nmax, R, run_layer, assign, ws, ws.need_exact, st);
+}
+
+// fp32 table for the screened scan, stream-ordered allocation freed on every exit path
+struct Lut32Guard {
+  float* p = nullptr;
+  cudaStream_t st = nullptr;
+  ~Lut32Guard() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+static int make_lut32(const double* lut, int G, int64_t nmax, Lut32Guard& g, SearchWs& ws, cudaStream_t st) {
+  const int64_t n = (int64_t)G * (nmax + 1);
+  g.st = st;
+  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g.p), (size_t)n * sizeof(float), st));
+  lut_to_f32_kernel<<<(unsigned)imin64((n + 255) / 256, 4096), 256, 0, st>>>(lut, n, g.p);
+  GEM_CHECK_LAUNCH("lut_to_f32_kernel");
+  ws.lut32 = g.p;
   return GEM_OK;
 }
 
@@ -443,6 +835,8 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
   cudaStream_t st = as_stream(stream);
   SearchWs ws;
   carve(&ws, workspace, R, T, G);
+  Lut32Guard lut32;
+  if (G >= 2 && (rc = make_lut32(lut, G, nmax, lut32, ws, st))) return rc;
   GEM_CHECK_CUDA(cudaMemsetAsync(ws.counters, 0, 16, st));
   const size_t gsmem = (size_t)G * kGreedyTChunk * sizeof(double);
   GEM_CHECK_CUDA(cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
@@ -458,8 +852,9 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
   }
   init_score_kernel<<<(unsigned)R, kSearchThreads, 0, st>>>(T, G, lut, nmax, ws, traj_cap, trajectory, swaps);
   GEM_CHECK_LAUNCH("init_score_kernel");
+  int64_t n_active = R;  // every run is active before its first scan
   for (int64_t it = 0; it < swap_cap; ++it) {
-    rc = launch_scan(hist, T, E, G, lut, nmax, R, run_layer, assign, ws, st);
+    rc = launch_scan(hist, T, E, G, lut, nmax, R, n_active, run_layer, assign, ws, st);
     if (rc) return rc;
     if (G < 2) break;  // no cross-GPU pair exists: found == false for every run
     GEM_CHECK_CUDA(cudaMemsetAsync(ws.counters, 0, 4, st));
@@ -470,6 +865,7 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
     GEM_CHECK_CUDA(cudaMemcpyAsync(&active, ws.counters, 4, cudaMemcpyDeviceToHost, st));
     GEM_CHECK_CUDA(cudaStreamSynchronize(st));
     if (active == 0) break;
+    n_active = active;
   }
   final_copy_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(R, ws, final_score);
   GEM_CHECK_LAUNCH("final_copy_kernel");
@@ -493,6 +889,8 @@ extern "C" int gem_best_swap_runs(const int32_t* hist, int64_t L, int64_t T, int
   cudaStream_t st = as_stream(stream);
   SearchWs ws;
   carve(&ws, workspace, R, T, G);
+  Lut32Guard lut32;
+  if (G >= 2 && (rc = make_lut32(lut, G, nmax, lut32, ws, st))) return rc;
   int64_t bx = (T * G + 255) / 256;
   if (bx > 64) bx = 64;
   init_loads_kernel<<<dim3((unsigned)bx, (unsigned)R), 256, E, st>>>(hist, T, E, G, run_layer, nullptr, assign,
@@ -501,7 +899,7 @@ extern "C" int gem_best_swap_runs(const int32_t* hist, int64_t L, int64_t T, int
   std::vector<int32_t> ones(R, 1);
   GEM_CHECK_CUDA(cudaMemcpyAsync(ws.run_active, ones.data(), R * 4, cudaMemcpyHostToDevice, st));
   if (G >= 2) {
-    rc = launch_scan(hist, T, E, G, lut, nmax, R, run_layer, assign, ws, st);
+    rc = launch_scan(hist, T, E, G, lut, nmax, R, R, run_layer, assign, ws, st);
     if (rc) return rc;
     GEM_CHECK_CUDA(cudaMemcpyAsync(found, ws.run_found, R * 4, cudaMemcpyDeviceToDevice, st));
     GEM_CHECK_CUDA(cudaMemcpyAsync(best_i, ws.run_i, R * 4, cudaMemcpyDeviceToDevice, st));

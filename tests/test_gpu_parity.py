@@ -263,10 +263,13 @@ def test_search_golden():
         assert init.assignment.tolist() == case["initial_1"]
 
 
-@pytest.mark.parametrize("G,E,T", [(2, 8, 16), (4, 16, 40), (8, 64, 128), (3, 12, 1), (8, 8, 30)])
-def test_search_matches_oracle(oracle, G, E, T):
+@pytest.mark.parametrize("G,E,T,high", [(2, 8, 16, 300), (4, 16, 40, 300), (8, 64, 128, 300), (3, 12, 1, 300),
+                                        (8, 8, 30, 300), (2, 128, 12, 300), (32, 256, 6, 40), (4, 16, 20, 4000)])
+def test_search_matches_oracle(oracle, G, E, T, high):
+    """Covers the shared-memory swap scan (one pass, multi-pass with 64x64 expert pairs per GPU pair,
+    16 runs per CTA at G=32) and the L1 fallback (step totals > 11k: the two table rows exceed smem)."""
     rng = np.random.default_rng(G * 1000 + E + T)
-    tok = random_counts(rng, T, E, high=300)
+    tok = random_counts(rng, T, E, high=high)
     p = mixed_profile(gem, rng, G) if E < 64 else staircase_profile(gem, rng, G, tile=64, tiles=256)
     res = gem.search(gem.ExpertTrace(tok), p, gem.SearchConfig(restarts=5, rng_seed=E))
     want = oracle.search(tok, oracle.Curves.from_profile(p), restarts=5, rng_seed=E)
