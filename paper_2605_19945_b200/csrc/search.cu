@@ -47,6 +47,7 @@ struct SearchWs {
   int32_t* cand_n;     // [R]
   int32_t* need_exact; // [R] window overflow -> exact full scan of the run
   double* cand_exact;  // [R][kCandK]
+  float* lat32;        // [R][T][G] fp32 latencies of the current loads (screened scan only)
   const float* lut32;  // [G][nmax+1] fp32 rounding of the latency table (set by the driver)
 };
 
@@ -80,6 +81,7 @@ static size_t carve(SearchWs* ws, void* base, int64_t R, int64_t T, int G) {
   w.cand_n = (int32_t*)take((size_t)R * 4);
   w.need_exact = (int32_t*)take((size_t)R * 4);
   w.cand_exact = (double*)take((size_t)R * kCandK * 8);
+  w.lat32 = (float*)take((size_t)R * T * G * 4);
   w.lut32 = nullptr;
   if (ws) *ws = w;
   return off;
@@ -376,17 +378,19 @@ best_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, cons
 // l_a, l_b and the counts of the a- and b-experts for each of its runs.
 constexpr int kSwapY = 4;
 constexpr int kSwap3Threads = 256;
-constexpr int kSwap3TChunk = 64;
+constexpr int kSwap3TChunk = 32;
 constexpr double kWindow = 1.0 + 1.0 / 1048576.0;  // 1 + 2^-20
 
 struct Swap3Geom {
-  int n, ng, units_per_run, rpc;
+  int n, ng, nb_pad, row_items, units_per_run, rpc;
 };
 
 __host__ __device__ inline Swap3Geom swap3_geom(int E, int G) {
   Swap3Geom g;
   g.n = E / G;
   g.ng = (g.n + kSwapY - 1) / kSwapY;
+  g.nb_pad = g.ng * kSwapY;
+  g.row_items = g.n + g.nb_pad;
   g.units_per_run = g.n * g.ng;
   g.rpc = kSwap3Threads / g.units_per_run;
   if (g.rpc < 1) g.rpc = 1;
@@ -394,16 +398,30 @@ __host__ __device__ inline Swap3Geom swap3_geom(int E, int G) {
   return g;
 }
 
+// one staging buffer (per run, per step of a chunk): counts of the a- and
+// b-experts, the fp32 latency row, l_a, l_b and the derived pother'
+__host__ __device__ inline size_t swap3_buf_bytes(const Swap3Geom& g, int G) {
+  return (size_t)g.rpc * kSwap3TChunk * (4 * (size_t)g.row_items + 4 * (size_t)G + 4 + 4 + 4);
+}
+
 __host__ __device__ inline size_t swap3_smem(int E, int G, int64_t nmax) {
   const Swap3Geom g = swap3_geom(E, G);
   const size_t lut = ((size_t)2 * (size_t)(nmax + 1) * 4 + 15) & ~size_t(15);
-  const size_t per_run_chunk = (size_t)kSwap3TChunk * (4 + 4 + 4 + 4 * (size_t)g.n + 4 * (size_t)g.ng * kSwapY);
-  return lut + (size_t)g.rpc * per_run_chunk + (size_t)g.rpc * (8 + 2 * g.n * 2) + 64;
+  const size_t fixed = (size_t)g.rpc * (8 + 8 + 8 + 2 * g.n * 2 + 2 * g.row_items) + 64;
+  return lut + 2 * swap3_buf_bytes(g, G) + fixed;
 }
 
 __device__ __forceinline__ unsigned long long ord_bits(double v) {  // monotone for v >= 0 (and +inf)
   return (unsigned long long)__double_as_longlong(v);
 }
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 __global__ void __launch_bounds__(kSwap3Threads, 2)
 approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, int64_t nmax,
@@ -411,7 +429,7 @@ approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, in
                    SearchWs ws) {
   extern __shared__ __align__(16) unsigned char s3[];
   const Swap3Geom geo = swap3_geom(E, G);
-  const int n = geo.n, ng = geo.ng, RPC = geo.rpc;
+  const int n = geo.n, ng = geo.ng, RPC = geo.rpc, nb_pad = geo.nb_pad, row_items = geo.row_items;
   const int NP = G * (G - 1) / 2;
   const int slot0 = blockIdx.y * RPC;
   if (slot0 >= n_active) return;
@@ -420,30 +438,55 @@ approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, in
   while (p >= G - 1 - a) { p -= G - 1 - a; ++a; }
   const int b = a + 1 + p;
   const int64_t width = nmax + 1;
-  const int nb_pad = ng * kSwapY;
+  constexpr int TC = kSwap3TChunk;
 
+  // ---- carve: table rows | 2 staging buffers | per-run constants
   float* lut_a = reinterpret_cast<float*>(s3);
   float* lut_b = lut_a + width;
   unsigned char* cur = s3 + (((size_t)2 * width * 4 + 15) & ~size_t(15));
-  int32_t* hA = reinterpret_cast<int32_t*>(cur);   cur += (size_t)RPC * kSwap3TChunk * n * 4;
-  int32_t* hB = reinterpret_cast<int32_t*>(cur);   cur += (size_t)RPC * kSwap3TChunk * nb_pad * 4;
-  float* po = reinterpret_cast<float*>(cur);       cur += (size_t)RPC * kSwap3TChunk * 4;
-  int32_t* la = reinterpret_cast<int32_t*>(cur);   cur += (size_t)RPC * kSwap3TChunk * 4;
-  int32_t* lb = reinterpret_cast<int32_t*>(cur);   cur += (size_t)RPC * kSwap3TChunk * 4;
+  const size_t buf_bytes = swap3_buf_bytes(geo, G);
+  unsigned char* bufs = cur;
+  cur += 2 * buf_bytes;
   unsigned long long* smin = reinterpret_cast<unsigned long long*>(cur);  cur += (size_t)RPC * 8;
-  int16_t* lists = reinterpret_cast<int16_t*>(cur);  // [RPC][2][n]
+  int64_t* rowoff = reinterpret_cast<int64_t*>(cur);  cur += (size_t)RPC * 8;   // r * T
+  int64_t* histoff = reinterpret_cast<int64_t*>(cur); cur += (size_t)RPC * 8;   // layer * T * E
+  int16_t* colidx = reinterpret_cast<int16_t*>(cur);  cur += (size_t)RPC * row_items * 2;
+  int16_t* lists = reinterpret_cast<int16_t*>(cur);   // [RPC][2][n]
+  struct Buf {
+    int32_t* h;    // [RPC][TC][row_items]: a-experts then b-experts (zero padded)
+    float* lat;    // [RPC][TC][G]
+    int32_t* la;   // [RPC][TC]
+    int32_t* lb;   // [RPC][TC]
+    float* po;     // [RPC][TC]
+  };
+  auto buf_at = [&](int k) {
+    unsigned char* c = bufs + k * buf_bytes;
+    Buf B;
+    B.h = reinterpret_cast<int32_t*>(c);  c += (size_t)RPC * TC * row_items * 4;
+    B.lat = reinterpret_cast<float*>(c);  c += (size_t)RPC * TC * G * 4;
+    B.la = reinterpret_cast<int32_t*>(c); c += (size_t)RPC * TC * 4;
+    B.lb = reinterpret_cast<int32_t*>(c); c += (size_t)RPC * TC * 4;
+    B.po = reinterpret_cast<float*>(c);
+    return B;
+  };
 
-  const int tid = threadIdx.x;
-  const float* la32 = ws.lut32 + (int64_t)a * width;
-  const float* lb32 = ws.lut32 + (int64_t)b * width;
-  for (int64_t i = tid; i < width; i += blockDim.x) {
-    lut_a[i] = __ldg(la32 + i);
-    lut_b[i] = __ldg(lb32 + i);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  {
+    const float* la32 = ws.lut32 + (int64_t)a * width;
+    const float* lb32 = ws.lut32 + (int64_t)b * width;
+    for (int64_t i = tid; i < width; i += blockDim.x) {
+      lut_a[i] = __ldg(la32 + i);
+      lut_b[i] = __ldg(lb32 + i);
+    }
   }
   if (tid < RPC) smin[tid] = ord_bits(__longlong_as_double(0x7ff0000000000000LL));
+  if (tid < nruns) {
+    const int r = ws.run_list[slot0 + tid];
+    rowoff[tid] = (int64_t)r * T;
+    histoff[tid] = (int64_t)run_layer[r] * T * E;
+  }
   // expert lists of the CTA's runs (ascending expert index on each GPU)
-  for (int w = tid >> 5; w < nruns; w += blockDim.x >> 5) {
-    const int lane = tid & 31;
+  for (int w = wid; w < nruns; w += nw) {
     const int r = ws.run_list[slot0 + w];
     const int8_t* as = assign + (int64_t)r * E;
     int base_a = 0, base_b = 0;
@@ -459,6 +502,37 @@ approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, in
     }
   }
   __syncthreads();
+  for (int i = tid; i < nruns * row_items; i += blockDim.x) {
+    const int ss = i / row_items, c = i % row_items;
+    colidx[i] = c < n ? lists[(ss * 2 + 0) * n + c] : (c - n < n ? lists[(ss * 2 + 1) * n + (c - n)] : (int16_t)-1);
+  }
+  __syncthreads();
+
+  // issue the asynchronous copies of one t-chunk into buffer k
+  auto issue = [&](int64_t t0, int k) {
+    const Buf B = buf_at(k);
+    const int tn = (int)imin64(TC, T - t0);
+    const int rows = nruns * tn;
+    for (int rr = wid; rr < rows; rr += nw) {
+      const int ss = rr / tn, tt = rr - ss * tn;
+      const int32_t* hrow = hist + histoff[ss] + (t0 + tt) * E;
+      for (int c = lane; c < row_items; c += 32) {
+        const int e = colidx[ss * row_items + c];
+        cp_async4(B.h + (ss * TC + tt) * row_items + c, hrow + (e >= 0 ? e : 0), e >= 0);
+      }
+    }
+    for (int i = tid; i < rows * G; i += blockDim.x) {
+      const int rr = i / G, g = i - rr * G;
+      const int ss = rr / tn, tt = rr - ss * tn;
+      cp_async4(B.lat + (ss * TC + tt) * G + g, ws.lat32 + (rowoff[ss] + t0 + tt) * G + g, true);
+    }
+    for (int rr = tid; rr < rows; rr += blockDim.x) {
+      const int ss = rr / tn, tt = rr - ss * tn;
+      const int32_t* lrow = ws.loads + (rowoff[ss] + t0 + tt) * G;
+      cp_async4(B.la + ss * TC + tt, lrow + a, true);
+      cp_async4(B.lb + ss * TC + tt, lrow + b, true);
+    }
+  };
 
   const int units_total = nruns * geo.units_per_run;
   for (int pass0 = 0; pass0 < units_total; pass0 += blockDim.x) {
@@ -471,58 +545,46 @@ approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, in
 #pragma unroll
     for (int q = 0; q < kSwapY; ++q) acc[q] = 0.0;
 
-    for (int64_t t0 = 0; t0 < T; t0 += kSwap3TChunk) {
-      const int tn = (int)imin64(kSwap3TChunk, T - t0);
+    issue(0, 0);
+    cp_async_commit();
+    int k = 0;
+    for (int64_t t0 = 0; t0 < T; t0 += TC, k ^= 1) {
+      const int tn = (int)imin64(TC, T - t0);
+      if (t0 + TC < T) issue(t0 + TC, k ^ 1);
+      cp_async_commit();  // (possibly empty) group of the next chunk
+      cp_async_wait1();   // this chunk's group has landed
       __syncthreads();
-      for (int i = tid; i < nruns * tn; i += blockDim.x) {
-        const int ss = i / tn, tt = i % tn;
-        const int r = ws.run_list[slot0 + ss];
-        const int32_t* lrow = ws.loads + ((int64_t)r * T + t0 + tt) * G;
+      const Buf B = buf_at(k);
+      for (int rr = tid; rr < nruns * TC; rr += blockDim.x) {
+        const int ss = rr / TC, tt = rr % TC;  // TC is a power of two
+        if (tt >= tn) continue;
+        const float* lat = B.lat + (ss * TC + tt) * G;
         float m = __int_as_float(0xff800000);  // -inf when G == 2
-        for (int g = 0; g < G; ++g) {
-          if (g == a || g == b) continue;
-          const float v = __ldg(ws.lut32 + g * width + lrow[g]);
-          m = fmaxf(m, v);
-        }
-        po[ss * kSwap3TChunk + tt] = m;
-        la[ss * kSwap3TChunk + tt] = lrow[a];
-        lb[ss * kSwap3TChunk + tt] = lrow[b];
-      }
-      const int row_items = n + nb_pad;
-      for (int i = tid; i < nruns * tn * row_items; i += blockDim.x) {
-        const int ss = i / (tn * row_items);
-        const int rem = i % (tn * row_items);
-        const int tt = rem / row_items, c = rem % row_items;
-        const int r = ws.run_list[slot0 + ss];
-        const int32_t* hrow = hist + ((int64_t)run_layer[r] * T + t0 + tt) * E;
-        if (c < n) {
-          hA[(ss * kSwap3TChunk + tt) * n + c] = __ldg(hrow + lists[(ss * 2 + 0) * n + c]);
-        } else {
-          const int y = c - n;
-          hB[(ss * kSwap3TChunk + tt) * nb_pad + y] = y < n ? __ldg(hrow + lists[(ss * 2 + 1) * n + y]) : 0;
-        }
+        for (int g = 0; g < G; ++g)
+          if (g != a && g != b) m = fmaxf(m, lat[g]);
+        B.po[ss * TC + tt] = m;
       }
       __syncthreads();
       if (live) {
-        const float* pos = po + s * kSwap3TChunk;
-        const int32_t* las = la + s * kSwap3TChunk;
-        const int32_t* lbs = lb + s * kSwap3TChunk;
-        const int32_t* hAs = hA + (size_t)s * kSwap3TChunk * n + x;
-        const int32_t* hBs = hB + (size_t)s * kSwap3TChunk * nb_pad + yg * kSwapY;
+        const float* pos = B.po + s * TC;
+        const int32_t* las = B.la + s * TC;
+        const int32_t* lbs = B.lb + s * TC;
+        const int32_t* hAs = B.h + (size_t)s * TC * row_items + x;
+        const int32_t* hBs = B.h + (size_t)s * TC * row_items + n + yg * kSwapY;
 #pragma unroll 4
         for (int tt = 0; tt < tn; ++tt) {
-          const int32_t hx = hAs[tt * n];
+          const int32_t hx = hAs[tt * row_items];
           const int32_t ra = las[tt] - hx, rb = lbs[tt] + hx;
           const float pm = pos[tt];
-          const int4 hy = *reinterpret_cast<const int4*>(hBs + tt * nb_pad);
-          const int32_t hys[4] = {hy.x, hy.y, hy.z, hy.w};
+          const int32_t* hy = hBs + tt * row_items;
 #pragma unroll
           for (int q = 0; q < kSwapY; ++q) {
-            const float m = fmaxf(fmaxf(pm, lut_a[ra + hys[q]]), lut_b[rb - hys[q]]);
+            const float m = fmaxf(fmaxf(pm, lut_a[ra + hy[q]]), lut_b[rb - hy[q]]);
             acc[q] = dadd(acc[q], (double)m);
           }
         }
       }
+      __syncthreads();  // buffer k is rewritten by the issue of the chunk after next
     }
     // tile minimum, then every pair inside the tile's window is recorded
     if (live) {
@@ -544,10 +606,10 @@ approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, in
         if (yi >= n || !(acc[q] <= lim)) continue;
         const int ye = lists[(s * 2 + 1) * n + yi];
         const int f = xe < ye ? xe * E + ye : ye * E + xe;
-        const int k = atomicAdd(&ws.loc_cnt[tile], 1);
-        if (k < kLocK) {
-          ws.loc_cand[tile * kLocK + k] = acc[q];
-          ws.loc_flat[tile * kLocK + k] = f;
+        const int kk = atomicAdd(&ws.loc_cnt[tile], 1);
+        if (kk < kLocK) {
+          ws.loc_cand[tile * kLocK + kk] = acc[q];
+          ws.loc_flat[tile * kLocK + kk] = f;
         }
       }
     }
@@ -648,6 +710,12 @@ __global__ void select_pairs_kernel(int32_t n_active, int E, SearchWs ws) {
   }
 }
 
+// fp32 latency matrix of the current loads for every run (screened scan)
+__global__ void lat32_fill_kernel(int64_t n, int G, int64_t width, SearchWs ws) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    ws.lat32[i] = ws.lut32[(int64_t)(i % G) * width + ws.loads[i]];
+}
+
 // fp64 latency table -> its fp32 rounding (round to nearest: monotone)
 __global__ void lut_to_f32_kernel(const double* __restrict__ lut, int64_t n, float* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -703,10 +771,17 @@ apply_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, con
   const int a = assign[r * E + i], b = assign[r * E + j];
   const int32_t* h = hist + (int64_t)run_layer[r] * T * E;
   int32_t* ld = ws.loads + r * T * G;
+  float* l32 = ws.lut32 ? ws.lat32 + r * T * G : nullptr;
+  const int64_t width = nmax + 1;
   for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
     const int32_t d = h[t * E + j] - h[t * E + i];
-    ld[t * G + a] += d;
-    ld[t * G + b] -= d;
+    const int32_t na = ld[t * G + a] + d, nb = ld[t * G + b] - d;
+    ld[t * G + a] = na;
+    ld[t * G + b] = nb;
+    if (l32) {
+      l32[t * G + a] = ws.lut32[a * width + na];
+      l32[t * G + b] = ws.lut32[b * width + nb];
+    }
   }
   __syncthreads();
   const double s = block_score(ld, T, G, lut, nmax + 1, buf);
@@ -852,6 +927,10 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
   }
   init_score_kernel<<<(unsigned)R, kSearchThreads, 0, st>>>(T, G, lut, nmax, ws, traj_cap, trajectory, swaps);
   GEM_CHECK_LAUNCH("init_score_kernel");
+  if (ws.lut32) {
+    lat32_fill_kernel<<<4 * num_sms(), 256, 0, st>>>(R * T * G, G, nmax + 1, ws);
+    GEM_CHECK_LAUNCH("lat32_fill_kernel");
+  }
   int64_t n_active = R;  // every run is active before its first scan
   for (int64_t it = 0; it < swap_cap; ++it) {
     rc = launch_scan(hist, T, E, G, lut, nmax, R, n_active, run_layer, assign, ws, st);
@@ -896,6 +975,10 @@ extern "C" int gem_best_swap_runs(const int32_t* hist, int64_t L, int64_t T, int
   init_loads_kernel<<<dim3((unsigned)bx, (unsigned)R), 256, E, st>>>(hist, T, E, G, run_layer, nullptr, assign,
                                                                      ws.loads);
   GEM_CHECK_LAUNCH("init_loads_kernel");
+  if (ws.lut32) {
+    lat32_fill_kernel<<<4 * num_sms(), 256, 0, st>>>(R * T * G, G, nmax + 1, ws);
+    GEM_CHECK_LAUNCH("lat32_fill_kernel");
+  }
   std::vector<int32_t> ones(R, 1);
   GEM_CHECK_CUDA(cudaMemcpyAsync(ws.run_active, ones.data(), R * 4, cudaMemcpyHostToDevice, st));
   if (G >= 2) {
