@@ -25,6 +25,8 @@ constexpr int kSearchThreads = 256;
 constexpr int kGreedyTChunk = 256;
 constexpr int kSwapTChunk = 64;
 constexpr int kSwapPairsPerThread = 4;
+// screening window: exact winners satisfy approx <= min(approx) * (1 + 2^-20) (see K6 v3 / K7 v2)
+constexpr double kWindow = 1.0 + 1.0 / 1048576.0;
 
 struct SearchWs {
   int32_t* loads;      // [R][T][G]
@@ -165,6 +167,218 @@ greedy_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, const d
     if (tid == 0) assign[r * E + e] = (int8_t)bg;
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------------------
+// K7 v2: screened greedy placement.
+//
+// Greedy (search.py:142-163) places the experts of a run one at a time on the
+// GPU with the smallest exact serial-fp64 score sum_t max(others, C_g(l_g+h)),
+// lowest GPU on ties. v1 pays two L1 table gathers per (t, GPU) and a serial
+// chain per GPU. v2 keeps the fp32 rounding of the table window [0, U] in
+// shared memory (U = max over steps of the sum of the n = E/G largest counts:
+// no GPU load, before or after a placement, can exceed it) and scores every
+// candidate GPU approximately: terms fl32(max(..)) summed in fp64 in ANY
+// order (per-thread partials + tree), so |S' - S| <= (2^-24 + T 2^-52) S and
+// the exact winner lies inside S' <= min' (1 + 2^-20). One GPU in the window
+// decides; otherwise the window's GPUs are scored exactly (v1's serial chain
+// in t order) and the strict-< / lowest-index rule picks among them.
+constexpr int kG2Threads = 512;
+
+// U[l] = max_t (sum of the n largest counts of step t): one warp per step row
+__global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, int64_t T, int E, int n,
+                                  int32_t* __restrict__ bound) {
+  extern __shared__ int32_t tb_rows[];  // [warps][E]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int32_t* row = tb_rows + (size_t)w * E;
+  const int64_t rows = L * T;
+  for (int64_t rr = (int64_t)blockIdx.x * nw + w; rr < rows; rr += (int64_t)gridDim.x * nw) {
+    const int32_t* h = hist + rr * E;
+    for (int e = lane; e < E; e += 32) row[e] = h[e];
+    __syncwarp();
+    int64_t sum = 0;
+    for (int k = 0; k < n; ++k) {
+      int best = -1, bi = -1;
+      for (int e = lane; e < E; e += 32)
+        if (row[e] > best) { best = row[e]; bi = e; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const int ob = __shfl_xor_sync(0xffffffffu, best, o), oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      sum += best;
+      if (lane == 0) row[bi] = -1;
+      __syncwarp();
+    }
+    if (lane == 0) atomicMax(&bound[rr / T], (int32_t)(sum < 0x7fffffff ? sum : 0x7fffffff));
+    __syncwarp();
+  }
+}
+
+// transposed uint16 copy of the histogram: ht[l][e][t] = hist[l][t][e] (all counts <= U < 65536)
+__global__ void hist_t16_kernel(const int32_t* __restrict__ hist, int64_t T, int E, uint16_t* __restrict__ ht) {
+  __shared__ uint16_t tile[32][33];
+  const int64_t l = blockIdx.z;
+  const int64_t t0 = (int64_t)blockIdx.x * 32;
+  const int e0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t t = t0 + k;
+    const int e = e0 + tx;
+    tile[k][tx] = (t < T && e < E) ? (uint16_t)hist[(l * T + t) * E + e] : (uint16_t)0;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int e = e0 + k;
+    const int64_t t = t0 + tx;
+    if (t < T && e < E) ht[(l * E + e) * T + t] = tile[tx][k];
+  }
+}
+
+template <int GM>
+__global__ void __launch_bounds__(kG2Threads, 1)
+greedy2_kernel(const int32_t* __restrict__ hist, const uint16_t* __restrict__ ht, int64_t T, int E, int G,
+               const double* __restrict__ lut, int64_t nmax, int W, const int32_t* __restrict__ run_layer,
+               const uint8_t* __restrict__ needs_greedy, const int16_t* __restrict__ order,
+               int8_t* __restrict__ assign, uint16_t* __restrict__ loads16, SearchWs ws) {
+  extern __shared__ __align__(16) unsigned char g2s[];
+  float* s_lut = reinterpret_cast<float*>(g2s);                                        // [G][W]
+  double* red = reinterpret_cast<double*>(g2s + (((size_t)G * W * 4 + 15) & ~size_t(15)));  // [warps][GM]
+  double* buf = red + (kG2Threads / 32) * GM;                                           // [kGreedyTChunk]
+  __shared__ int counts[GM];
+  __shared__ int s_best, s_ncand;
+  __shared__ int s_cand[GM];
+  const int64_t r = blockIdx.x;
+  if (!needs_greedy[r]) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int64_t width = nmax + 1;
+  const int64_t layer = run_layer[r];
+  const int32_t* h = hist + layer * T * E;
+  const uint16_t* hl = ht + layer * E * T;
+  uint16_t* ld = loads16 + r * T * GM;  // row stride GM (padded), unused GPUs stay 0
+  for (int i = tid; i < G * W; i += blockDim.x) {
+    const int g = i / W, nn = i - g * W;
+    s_lut[i] = ws.lut32[(int64_t)g * width + nn];
+  }
+  if (tid < GM) counts[tid] = 0;
+  for (int64_t i = tid; i < T * GM; i += blockDim.x) ld[i] = 0;
+  const int cap = E / G;
+  __syncthreads();
+  for (int idx = 0; idx < E; ++idx) {
+    const int e = order[r * E + idx];
+    const uint16_t* hcol = hl + (int64_t)e * T;
+    unsigned avail = 0;
+    for (int g = 0; g < G; ++g)
+      if (counts[g] < cap) avail |= 1u << g;
+    // ---- approximate scores of every GPU with capacity (any summation order)
+    double acc[GM];
+#pragma unroll
+    for (int g = 0; g < GM; ++g) acc[g] = 0.0;
+#pragma unroll 2
+    for (int64_t t = tid; t < T; t += blockDim.x) {
+      const int hv = hcol[t];
+      uint16_t lrow[GM];
+      if (GM == 8) {
+        const uint4 v = *reinterpret_cast<const uint4*>(ld + t * GM);
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { lrow[2 * q] = (uint16_t)(w4[q] & 0xffffu); lrow[2 * q + 1] = (uint16_t)(w4[q] >> 16); }
+      } else {
+#pragma unroll
+        for (int g = 0; g < GM; ++g) lrow[g] = ld[t * GM + g];
+      }
+      float m1 = __int_as_float(0xff800000), m2 = m1;
+      int i1 = -1;
+#pragma unroll
+      for (int g = 0; g < GM; ++g) {
+        if (g < G) {
+          const float v = s_lut[g * W + lrow[g]];
+          if (v > m1) { m2 = m1; m1 = v; i1 = g; }
+          else if (v > m2) { m2 = v; }
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < GM; ++g) {
+        if (g < G && (avail >> g & 1u)) {
+          const float cl = s_lut[g * W + lrow[g] + hv];
+          const float others = (i1 == g) ? m2 : m1;
+          acc[g] += (double)fmaxf(others, cl);
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < GM; ++g) {
+      double v = acc[g];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp * GM + g] = v;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double mn = __longlong_as_double(0x7ff0000000000000LL);
+      for (int g = 0; g < G; ++g) {
+        double v = 0.0;
+        for (int w = 0; w < nwarps; ++w) v += red[w * GM + g];
+        red[g] = v;  // warp 0's slots are no longer needed
+        if (avail >> g & 1u) mn = fmin(mn, v);
+      }
+      const double lim = mn * kWindow;
+      int nc = 0;
+      for (int g = 0; g < G; ++g)
+        if ((avail >> g & 1u) && red[g] <= lim) s_cand[nc++] = g;
+      s_ncand = nc;
+      s_best = s_cand[0];
+      if (nc > 1) atomicAdd(&ws.counters[2], 1);  // statistics: exact re-scores
+    }
+    __syncthreads();
+    if (s_ncand > 1) {
+      // ---- exact serial scores of the window's GPUs (v1 arithmetic, t order)
+      double best = 0.0;
+      int bg = -1;
+      for (int c = 0; c < s_ncand; ++c) {
+        const int g = s_cand[c];
+        double sum = 0.0;
+        for (int64_t t0 = 0; t0 < T; t0 += kGreedyTChunk) {
+          const int tn = (int)imin64(kGreedyTChunk, T - t0);
+          for (int tt = tid; tt < tn; tt += blockDim.x) {
+            const int64_t t = t0 + tt;
+            const uint16_t* lrow = ld + t * GM;
+            double m1 = -1.0, m2 = -1.0;
+            int i1 = -1;
+            for (int q = 0; q < G; ++q) {
+              const double v = __ldg(lut + q * width + lrow[q]);
+              if (v > m1) { m2 = m1; m1 = v; i1 = q; }
+              else if (v > m2) { m2 = v; }
+            }
+            const double cl = __ldg(lut + g * width + (int64_t)lrow[g] + h[t * E + e]);
+            double scv = cl;
+            if (G > 1) {
+              const double others = (i1 == g) ? m2 : m1;
+              scv = others > cl ? others : cl;
+            }
+            buf[tt] = scv;
+          }
+          __syncthreads();
+          if (tid == 0)
+            for (int tt = 0; tt < tn; ++tt) sum = dadd(sum, buf[tt]);
+          __syncthreads();
+        }
+        if (tid == 0 && (bg < 0 || sum < best)) { best = sum; bg = g; }
+      }
+      if (tid == 0) s_best = bg;
+      __syncthreads();
+    }
+    const int bg = s_best;
+    for (int64_t t = tid; t < T; t += blockDim.x) ld[t * GM + bg] = (uint16_t)(ld[t * GM + bg] + hcol[t]);
+    if (tid == 0) {
+      assign[r * E + e] = (int8_t)bg;
+      counts[bg] += 1;
+    }
+    __syncthreads();
+  }
+  // hand the loads to the refinement in the int32 [T][G] layout
+  int32_t* out = ws.loads + r * T * G;
+  for (int64_t i = tid; i < T * G; i += blockDim.x) out[i] = ld[(i / G) * GM + (i % G)];
 }
 
 // loads for seeded runs (or all runs when all_runs)
@@ -379,7 +593,6 @@ best_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, cons
 constexpr int kSwapY = 4;
 constexpr int kSwap3Threads = 256;
 constexpr int kSwap3TChunk = 32;
-constexpr double kWindow = 1.0 + 1.0 / 1048576.0;  // 1 + 2^-20
 
 struct Swap3Geom {
   int n, ng, nb_pad, row_items, units_per_run, rpc;
@@ -879,6 +1092,66 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   return launch_exact_scan(hist, T, E, G, lut, nmax, R, run_layer, assign, ws, ws.need_exact, st);
 }
 
+static int launch_greedy(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G, const double* lut,
+                         int64_t nmax, int64_t R, const int32_t* run_layer, const uint8_t* needs_greedy,
+                         const int16_t* order, int8_t* assign, const SearchWs& ws, cudaStream_t st) {
+  int dev = 0, optin = 0;
+  GEM_CHECK_CUDA(cudaGetDevice(&dev));
+  GEM_CHECK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (ws.lut32 && G <= 32 && T <= (1LL << 24)) {
+    // table window [0, U]: U = max over steps of the sum of the E/G largest counts
+    int32_t* bound = nullptr;
+    GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bound), (size_t)L * 4, st));
+    GEM_CHECK_CUDA(cudaMemsetAsync(bound, 0, (size_t)L * 4, st));
+    const int warps = 8;
+    topn_bound_kernel<<<(unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms()), warps * 32,
+                        (size_t)warps * E * 4, st>>>(hist, L, T, E, E / G, bound);
+    std::vector<int32_t> ub((size_t)L);
+    cudaError_t e1 = cudaGetLastError();
+    cudaError_t e2 = cudaMemcpyAsync(ub.data(), bound, (size_t)L * 4, cudaMemcpyDeviceToHost, st);
+    cudaError_t e3 = cudaStreamSynchronize(st);
+    cudaFreeAsync(bound, st);
+    if (e1 != cudaSuccess) return fail_cuda(e1, "topn_bound_kernel");
+    if (e2 != cudaSuccess) return fail_cuda(e2, "topn bound copy");
+    if (e3 != cudaSuccess) return fail_cuda(e3, "topn bound sync");
+    int64_t U = 0;
+    for (int32_t v : ub) U = imax64(U, v);
+    const int W = (int)imin64(U, nmax) + 1;
+    const int GM = G <= 8 ? 8 : (G <= 16 ? 16 : 32);
+    const size_t smem = (((size_t)G * W * 4 + 15) & ~size_t(15)) + (size_t)(kG2Threads / 32) * GM * 8 +
+                        (size_t)kGreedyTChunk * 8;
+    if (smem <= (size_t)optin && U < 65536) {
+      // transposed uint16 histogram + uint16 per-run loads (stream-ordered scratch)
+      uint16_t* ht = nullptr;
+      uint16_t* l16 = nullptr;
+      GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ht), (size_t)L * E * T * 2, st));
+      cudaError_t ea = cudaMallocAsync(reinterpret_cast<void**>(&l16), (size_t)R * T * GM * 2, st);
+      if (ea != cudaSuccess) { cudaFreeAsync(ht, st); return fail_cuda(ea, "greedy loads16"); }
+      dim3 tg((unsigned)((T + 31) / 32), (unsigned)((E + 31) / 32), (unsigned)L);
+      hist_t16_kernel<<<tg, dim3(32, 8), 0, st>>>(hist, T, E, ht);
+      cudaError_t ek = cudaGetLastError();
+      auto go = [&](auto kern) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<(unsigned)R, kG2Threads, smem, st>>>(hist, ht, T, E, G, lut, nmax, W, run_layer, needs_greedy, order,
+                                                    assign, l16, ws);
+        return cudaGetLastError();
+      };
+      if (ek == cudaSuccess) ek = GM == 8 ? go(greedy2_kernel<8>) : (GM == 16 ? go(greedy2_kernel<16>) : go(greedy2_kernel<32>));
+      cudaFreeAsync(l16, st);
+      cudaFreeAsync(ht, st);
+      if (ek != cudaSuccess) return fail_cuda(ek, "greedy2_kernel");
+      return GEM_OK;
+    }
+  }
+  const size_t gsmem = (size_t)G * kGreedyTChunk * sizeof(double);
+  GEM_CHECK_CUDA(cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
+  greedy_kernel<<<(unsigned)R, kSearchThreads, gsmem, st>>>(hist, T, E, G, lut, nmax, run_layer, needs_greedy, order,
+                                                            assign, ws.loads);
+  GEM_CHECK_LAUNCH("greedy_kernel");
+  return GEM_OK;
+}
+
 // fp32 table for the screened scan, stream-ordered allocation freed on every exit path
 struct Lut32Guard {
   float* p = nullptr;
@@ -913,11 +1186,8 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
   Lut32Guard lut32;
   if (G >= 2 && (rc = make_lut32(lut, G, nmax, lut32, ws, st))) return rc;
   GEM_CHECK_CUDA(cudaMemsetAsync(ws.counters, 0, 16, st));
-  const size_t gsmem = (size_t)G * kGreedyTChunk * sizeof(double);
-  GEM_CHECK_CUDA(cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
-  greedy_kernel<<<(unsigned)R, kSearchThreads, gsmem, st>>>(hist, T, E, G, lut, nmax, run_layer, needs_greedy, order,
-                                                            assign, ws.loads);
-  GEM_CHECK_LAUNCH("greedy_kernel");
+  rc = launch_greedy(hist, L, T, E, G, lut, nmax, R, run_layer, needs_greedy, order, assign, ws, st);
+  if (rc) return rc;
   {
     int64_t bx = (T * G + 255) / 256;
     if (bx > 64) bx = 64;
