@@ -49,8 +49,11 @@ struct SearchWs {
   int32_t* cand_n;     // [R]
   int32_t* need_exact; // [R] window overflow -> exact full scan of the run
   double* cand_exact;  // [R][kCandK]
-  float* lat32;        // [R][T][G] fp32 latencies of the current loads (screened scan only)
+  float* latT;         // [R][G][Tp] fp32 latencies of the current loads (screened scan)
+  uint16_t* loadT;     // [R][G][Tp] current loads (screened scan)
+  int64_t Tp;          // T rounded up to 32 (whole 16-byte pieces for every chunk of the transposed arrays)
   const float* lut32;  // [G][nmax+1] fp32 rounding of the latency table (set by the driver)
+  const uint16_t* ht16;  // [L][E][Tp] transposed counts (set by the driver when every count < 65536)
 };
 
 constexpr int kLocK = 8;
@@ -83,8 +86,11 @@ static size_t carve(SearchWs* ws, void* base, int64_t R, int64_t T, int G) {
   w.cand_n = (int32_t*)take((size_t)R * 4);
   w.need_exact = (int32_t*)take((size_t)R * 4);
   w.cand_exact = (double*)take((size_t)R * kCandK * 8);
-  w.lat32 = (float*)take((size_t)R * T * G * 4);
+  w.Tp = (T + 31) / 32 * 32;
+  w.latT = (float*)take((size_t)R * G * w.Tp * 4);
+  w.loadT = (uint16_t*)take((size_t)R * G * w.Tp * 2);
   w.lut32 = nullptr;
+  w.ht16 = nullptr;
   if (ws) *ws = w;
   return off;
 }
@@ -215,8 +221,10 @@ __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, i
   }
 }
 
-// transposed uint16 copy of the histogram: ht[l][e][t] = hist[l][t][e] (all counts <= U < 65536)
-__global__ void hist_t16_kernel(const int32_t* __restrict__ hist, int64_t T, int E, uint16_t* __restrict__ ht) {
+// transposed uint16 copy of the histogram: ht[l][e][t] = hist[l][t][e] for
+// t < T, 0 for T <= t < Tp (every count <= U < 65536 on this path)
+__global__ void hist_t16_kernel(const int32_t* __restrict__ hist, int64_t T, int64_t Tp, int E,
+                                uint16_t* __restrict__ ht) {
   __shared__ uint16_t tile[32][33];
   const int64_t l = blockIdx.z;
   const int64_t t0 = (int64_t)blockIdx.x * 32;
@@ -231,13 +239,13 @@ __global__ void hist_t16_kernel(const int32_t* __restrict__ hist, int64_t T, int
   for (int k = ty; k < 32; k += 8) {
     const int e = e0 + k;
     const int64_t t = t0 + tx;
-    if (t < T && e < E) ht[(l * E + e) * T + t] = tile[tx][k];
+    if (t < Tp && e < E) ht[(l * E + e) * Tp + t] = tile[tx][k];
   }
 }
 
 template <int GM>
 __global__ void __launch_bounds__(kG2Threads, 1)
-greedy2_kernel(const int32_t* __restrict__ hist, const uint16_t* __restrict__ ht, int64_t T, int E, int G,
+greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G,
                const double* __restrict__ lut, int64_t nmax, int W, const int32_t* __restrict__ run_layer,
                const uint8_t* __restrict__ needs_greedy, const int16_t* __restrict__ order,
                int8_t* __restrict__ assign, uint16_t* __restrict__ loads16, SearchWs ws) {
@@ -254,7 +262,7 @@ greedy2_kernel(const int32_t* __restrict__ hist, const uint16_t* __restrict__ ht
   const int64_t width = nmax + 1;
   const int64_t layer = run_layer[r];
   const int32_t* h = hist + layer * T * E;
-  const uint16_t* hl = ht + layer * E * T;
+  const uint16_t* hl = ws.ht16 + layer * E * ws.Tp;
   uint16_t* ld = loads16 + r * T * GM;  // row stride GM (padded), unused GPUs stay 0
   for (int i = tid; i < G * W; i += blockDim.x) {
     const int g = i / W, nn = i - g * W;
@@ -266,7 +274,7 @@ greedy2_kernel(const int32_t* __restrict__ hist, const uint16_t* __restrict__ ht
   __syncthreads();
   for (int idx = 0; idx < E; ++idx) {
     const int e = order[r * E + idx];
-    const uint16_t* hcol = hl + (int64_t)e * T;
+    const uint16_t* hcol = hl + (int64_t)e * ws.Tp;
     unsigned avail = 0;
     for (int g = 0; g < G; ++g)
       if (counts[g] < cap) avail |= 1u << g;
@@ -588,14 +596,17 @@ best_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, cons
 // CTA = (GPU pair a<b, RPC active runs). Every run places exactly n = E/G
 // experts on each GPU, so a (run, pair) tile has n*n expert pairs; a thread
 // owns one x (on a) and kSwapY consecutive y (on b): kSwapY independent
-// chains. Per t-chunk the CTA stages po' (max of the other GPUs' latencies),
-// l_a, l_b and the counts of the a- and b-experts for each of its runs.
+// chains. Per t-chunk the CTA copies, with 16-byte cp.async into a double
+// buffer, for each of its runs: the count rows of the a- and b-experts
+// (transposed uint16 histogram, one contiguous 64-byte run per expert), the
+// run's l_a / l_b rows and the fp32 latency rows of every GPU (transposed
+// per-run state kept current across swaps), then derives pother'.
 constexpr int kSwapY = 4;
 constexpr int kSwap3Threads = 256;
 constexpr int kSwap3TChunk = 32;
 
 struct Swap3Geom {
-  int n, ng, nb_pad, row_items, units_per_run, rpc;
+  int n, ng, nb_pad, units_per_run, rpc;
 };
 
 __host__ __device__ inline Swap3Geom swap3_geom(int E, int G) {
@@ -603,7 +614,6 @@ __host__ __device__ inline Swap3Geom swap3_geom(int E, int G) {
   g.n = E / G;
   g.ng = (g.n + kSwapY - 1) / kSwapY;
   g.nb_pad = g.ng * kSwapY;
-  g.row_items = g.n + g.nb_pad;
   g.units_per_run = g.n * g.ng;
   g.rpc = kSwap3Threads / g.units_per_run;
   if (g.rpc < 1) g.rpc = 1;
@@ -611,16 +621,16 @@ __host__ __device__ inline Swap3Geom swap3_geom(int E, int G) {
   return g;
 }
 
-// one staging buffer (per run, per step of a chunk): counts of the a- and
-// b-experts, the fp32 latency row, l_a, l_b and the derived pother'
+// one staging buffer: per run, [n + nb_pad] count rows + l_a + l_b (uint16),
+// [G] latency rows + pother' (fp32); every row is kSwap3TChunk long
 __host__ __device__ inline size_t swap3_buf_bytes(const Swap3Geom& g, int G) {
-  return (size_t)g.rpc * kSwap3TChunk * (4 * (size_t)g.row_items + 4 * (size_t)G + 4 + 4 + 4);
+  return (size_t)g.rpc * kSwap3TChunk * (2 * ((size_t)g.n + g.nb_pad + 2) + 4 * ((size_t)G + 1));
 }
 
 __host__ __device__ inline size_t swap3_smem(int E, int G, int64_t nmax) {
   const Swap3Geom g = swap3_geom(E, G);
   const size_t lut = ((size_t)2 * (size_t)(nmax + 1) * 4 + 15) & ~size_t(15);
-  const size_t fixed = (size_t)g.rpc * (8 + 8 + 8 + 2 * g.n * 2 + 2 * g.row_items) + 64;
+  const size_t fixed = (size_t)g.rpc * (8 + 8 + 8 + 8 + 2 * g.n * 2) + 64;
   return lut + 2 * swap3_buf_bytes(g, G) + fixed;
 }
 
@@ -628,21 +638,20 @@ __device__ __forceinline__ unsigned long long ord_bits(double v) {  // monotone 
   return (unsigned long long)__double_as_longlong(v);
 }
 
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
-               "l"(gmem), "r"(valid ? 4 : 0)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 __global__ void __launch_bounds__(kSwap3Threads, 2)
-approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, int64_t nmax,
-                   const int32_t* __restrict__ run_layer, const int8_t* __restrict__ assign, int32_t n_active,
-                   SearchWs ws) {
+approx_scan_kernel(int64_t T, int E, int G, int64_t nmax, const int32_t* __restrict__ run_layer,
+                   const int8_t* __restrict__ assign, int32_t n_active, SearchWs ws) {
   extern __shared__ __align__(16) unsigned char s3[];
   const Swap3Geom geo = swap3_geom(E, G);
-  const int n = geo.n, ng = geo.ng, RPC = geo.rpc, nb_pad = geo.nb_pad, row_items = geo.row_items;
+  const int n = geo.n, ng = geo.ng, RPC = geo.rpc, nb_pad = geo.nb_pad;
   const int NP = G * (G - 1) / 2;
   const int slot0 = blockIdx.y * RPC;
   if (slot0 >= n_active) return;
@@ -651,9 +660,12 @@ approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, in
   while (p >= G - 1 - a) { p -= G - 1 - a; ++a; }
   const int b = a + 1 + p;
   const int64_t width = nmax + 1;
+  const int64_t Tp = ws.Tp;
   constexpr int TC = kSwap3TChunk;
+  constexpr int V = TC * 2 / 16;  // 16-byte pieces per uint16 row of a chunk
+  constexpr int VF = TC * 4 / 16; // 16-byte pieces per fp32 row of a chunk
+  const int hrows = n + nb_pad;   // a-expert rows, then b-expert rows (zero padded)
 
-  // ---- carve: table rows | 2 staging buffers | per-run constants
   float* lut_a = reinterpret_cast<float*>(s3);
   float* lut_b = lut_a + width;
   unsigned char* cur = s3 + (((size_t)2 * width * 4 + 15) & ~size_t(15));
@@ -661,24 +673,22 @@ approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, in
   unsigned char* bufs = cur;
   cur += 2 * buf_bytes;
   unsigned long long* smin = reinterpret_cast<unsigned long long*>(cur);  cur += (size_t)RPC * 8;
-  int64_t* rowoff = reinterpret_cast<int64_t*>(cur);  cur += (size_t)RPC * 8;   // r * T
-  int64_t* histoff = reinterpret_cast<int64_t*>(cur); cur += (size_t)RPC * 8;   // layer * T * E
-  int16_t* colidx = reinterpret_cast<int16_t*>(cur);  cur += (size_t)RPC * row_items * 2;
-  int16_t* lists = reinterpret_cast<int16_t*>(cur);   // [RPC][2][n]
+  const uint16_t** hsrc = reinterpret_cast<const uint16_t**>(cur);       cur += (size_t)RPC * 8;  // ht16 + layer*E*Tp
+  const uint16_t** lsrc = reinterpret_cast<const uint16_t**>(cur);       cur += (size_t)RPC * 8;  // loadT + r*G*Tp
+  const float** fsrc = reinterpret_cast<const float**>(cur);             cur += (size_t)RPC * 8;  // latT + r*G*Tp
+  int16_t* lists = reinterpret_cast<int16_t*>(cur);                       // [RPC][2][n]
   struct Buf {
-    int32_t* h;    // [RPC][TC][row_items]: a-experts then b-experts (zero padded)
-    float* lat;    // [RPC][TC][G]
-    int32_t* la;   // [RPC][TC]
-    int32_t* lb;   // [RPC][TC]
+    uint16_t* h;   // [RPC][hrows][TC]
+    uint16_t* l;   // [RPC][2][TC]   l_a, l_b
+    float* lat;    // [RPC][G][TC]
     float* po;     // [RPC][TC]
   };
   auto buf_at = [&](int k) {
     unsigned char* c = bufs + k * buf_bytes;
     Buf B;
-    B.h = reinterpret_cast<int32_t*>(c);  c += (size_t)RPC * TC * row_items * 4;
-    B.lat = reinterpret_cast<float*>(c);  c += (size_t)RPC * TC * G * 4;
-    B.la = reinterpret_cast<int32_t*>(c); c += (size_t)RPC * TC * 4;
-    B.lb = reinterpret_cast<int32_t*>(c); c += (size_t)RPC * TC * 4;
+    B.h = reinterpret_cast<uint16_t*>(c);  c += (size_t)RPC * hrows * TC * 2;
+    B.l = reinterpret_cast<uint16_t*>(c);  c += (size_t)RPC * 2 * TC * 2;
+    B.lat = reinterpret_cast<float*>(c);   c += (size_t)RPC * G * TC * 4;
     B.po = reinterpret_cast<float*>(c);
     return B;
   };
@@ -695,8 +705,9 @@ approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, in
   if (tid < RPC) smin[tid] = ord_bits(__longlong_as_double(0x7ff0000000000000LL));
   if (tid < nruns) {
     const int r = ws.run_list[slot0 + tid];
-    rowoff[tid] = (int64_t)r * T;
-    histoff[tid] = (int64_t)run_layer[r] * T * E;
+    hsrc[tid] = ws.ht16 + (int64_t)run_layer[r] * E * Tp;
+    lsrc[tid] = ws.loadT + (int64_t)r * G * Tp;
+    fsrc[tid] = ws.latT + (int64_t)r * G * Tp;
   }
   // expert lists of the CTA's runs (ascending expert index on each GPU)
   for (int w = wid; w < nruns; w += nw) {
@@ -714,36 +725,36 @@ approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, in
       base_b += __popc(mb);
     }
   }
-  __syncthreads();
-  for (int i = tid; i < nruns * row_items; i += blockDim.x) {
-    const int ss = i / row_items, c = i % row_items;
-    colidx[i] = c < n ? lists[(ss * 2 + 0) * n + c] : (c - n < n ? lists[(ss * 2 + 1) * n + (c - n)] : (int16_t)-1);
+  // padded b-rows (y >= n) stay zero in both buffers
+  for (int k = 0; k < 2; ++k) {
+    const Buf B = buf_at(k);
+    for (int i = tid; i < RPC * hrows * TC; i += blockDim.x) B.h[i] = 0;
   }
   __syncthreads();
 
-  // issue the asynchronous copies of one t-chunk into buffer k
+  // 16-byte cp.async pieces of one chunk: per run, (n + n) count rows, 2 load
+  // rows, G latency rows
+  const int pieces_h = 2 * n * V, pieces_l = 2 * V, pieces_f = G * VF;
+  const int pieces_run = pieces_h + pieces_l + pieces_f;
   auto issue = [&](int64_t t0, int k) {
     const Buf B = buf_at(k);
-    const int tn = (int)imin64(TC, T - t0);
-    const int rows = nruns * tn;
-    for (int rr = wid; rr < rows; rr += nw) {
-      const int ss = rr / tn, tt = rr - ss * tn;
-      const int32_t* hrow = hist + histoff[ss] + (t0 + tt) * E;
-      for (int c = lane; c < row_items; c += 32) {
-        const int e = colidx[ss * row_items + c];
-        cp_async4(B.h + (ss * TC + tt) * row_items + c, hrow + (e >= 0 ? e : 0), e >= 0);
+    for (int i = tid; i < nruns * pieces_run; i += blockDim.x) {
+      const int ss = i / pieces_run;
+      int q = i - ss * pieces_run;
+      if (q < pieces_h) {
+        const int row = q / V, v = q - row * V;  // row < n: a-expert row, else b-expert row - n
+        const int e = row < n ? lists[(ss * 2 + 0) * n + row] : lists[(ss * 2 + 1) * n + row - n];
+        const int drow = row < n ? row : row - n + n;  // b rows start at n (padding after them)
+        cp_async16(B.h + ((size_t)ss * hrows + drow) * TC + v * 8, hsrc[ss] + (int64_t)e * Tp + t0 + v * 8);
+      } else if ((q -= pieces_h) < pieces_l) {
+        const int which = q / V, v = q - which * V;
+        cp_async16(B.l + ((size_t)ss * 2 + which) * TC + v * 8,
+                   lsrc[ss] + (int64_t)(which ? b : a) * Tp + t0 + v * 8);
+      } else {
+        q -= pieces_l;
+        const int g = q / VF, v = q - g * VF;
+        cp_async16(B.lat + ((size_t)ss * G + g) * TC + v * 4, fsrc[ss] + (int64_t)g * Tp + t0 + v * 4);
       }
-    }
-    for (int i = tid; i < rows * G; i += blockDim.x) {
-      const int rr = i / G, g = i - rr * G;
-      const int ss = rr / tn, tt = rr - ss * tn;
-      cp_async4(B.lat + (ss * TC + tt) * G + g, ws.lat32 + (rowoff[ss] + t0 + tt) * G + g, true);
-    }
-    for (int rr = tid; rr < rows; rr += blockDim.x) {
-      const int ss = rr / tn, tt = rr - ss * tn;
-      const int32_t* lrow = ws.loads + (rowoff[ss] + t0 + tt) * G;
-      cp_async4(B.la + ss * TC + tt, lrow + a, true);
-      cp_async4(B.lb + ss * TC + tt, lrow + b, true);
     }
   };
 
@@ -769,30 +780,29 @@ approx_scan_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, in
       __syncthreads();
       const Buf B = buf_at(k);
       for (int rr = tid; rr < nruns * TC; rr += blockDim.x) {
-        const int ss = rr / TC, tt = rr % TC;  // TC is a power of two
-        if (tt >= tn) continue;
-        const float* lat = B.lat + (ss * TC + tt) * G;
+        const int ss = rr / TC, tt = rr % TC;
+        const float* lat = B.lat + (size_t)ss * G * TC + tt;
         float m = __int_as_float(0xff800000);  // -inf when G == 2
         for (int g = 0; g < G; ++g)
-          if (g != a && g != b) m = fmaxf(m, lat[g]);
+          if (g != a && g != b) m = fmaxf(m, lat[g * TC]);
         B.po[ss * TC + tt] = m;
       }
       __syncthreads();
       if (live) {
         const float* pos = B.po + s * TC;
-        const int32_t* las = B.la + s * TC;
-        const int32_t* lbs = B.lb + s * TC;
-        const int32_t* hAs = B.h + (size_t)s * TC * row_items + x;
-        const int32_t* hBs = B.h + (size_t)s * TC * row_items + n + yg * kSwapY;
+        const uint16_t* las = B.l + (size_t)s * 2 * TC;
+        const uint16_t* lbs = las + TC;
+        const uint16_t* hAs = B.h + ((size_t)s * hrows + x) * TC;
+        const uint16_t* hBs = B.h + ((size_t)s * hrows + n + yg * kSwapY) * TC;
 #pragma unroll 4
         for (int tt = 0; tt < tn; ++tt) {
-          const int32_t hx = hAs[tt * row_items];
-          const int32_t ra = las[tt] - hx, rb = lbs[tt] + hx;
+          const int32_t hx = hAs[tt];
+          const int32_t ra = (int32_t)las[tt] - hx, rb = (int32_t)lbs[tt] + hx;
           const float pm = pos[tt];
-          const int32_t* hy = hBs + tt * row_items;
 #pragma unroll
           for (int q = 0; q < kSwapY; ++q) {
-            const float m = fmaxf(fmaxf(pm, lut_a[ra + hy[q]]), lut_b[rb - hy[q]]);
+            const int32_t hy = hBs[q * TC + tt];
+            const float m = fmaxf(fmaxf(pm, lut_a[ra + hy]), lut_b[rb - hy]);
             acc[q] = dadd(acc[q], (double)m);
           }
         }
@@ -923,10 +933,24 @@ __global__ void select_pairs_kernel(int32_t n_active, int E, SearchWs ws) {
   }
 }
 
-// fp32 latency matrix of the current loads for every run (screened scan)
-__global__ void lat32_fill_kernel(int64_t n, int G, int64_t width, SearchWs ws) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    ws.lat32[i] = ws.lut32[(int64_t)(i % G) * width + ws.loads[i]];
+// transposed per-run state for the screened scan: loadT[r][g][t], latT[r][g][t]
+// (zero past T)
+__global__ void state_t_kernel(int64_t R, int64_t T, int G, int64_t width, SearchWs ws) {
+  const int64_t Tp = ws.Tp;
+  const int64_t n = R * G * Tp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i % Tp, rg = i / Tp;
+    const int g = (int)(rg % G);
+    const int64_t r = rg / G;
+    int32_t l = 0;
+    float v = 0.0f;
+    if (t < T) {
+      l = ws.loads[(r * T + t) * G + g];
+      v = ws.lut32[(int64_t)g * width + l];
+    }
+    ws.loadT[i] = (uint16_t)l;
+    ws.latT[i] = v;
+  }
 }
 
 // fp64 latency table -> its fp32 rounding (round to nearest: monotone)
@@ -984,16 +1008,19 @@ apply_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, con
   const int a = assign[r * E + i], b = assign[r * E + j];
   const int32_t* h = hist + (int64_t)run_layer[r] * T * E;
   int32_t* ld = ws.loads + r * T * G;
-  float* l32 = ws.lut32 ? ws.lat32 + r * T * G : nullptr;
+  const bool screened = ws.ht16 != nullptr;
   const int64_t width = nmax + 1;
+  const int64_t Tp = ws.Tp;
   for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
     const int32_t d = h[t * E + j] - h[t * E + i];
     const int32_t na = ld[t * G + a] + d, nb = ld[t * G + b] - d;
     ld[t * G + a] = na;
     ld[t * G + b] = nb;
-    if (l32) {
-      l32[t * G + a] = ws.lut32[a * width + na];
-      l32[t * G + b] = ws.lut32[b * width + nb];
+    if (screened) {
+      ws.loadT[(r * G + a) * Tp + t] = (uint16_t)na;
+      ws.loadT[(r * G + b) * Tp + t] = (uint16_t)nb;
+      ws.latT[(r * G + a) * Tp + t] = ws.lut32[a * width + na];
+      ws.latT[(r * G + b) * Tp + t] = ws.lut32[b * width + nb];
     }
   }
   __syncthreads();
@@ -1067,7 +1094,7 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   int dev = 0, optin = 0;
   GEM_CHECK_CUDA(cudaGetDevice(&dev));
   GEM_CHECK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  if (ws.lut32 == nullptr || smem3 > (size_t)optin) {
+  if (ws.lut32 == nullptr || ws.ht16 == nullptr || smem3 > (size_t)optin) {
     return launch_exact_scan(hist, T, E, G, lut, nmax, R, run_layer, assign, ws, nullptr, st);
   }
   GEM_CHECK_CUDA(cudaMemsetAsync(ws.counters + 3, 0, 4, st));
@@ -1077,8 +1104,7 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   GEM_CHECK_CUDA(cudaFuncSetAttribute(approx_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   const Swap3Geom g = swap3_geom(E, G);
   dim3 grid((unsigned)NP, (unsigned)((n_active + g.rpc - 1) / g.rpc));
-  approx_scan_kernel<<<grid, kSwap3Threads, smem3, st>>>(hist, T, E, G, nmax, run_layer, assign, (int32_t)n_active,
-                                                         ws);
+  approx_scan_kernel<<<grid, kSwap3Threads, smem3, st>>>(T, E, G, nmax, run_layer, assign, (int32_t)n_active, ws);
   GEM_CHECK_LAUNCH("approx_scan_kernel");
   window_kernel<<<(unsigned)((n_active + 127) / 128), 128, 0, st>>>((int32_t)n_active, G, ws);
   GEM_CHECK_LAUNCH("window_kernel");
@@ -1092,54 +1118,30 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   return launch_exact_scan(hist, T, E, G, lut, nmax, R, run_layer, assign, ws, ws.need_exact, st);
 }
 
-static int launch_greedy(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G, const double* lut,
-                         int64_t nmax, int64_t R, const int32_t* run_layer, const uint8_t* needs_greedy,
+static int launch_greedy(const int32_t* hist, int64_t T, int32_t E, int32_t G, const double* lut, int64_t nmax,
+                         int64_t U, int64_t R, const int32_t* run_layer, const uint8_t* needs_greedy,
                          const int16_t* order, int8_t* assign, const SearchWs& ws, cudaStream_t st) {
   int dev = 0, optin = 0;
   GEM_CHECK_CUDA(cudaGetDevice(&dev));
   GEM_CHECK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  if (ws.lut32 && G <= 32 && T <= (1LL << 24)) {
-    // table window [0, U]: U = max over steps of the sum of the E/G largest counts
-    int32_t* bound = nullptr;
-    GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bound), (size_t)L * 4, st));
-    GEM_CHECK_CUDA(cudaMemsetAsync(bound, 0, (size_t)L * 4, st));
-    const int warps = 8;
-    topn_bound_kernel<<<(unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms()), warps * 32,
-                        (size_t)warps * E * 4, st>>>(hist, L, T, E, E / G, bound);
-    std::vector<int32_t> ub((size_t)L);
-    cudaError_t e1 = cudaGetLastError();
-    cudaError_t e2 = cudaMemcpyAsync(ub.data(), bound, (size_t)L * 4, cudaMemcpyDeviceToHost, st);
-    cudaError_t e3 = cudaStreamSynchronize(st);
-    cudaFreeAsync(bound, st);
-    if (e1 != cudaSuccess) return fail_cuda(e1, "topn_bound_kernel");
-    if (e2 != cudaSuccess) return fail_cuda(e2, "topn bound copy");
-    if (e3 != cudaSuccess) return fail_cuda(e3, "topn bound sync");
-    int64_t U = 0;
-    for (int32_t v : ub) U = imax64(U, v);
+  if (ws.ht16 && G <= 32) {
     const int W = (int)imin64(U, nmax) + 1;
     const int GM = G <= 8 ? 8 : (G <= 16 ? 16 : 32);
     const size_t smem = (((size_t)G * W * 4 + 15) & ~size_t(15)) + (size_t)(kG2Threads / 32) * GM * 8 +
                         (size_t)kGreedyTChunk * 8;
-    if (smem <= (size_t)optin && U < 65536) {
-      // transposed uint16 histogram + uint16 per-run loads (stream-ordered scratch)
-      uint16_t* ht = nullptr;
-      uint16_t* l16 = nullptr;
-      GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ht), (size_t)L * E * T * 2, st));
-      cudaError_t ea = cudaMallocAsync(reinterpret_cast<void**>(&l16), (size_t)R * T * GM * 2, st);
-      if (ea != cudaSuccess) { cudaFreeAsync(ht, st); return fail_cuda(ea, "greedy loads16"); }
-      dim3 tg((unsigned)((T + 31) / 32), (unsigned)((E + 31) / 32), (unsigned)L);
-      hist_t16_kernel<<<tg, dim3(32, 8), 0, st>>>(hist, T, E, ht);
-      cudaError_t ek = cudaGetLastError();
+    if (smem <= (size_t)optin) {
+      uint16_t* l16 = nullptr;  // uint16 per-run loads, stream-ordered scratch
+      GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&l16), (size_t)R * T * GM * 2, st));
       auto go = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        kern<<<(unsigned)R, kG2Threads, smem, st>>>(hist, ht, T, E, G, lut, nmax, W, run_layer, needs_greedy, order,
+        kern<<<(unsigned)R, kG2Threads, smem, st>>>(hist, T, E, G, lut, nmax, W, run_layer, needs_greedy, order,
                                                     assign, l16, ws);
         return cudaGetLastError();
       };
-      if (ek == cudaSuccess) ek = GM == 8 ? go(greedy2_kernel<8>) : (GM == 16 ? go(greedy2_kernel<16>) : go(greedy2_kernel<32>));
+      const cudaError_t ek =
+          GM == 8 ? go(greedy2_kernel<8>) : (GM == 16 ? go(greedy2_kernel<16>) : go(greedy2_kernel<32>));
       cudaFreeAsync(l16, st);
-      cudaFreeAsync(ht, st);
       if (ek != cudaSuccess) return fail_cuda(ek, "greedy2_kernel");
       return GEM_OK;
     }
@@ -1152,22 +1154,52 @@ static int launch_greedy(const int32_t* hist, int64_t L, int64_t T, int32_t E, i
   return GEM_OK;
 }
 
-// fp32 table for the screened scan, stream-ordered allocation freed on every exit path
-struct Lut32Guard {
-  float* p = nullptr;
+// Screening scratch (K6 v3+, K7 v2): the fp32 table, the transposed uint16
+// histogram and the load bound U; stream-ordered allocations freed on every
+// exit path. Without a transposed histogram (some count >= 65536) the search
+// runs the exact v1 kernels.
+struct Screen {
+  float* lut32 = nullptr;
+  uint16_t* ht16 = nullptr;
+  int64_t U = 0;
   cudaStream_t st = nullptr;
-  ~Lut32Guard() {
-    if (p) cudaFreeAsync(p, st);
+  ~Screen() {
+    if (lut32) cudaFreeAsync(lut32, st);
+    if (ht16) cudaFreeAsync(ht16, st);
   }
 };
 
-static int make_lut32(const double* lut, int G, int64_t nmax, Lut32Guard& g, SearchWs& ws, cudaStream_t st) {
+static int prepare_screen(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G, const double* lut,
+                          int64_t nmax, Screen& sc, SearchWs& ws, cudaStream_t st) {
+  sc.st = st;
+  if (G < 2 || T > (1LL << 24)) return GEM_OK;
   const int64_t n = (int64_t)G * (nmax + 1);
-  g.st = st;
-  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g.p), (size_t)n * sizeof(float), st));
-  lut_to_f32_kernel<<<(unsigned)imin64((n + 255) / 256, 4096), 256, 0, st>>>(lut, n, g.p);
+  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.lut32), (size_t)n * sizeof(float), st));
+  lut_to_f32_kernel<<<(unsigned)imin64((n + 255) / 256, 4096), 256, 0, st>>>(lut, n, sc.lut32);
   GEM_CHECK_LAUNCH("lut_to_f32_kernel");
-  ws.lut32 = g.p;
+  ws.lut32 = sc.lut32;
+  // U = max over layers and steps of the sum of the E/G largest counts
+  int32_t* bound = nullptr;
+  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bound), (size_t)L * 4, st));
+  GEM_CHECK_CUDA(cudaMemsetAsync(bound, 0, (size_t)L * 4, st));
+  const int warps = 8;
+  topn_bound_kernel<<<(unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms()), warps * 32,
+                      (size_t)warps * E * 4, st>>>(hist, L, T, E, E / G, bound);
+  std::vector<int32_t> ub((size_t)L);
+  cudaError_t e1 = cudaGetLastError();
+  cudaError_t e2 = cudaMemcpyAsync(ub.data(), bound, (size_t)L * 4, cudaMemcpyDeviceToHost, st);
+  cudaError_t e3 = cudaStreamSynchronize(st);
+  cudaFreeAsync(bound, st);
+  if (e1 != cudaSuccess) return fail_cuda(e1, "topn_bound_kernel");
+  if (e2 != cudaSuccess) return fail_cuda(e2, "topn bound copy");
+  if (e3 != cudaSuccess) return fail_cuda(e3, "topn bound sync");
+  for (int32_t v : ub) sc.U = imax64(sc.U, v);
+  if (sc.U >= 65536) return GEM_OK;
+  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.ht16), (size_t)L * E * ws.Tp * 2, st));
+  dim3 tg((unsigned)(ws.Tp / 32), (unsigned)((E + 31) / 32), (unsigned)L);
+  hist_t16_kernel<<<tg, dim3(32, 8), 0, st>>>(hist, T, ws.Tp, E, sc.ht16);
+  GEM_CHECK_LAUNCH("hist_t16_kernel");
+  ws.ht16 = sc.ht16;
   return GEM_OK;
 }
 
@@ -1183,10 +1215,10 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
   cudaStream_t st = as_stream(stream);
   SearchWs ws;
   carve(&ws, workspace, R, T, G);
-  Lut32Guard lut32;
-  if (G >= 2 && (rc = make_lut32(lut, G, nmax, lut32, ws, st))) return rc;
+  Screen screen;
+  if ((rc = prepare_screen(hist, L, T, E, G, lut, nmax, screen, ws, st))) return rc;
   GEM_CHECK_CUDA(cudaMemsetAsync(ws.counters, 0, 16, st));
-  rc = launch_greedy(hist, L, T, E, G, lut, nmax, R, run_layer, needs_greedy, order, assign, ws, st);
+  rc = launch_greedy(hist, T, E, G, lut, nmax, screen.U, R, run_layer, needs_greedy, order, assign, ws, st);
   if (rc) return rc;
   {
     int64_t bx = (T * G + 255) / 256;
@@ -1197,9 +1229,9 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
   }
   init_score_kernel<<<(unsigned)R, kSearchThreads, 0, st>>>(T, G, lut, nmax, ws, traj_cap, trajectory, swaps);
   GEM_CHECK_LAUNCH("init_score_kernel");
-  if (ws.lut32) {
-    lat32_fill_kernel<<<4 * num_sms(), 256, 0, st>>>(R * T * G, G, nmax + 1, ws);
-    GEM_CHECK_LAUNCH("lat32_fill_kernel");
+  if (ws.ht16) {
+    state_t_kernel<<<4 * num_sms(), 256, 0, st>>>(R, T, G, nmax + 1, ws);
+    GEM_CHECK_LAUNCH("state_t_kernel");
   }
   int64_t n_active = R;  // every run is active before its first scan
   for (int64_t it = 0; it < swap_cap; ++it) {
@@ -1238,16 +1270,16 @@ extern "C" int gem_best_swap_runs(const int32_t* hist, int64_t L, int64_t T, int
   cudaStream_t st = as_stream(stream);
   SearchWs ws;
   carve(&ws, workspace, R, T, G);
-  Lut32Guard lut32;
-  if (G >= 2 && (rc = make_lut32(lut, G, nmax, lut32, ws, st))) return rc;
+  Screen screen;
+  if ((rc = prepare_screen(hist, L, T, E, G, lut, nmax, screen, ws, st))) return rc;
   int64_t bx = (T * G + 255) / 256;
   if (bx > 64) bx = 64;
   init_loads_kernel<<<dim3((unsigned)bx, (unsigned)R), 256, E, st>>>(hist, T, E, G, run_layer, nullptr, assign,
                                                                      ws.loads);
   GEM_CHECK_LAUNCH("init_loads_kernel");
-  if (ws.lut32) {
-    lat32_fill_kernel<<<4 * num_sms(), 256, 0, st>>>(R * T * G, G, nmax + 1, ws);
-    GEM_CHECK_LAUNCH("lat32_fill_kernel");
+  if (ws.ht16) {
+    state_t_kernel<<<4 * num_sms(), 256, 0, st>>>(R, T, G, nmax + 1, ws);
+    GEM_CHECK_LAUNCH("state_t_kernel");
   }
   std::vector<int32_t> ones(R, 1);
   GEM_CHECK_CUDA(cudaMemcpyAsync(ws.run_active, ones.data(), R * 4, cudaMemcpyHostToDevice, st));
