@@ -216,26 +216,38 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     kev = []  # (start, end) events around K1 per timed step
 
+    phases = ("K1 topk_hist", "K2 step_gram", "all-reduce", "K3 finalize", "K3b classify")
+    pev = []  # per timed step: events bracketing each phase
+
     def stats_step(timed: bool):
         colsum = torch.zeros((L, E), dtype=torch.int64, device="cuda")
         active = torch.zeros((L, E), dtype=torch.int32, device="cuda")
         dropped = torch.zeros((L,), dtype=torch.int64, device="cuda")
         gram = torch.zeros((L, E, E), dtype=torch.int64, device="cuda")
-        if timed:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(phases) + 1)] if timed else None
+
+        def mark(i):
+            if timed:
+                evs[i].record(stream)
+
+        mark(0)
         _lib.call("gem_topk_hist", ids.data_ptr(), 2, L, n_local, k, B, E, hist.data_ptr(), colsum.data_ptr(),
                   active.data_ptr(), dropped.data_ptr(), stream.cuda_stream)
-        if timed:
-            e1.record(stream)
-            kev.append((e0, e1))
+        mark(1)
         _lib.call("gem_step_gram", hist.data_ptr(), L, t1 - t0, E, B * k, gram.data_ptr(), stream.cuda_stream)
+        mark(2)
         if use_dist:
             for t in (colsum, active, gram):
                 dist.all_reduce(t)
+        mark(3)
         ds = DeviceStats(colsum, active, gram, T)
         mu, af, corr = finalize_stats(ds, with_corr=True)
+        mark(4)
         cls = ingest.classify_device(colsum, active, gram, T)
+        mark(5)
+        if timed:
+            kev.append((evs[0], evs[1]))
+            pev.append(evs)
         return mu, af, corr, cls
 
     for _ in range(args.warmup):
@@ -251,6 +263,7 @@ def run_ours(args):
             out = stats_step(True)
         ev1.record(stream)
         torch.cuda.synchronize()
+    out[3].check()  # K3b's asynchronous range flag (checked outside the timed region)
     ms = ev0.elapsed_time(ev1) / args.steps
     if use_dist:
         t = torch.tensor([ms], device="cuda")
@@ -268,6 +281,8 @@ def run_ours(args):
                    "virtual_gpus": G, "id_dtype": "int16", "l2": "inputs 25 GB >> 126 MB L2 (no flush needed)",
                    "parallelism": f"token-range shards x{world}, NCCL all-reduce of integer stats"},
         "gpu_launches": 4 * args.steps,
+        "step_breakdown_ms": {name: sum(e[i].elapsed_time(e[i + 1]) for e in pev) / len(pev)
+                              for i, name in enumerate(phases)},
         "clocks": clk.summary(),
     }
     # roofline of the dominant kernel (K1)
@@ -298,6 +313,7 @@ def run_ours(args):
             else:
                 st = ingest.trace_statistics(dev_ids, B, E)
                 mu, cls = st.mean_utilization, st.classes.cls
+                st.check()
             res = (mu.to("cpu", non_blocking=True), cls.to("cpu", non_blocking=True))
             torch.cuda.current_stream().synchronize()
             return res
@@ -387,6 +403,7 @@ def run_ours(args):
             mu = st[0].cpu().numpy() if Tw == T else None
             return None, search_hist(h, B * k, profile, cfg, mean_util=mu)
 
+        ttm()  # warm-up: module load, stream-ordered pool growth (~1.5 GB of search scratch), LUT build
         (shm, results), tms = dev_time(ttm)
         info = {"value": tms / 1e3, "unit": "s", "steps_searched": Tw, "layers": L,
                 "runs_per_layer": cfg.restarts + 2, "timing": "CUDA events on the launching stream, max over ranks",

@@ -142,11 +142,14 @@ int gem_stats_finalize(const int64_t* colsum, const int32_t* active, const int64
  * temporal:    not consistent, and r(e,f) >= corr_num/corr_den (exact int128
  *              predicate) for some other non-consistent f
  * group:       connected components of the temporal correlation graph,
- *              labelled by their lowest expert index; -1 otherwise. */
+ *              labelled by their lowest expert index; -1 otherwise.
+ * Asynchronous: *err_flag (device, zeroed by the caller) becomes nonzero if a
+ * correlation statistic exceeds the exact int128 predicate range; the caller
+ * checks it when it next reads results (no host synchronisation here). */
 int gem_classify(const int64_t* colsum, const int32_t* active, const int64_t* gram,
                  int64_t L, int64_t T, int32_t E, int64_t cons_num, int64_t cons_den,
                  int64_t corr_num, int64_t corr_den, int8_t* cls, int16_t* group,
-                 void* stream);
+                 int32_t* err_flag, void* stream);
 
 /* --- K4: curve evaluation ----------------------------------------------- */
 int gem_eval_curve(const int64_t* xs_flat, const double* ys_flat, const int64_t* offsets,

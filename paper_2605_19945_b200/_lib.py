@@ -66,7 +66,7 @@ _SIGNATURES = {
     "gem_step_gram_cc": [P, I64, I64, I32, P, P],
     "gem_step_gram_tc": [P, I64, I64, I32, P, P],
     "gem_stats_finalize": [P, P, P, I64, I64, I32, P, P, P, P],
-    "gem_classify": [P, P, P, I64, I64, I32, I64, I64, I64, I64, P, P, P],
+    "gem_classify": [P, P, P, I64, I64, I32, I64, I64, I64, I64, P, P, P, P],
     "gem_eval_curve": [P, P, P, P, I32, P, I64, P, P],
     "gem_curve_lut": [P, P, P, P, I32, I64, P, P],
     "gem_score_batch": [P, I64, I64, I32, I32, P, I64, P, I64, P, P, P, P],

@@ -406,29 +406,17 @@ extern "C" int gem_stats_finalize(const int64_t* colsum, const int32_t* active, 
 
 extern "C" int gem_classify(const int64_t* colsum, const int32_t* active, const int64_t* gram, int64_t L, int64_t T,
                             int32_t E, int64_t cons_num, int64_t cons_den, int64_t corr_num, int64_t corr_den,
-                            int8_t* cls, int16_t* group, void* stream) {
-  GEM_REQUIRE(L >= 1 && T >= 1 && E >= 1 && E <= 1024 && colsum && active && gram && cls && group,
+                            int8_t* cls, int16_t* group, int32_t* err_flag, void* stream) {
+  GEM_REQUIRE(L >= 1 && T >= 1 && E >= 1 && E <= 1024 && colsum && active && gram && cls && group && err_flag,
               "gem_classify: bad arguments");
   GEM_REQUIRE(cons_den > 0 && cons_num >= 0 && corr_den > 0 && corr_num > 0 && corr_num <= corr_den &&
                   corr_den <= (1 << 20),
               "gem_classify: thresholds must be rationals with small positive denominators");
   cudaStream_t st = as_stream(stream);
-  int32_t* err = nullptr;
-  GEM_CHECK_CUDA(cudaMallocAsync(&err, sizeof(int32_t), st));
-  GEM_CHECK_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
   const int words = (E + 31) / 32;
   const size_t smem = (size_t)E * words * 4 + (size_t)E * 4 + (size_t)E;
   classify_kernel<<<(unsigned)L, 256, smem, st>>>(colsum, active, gram, T, E, cons_num, cons_den, corr_num, corr_den,
-                                                  cls, group, err);
-  cudaError_t le = cudaGetLastError();
-  int32_t h_err = 0;
-  cudaMemcpyAsync(&h_err, err, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-  cudaFreeAsync(err, st);
-  if (le != cudaSuccess) return fail_cuda(le, "classify_kernel");
-  GEM_CHECK_CUDA(cudaStreamSynchronize(st));
-  if (h_err) {
-    set_error("gem_classify: correlation statistics exceed the exact int128 predicate range");
-    return GEM_ERR_RANGE;
-  }
+                                                  cls, group, err_flag);
+  GEM_CHECK_LAUNCH("classify_kernel");
   return GEM_OK;
 }

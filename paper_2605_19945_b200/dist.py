@@ -169,7 +169,7 @@ class DeviceOps:
         from .trace import DeviceStats, finalize_stats
 
         mu, af, corr = finalize_stats(DeviceStats(colsum, active, gram, T))
-        cls = classify_device(colsum, active, gram, T)
+        cls = classify_device(colsum, active, gram, T).check()
         return mu, af, corr, cls.cls, cls.group
 
     def search(self, hist_owned, nmax, profile, config):

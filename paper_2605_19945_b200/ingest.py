@@ -204,6 +204,13 @@ def step_coactivation(hist: torch.Tensor, gram: torch.Tensor | None = None, max_
 class ExpertClasses:
     cls: torch.Tensor    # [L, E] int8: CLASS_OTHER / CLASS_CONSISTENT / CLASS_TEMPORAL
     group: torch.Tensor  # [L, E] int16: lowest expert index of the correlated-temporal group, -1 otherwise
+    err: torch.Tensor | None = None  # [1] int32 device flag set by K3b on int128 range overflow
+
+    def check(self) -> "ExpertClasses":
+        """Raise if the (asynchronous) classification overflowed its exact predicate range."""
+        if self.err is not None and int(self.err.item()):
+            raise _lib.KernelError("gem_classify: correlation statistics exceed the exact int128 predicate range")
+        return self
 
 
 @dataclass(frozen=True)
@@ -223,9 +230,10 @@ def classify_device(colsum, active, gram, num_steps: int, config: ClassifyConfig
     grp = _device.empty((L, E), torch.int16)
     cn, cd = config.consistent_fraction
     rn, rd = config.correlation_threshold
+    err = _device.zeros((1,), torch.int32)
     _lib.call("gem_classify", ptr(colsum), ptr(active), ptr(gram), L, num_steps, E, cn, cd, rn, rd, ptr(cls),
-              ptr(grp), stream())
-    return ExpertClasses(cls, grp)
+              ptr(grp), ptr(err), stream())
+    return ExpertClasses(cls, grp, err)
 
 
 @dataclass
@@ -239,6 +247,12 @@ class TraceStatistics:
     correlation: torch.Tensor | None  # [L, E, E] fp64
     classes: ExpertClasses | None
     extra: dict = field(default_factory=dict)
+
+    def check(self) -> "TraceStatistics":
+        """Raise on any asynchronous kernel-side error flag (synchronises the stream)."""
+        if self.classes is not None:
+            self.classes.check()
+        return self
 
     def layer_stats(self, l: int) -> TraceStats:
         """The reference's TraceStats for layer l."""
