@@ -169,6 +169,22 @@ int gem_score_batch(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_
                     const int8_t* cand, int64_t C, const double* lut, int64_t nmax,
                     double* layer_scores, double* total, int32_t* err_flag, void* stream);
 
+/* The two implementations behind gem_score_batch (which tries the first and
+ * falls back to the second):
+ *  - gem_score_batch_tc: candidate loads as a one-hot fp16 GEMM on tcgen05
+ *    (exact: counts <= 2048, loads < 2^24), written as uint16, then one thread
+ *    per (candidate, layer) takes the exact per-step maximum (fp32 table
+ *    window in shared memory picks the GPU, the fp64 table gives the value)
+ *    and sums serially. Needs E in {64, 128}, G | 256. Returns 1 (nothing
+ *    done) when a precondition fails; stream-ordered scratch, one host sync.
+ *  - gem_score_batch_v1: CUDA cores, any shape (E <= 256). */
+int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G,
+                       const int8_t* cand, int64_t C, const double* lut, int64_t nmax,
+                       double* layer_scores, int32_t* err_flag, void* stream);
+int gem_score_batch_v1(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G,
+                       const int8_t* cand, int64_t C, const double* lut, int64_t nmax,
+                       double* layer_scores, int32_t* err_flag, void* stream);
+
 /* total[c] = serial-in-l sum of layer_scores[c][0..L) (cli.py:427 aggregate order) */
 int gem_layer_sum(const double* layer_scores, int64_t C, int64_t L, double* total, void* stream);
 

@@ -71,6 +71,8 @@ _SIGNATURES = {
     "gem_curve_lut": [P, P, P, P, I32, I64, P, P],
     "gem_score_batch": [P, I64, I64, I32, I32, P, I64, P, I64, P, P, P, P],
     "gem_layer_sum": [P, I64, I64, P, P],
+    "gem_score_batch_tc": [P, I64, I64, I32, I32, P, I64, P, I64, P, P, P],
+    "gem_score_batch_v1": [P, I64, I64, I32, I32, P, I64, P, I64, P, P, P],
     "gem_replay": [P, I64, I32, I32, P, P, I64, P, P, P, P, P, P, P, P, P],
     "gem_search_runs": [P, I64, I64, I32, I32, P, I64, I64, P, P, P, P, F64, I64, I64, P, P, P, P, SZ, P],
     "gem_best_swap_runs": [P, I64, I64, I32, I32, P, I64, I64, P, P, P, P, P, P, P, SZ, P],

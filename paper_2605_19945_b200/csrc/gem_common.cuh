@@ -48,6 +48,7 @@ __host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { retur
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int num_sms();
+void keep_pool();
 
 // ---------------------------------------------------------------------------
 // Curve evaluation: C_g(n) for one GPU's sampled curve.

@@ -20,6 +20,17 @@ int fail_cuda(cudaError_t err, const char* what) {
   return GEM_ERR_CUDA;
 }
 
+// Stream-ordered scratch (cudaMallocAsync) must not be returned to the OS at
+// every synchronisation: keep the current device's default pool warm.
+void keep_pool() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+  uint64_t thr = ~0ull;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+}
+
 int num_sms() {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)

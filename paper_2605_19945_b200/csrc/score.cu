@@ -190,6 +190,22 @@ extern "C" int gem_curve_lut(const int64_t* xs_flat, const double* ys_flat, cons
   return GEM_OK;
 }
 
+extern "C" int gem_score_batch_v1(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G,
+                                  const int8_t* cand, int64_t C, const double* lut, int64_t nmax,
+                                  double* layer_scores, int32_t* err_flag, void* stream) {
+  GEM_REQUIRE(hist && cand && lut && err_flag && layer_scores && L >= 1 && L <= 65535 && T >= 1 && E >= 1 &&
+                  E <= 256 && G >= 1 && G <= 127 && C >= 1,
+              "gem_score_batch_v1: bad arguments");
+  cudaStream_t st = as_stream(stream);
+  const size_t smem = (size_t)kScoreTChunk * E * 4 + (size_t)E * kScoreThreads + (size_t)(G + 1) * kScoreThreads * 2;
+  GEM_CHECK_CUDA(cudaFuncSetAttribute(score_layers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)((C + kScoreThreads - 1) / kScoreThreads), (unsigned)L);
+  score_layers_kernel<<<grid, kScoreThreads, smem, st>>>(hist, T, E, G, cand, C, L, lut, nmax, layer_scores,
+                                                         err_flag);
+  GEM_CHECK_LAUNCH("score_layers_kernel");
+  return GEM_OK;
+}
+
 extern "C" int gem_score_batch(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G, const int8_t* cand,
                                int64_t C, const double* lut, int64_t nmax, double* layer_scores, double* total,
                                int32_t* err_flag, void* stream) {
@@ -199,12 +215,18 @@ extern "C" int gem_score_batch(const int32_t* hist, int64_t L, int64_t T, int32_
   GEM_REQUIRE(L <= 65535, "gem_score_batch: L too large");
   GEM_REQUIRE(layer_scores, "gem_score_batch: layer_scores workspace is required");
   cudaStream_t st = as_stream(stream);
-  const size_t smem = (size_t)kScoreTChunk * E * 4 + (size_t)E * kScoreThreads + (size_t)(G + 1) * kScoreThreads * 2;
-  GEM_CHECK_CUDA(cudaFuncSetAttribute(score_layers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)((C + kScoreThreads - 1) / kScoreThreads), (unsigned)L);
-  score_layers_kernel<<<grid, kScoreThreads, smem, st>>>(hist, T, E, G, cand, C, L, lut, nmax, layer_scores,
-                                                         err_flag);
-  GEM_CHECK_LAUNCH("score_layers_kernel");
+  // tensor-core loads + screened exact maximum (score_tc.cu) when its preconditions hold
+  const int rc = gem_score_batch_tc(hist, L, T, E, G, cand, C, lut, nmax, layer_scores, err_flag, stream);
+  if (rc < 0) return rc;
+  if (rc == 1) {
+    const size_t smem =
+        (size_t)kScoreTChunk * E * 4 + (size_t)E * kScoreThreads + (size_t)(G + 1) * kScoreThreads * 2;
+    GEM_CHECK_CUDA(cudaFuncSetAttribute(score_layers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((unsigned)((C + kScoreThreads - 1) / kScoreThreads), (unsigned)L);
+    score_layers_kernel<<<grid, kScoreThreads, smem, st>>>(hist, T, E, G, cand, C, L, lut, nmax, layer_scores,
+                                                           err_flag);
+    GEM_CHECK_LAUNCH("score_layers_kernel");
+  }
   if (total) {
     layer_sum_kernel<<<grid_for(C, 256), 256, 0, st>>>(layer_scores, C, L, total);
     GEM_CHECK_LAUNCH("layer_sum_kernel");

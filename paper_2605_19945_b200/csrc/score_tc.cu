@@ -1,0 +1,419 @@
+// K5 v2: straggler scoring of thousands of candidate mappings on B200.
+//
+//   score[c][l] = sum_t (serial fp64)  max_g C_g( n_g(c,l,t) ),
+//   n_g(c,l,t)  = sum_{e : cand[c][l][e] == g} h[l][t][e]        (mapping.py:146-166)
+//
+// Two passes per batch of P layers:
+//
+//  pass 1 (loads_tc_kernel, tcgen05): the per-GPU loads of every candidate are
+//    a one-hot GEMM  D[t][(c,g)] = sum_e H[t][e] * O[e][(c,g)]  with H in fp16
+//    (counts <= 2048 are exact) and O the 0/1 one-hot of the candidate tables,
+//    accumulated in fp32 in TMEM (loads < 2^24 are exact). M = 128 steps,
+//    N = 256 (candidate, GPU) columns, K = E. The one-hot B tile is built once
+//    per CTA; the H tiles are produced from the int32 histogram by all warps
+//    (fp16 convert, K-major 16-byte stores) into a 2-stage ring; one thread
+//    issues the MMAs; the epilogue drains TMEM (tcgen05.ld) and writes the
+//    loads as uint16 [layer][t][c][g] (each thread a contiguous row segment).
+//
+//  pass 2 (score_epi_kernel, CUDA cores): one thread per (candidate, layer)
+//    walks t in order. The fp32 rounding of the latency table window [0, U]
+//    (U = max over steps of the sum of the `maxcnt` largest counts, maxcnt =
+//    the most experts any candidate puts on one GPU: no load can exceed it)
+//    sits in shared memory and picks the arg-max GPU (rounding is monotone,
+//    so a unique fp32 maximum is the exact maximum's GPU); the exact fp64
+//    value of that GPU alone is read from the L2-resident table (all fp32-tied
+//    GPUs are read when the maximum is not unique) and added to the serial
+//    chain exactly as the reference sums (_util.py:8-18).
+//
+// Bit-exact with score_layers_kernel and the oracle by construction.
+#include <cuda_fp16.h>
+
+#include <vector>
+
+#include "gem_common.cuh"
+#include "tc.cuh"
+
+namespace gem {
+
+__global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, int64_t T, int E, int n,
+                                  int32_t* __restrict__ bound);  // search.cu
+
+constexpr int kLtThreads = 256;
+constexpr int kLtN = 256;  // MMA N (candidate x GPU columns per CTA)
+
+struct LoadsTcShared {
+  uint64_t mma_bar;
+  uint32_t tmem_base;
+};
+
+// max number of experts any candidate places on one GPU, and a flag for
+// entries outside [0, G): out[0] = maxcnt, out[1] = invalid
+__global__ void cand_stats_kernel(const int8_t* __restrict__ cand, int64_t rows, int E, int G,
+                                  int32_t* __restrict__ out) {
+  extern __shared__ int32_t cs_cnt[];  // [warps][G]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int32_t* cnt = cs_cnt + (size_t)w * G;
+  for (int64_t r = (int64_t)blockIdx.x * nw + w; r < rows; r += (int64_t)gridDim.x * nw) {
+    for (int g = lane; g < G; g += 32) cnt[g] = 0;
+    __syncwarp();
+    const int8_t* m = cand + r * E;
+    for (int e = lane; e < E; e += 32) {
+      const int g = m[e];
+      if (g < 0 || g >= G) atomicExch(&out[1], 1);
+      else atomicAdd(&cnt[g], 1);
+    }
+    __syncwarp();
+    int mx = 0;
+    for (int g = lane; g < G; g += 32) mx = max(mx, cnt[g]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) atomicMax(&out[0], mx);
+    __syncwarp();
+  }
+}
+
+__global__ void lut_window_f32_kernel(const double* __restrict__ lut, int G, int64_t width, int W,
+                                      float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)G * W;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int g = (int)(i / W);
+    const int64_t n = i % W;
+    out[i] = __double2float_rn(lut[g * width + n]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pass 1: CTA = (candidate tile of CT = N/G candidates, layer of the batch);
+// loops over every 128-step tile of the layer: produce the fp16 H tile, one
+// thread issues the E/16 MMAs, all warps drain TMEM. Each CTA is serial; two
+// CTAs per SM (96 KB shared memory, 256 TMEM columns each) overlap one
+// another's load latency with the other's MMA and epilogue.
+template <int E>
+__global__ void __launch_bounds__(kLtThreads, 2)
+loads_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int G, const int8_t* __restrict__ cand, int64_t C,
+                int64_t L, int64_t layer0, int64_t Cp, uint16_t* __restrict__ loads) {
+  constexpr int KCH = E / 8;                // 16-byte K chunks (8 fp16 experts)
+  constexpr uint32_t LBO_A = 128 * 16;      // A: [KCH][128 rows][16 B]
+  constexpr uint32_t LBO_B = kLtN * 16;     // B: [KCH][N rows][16 B]
+  constexpr int A_BYTES = 128 * E * 2;
+  constexpr int B_BYTES = kLtN * E * 2;
+  extern __shared__ __align__(1024) unsigned char lt_smem[];
+  unsigned char* sa = lt_smem;
+  unsigned char* sb = lt_smem + A_BYTES;
+  LoadsTcShared* sh = reinterpret_cast<LoadsTcShared*>(sb + B_BYTES);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int CT = kLtN / G;                  // candidates per CTA
+  const int64_t c0 = (int64_t)blockIdx.x * CT;
+  const int64_t lb = blockIdx.y;            // layer within the batch
+  const int64_t l = layer0 + lb;
+  const int32_t* hl = hist + l * T * E;
+  uint16_t* out = loads + lb * T * Cp * G;
+
+  if (tid == 0) {
+    tc::mbar_init(&sh->mma_bar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<kLtN>(&sh->tmem_base);
+  // one-hot B: row r = j*G + g (candidate j of the tile, GPU g), 1.0 where cand == g
+  for (int i = tid; i < kLtN * KCH; i += blockDim.x) {
+    const int r = i / KCH, q = i % KCH;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    const int j = r / G, g = r % G;
+    if (c0 + j < C) {
+      const int8_t* m = cand + ((c0 + j) * L + l) * E + q * 8;
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+        if (m[x] == g) w[x >> 1] |= 0x3C00u << ((x & 1) * 16);
+    }
+    *reinterpret_cast<uint4*>(sb + (size_t)q * LBO_B + (size_t)r * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  tc::fence_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = sh->tmem_base;
+  const uint32_t sa_addr = tc::smem_u32(sa), sb_addr = tc::smem_u32(sb);
+  const uint32_t idesc = tc::instr_desc(/*F32*/ 1, /*F16*/ 0, /*F16*/ 0, 128, kLtN);
+  const int ntiles = (int)((T + 127) / 128);
+  const int lg = warp & 3, half = warp >> 2;
+
+  for (int i = 0; i < ntiles; ++i) {
+    // ---- H tile i: all loads in flight, then fp16 convert + K-major 16-byte stores
+    {
+      constexpr int PER = 128 * KCH / kLtThreads;  // chunks per thread (8 for E = 128)
+      int4 x[PER][2];
+#pragma unroll
+      for (int v = 0; v < PER; ++v) {
+        const int u = tid + v * kLtThreads;
+        const int row = u % 128, q = u / 128;  // lanes = consecutive rows -> 512 B contiguous stores
+        const int64_t t = (int64_t)i * 128 + row;
+        if (t < T) {
+          const int4* src = reinterpret_cast<const int4*>(hl + t * E + q * 8);
+          x[v][0] = __ldg(src);
+          x[v][1] = __ldg(src + 1);
+        } else {
+          x[v][0] = x[v][1] = make_int4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < PER; ++v) {
+        const int u = tid + v * kLtThreads;
+        const int row = u % 128, q = u / 128;
+        auto h2 = [](int a, int b) {
+          return (uint32_t)__half_as_ushort(__int2half_rn(a)) | ((uint32_t)__half_as_ushort(__int2half_rn(b)) << 16);
+        };
+        const uint4 w = make_uint4(h2(x[v][0].x, x[v][0].y), h2(x[v][0].z, x[v][0].w), h2(x[v][1].x, x[v][1].y),
+                                   h2(x[v][1].z, x[v][1].w));
+        *reinterpret_cast<uint4*>(sa + (size_t)q * LBO_A + (size_t)row * 16) = w;
+      }
+    }
+    tc::fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc::tc_fence_after();
+#pragma unroll
+      for (int k = 0; k < E / 16; ++k) {
+        const uint64_t ad = tc::smem_desc(sa_addr + k * 2 * LBO_A, LBO_A, 128);
+        const uint64_t bd = tc::smem_desc(sb_addr + k * 2 * LBO_B, LBO_B, 128);
+        tc::mma_f16(tmem, ad, bd, idesc, k > 0 ? 1u : 0u);
+      }
+      tc::mma_commit(&sh->mma_bar);
+    }
+    tc::mbar_wait(&sh->mma_bar, (uint32_t)(i & 1));
+    tc::tc_fence_after();
+    // ---- epilogue: warp w drains TMEM lanes 32(w%4).. and column half w/4, two
+    // 32-column loads in flight, exact fp32 integers -> uint16 pairs
+    {
+      const int64_t t = (int64_t)i * 128 + lg * 32 + lane;
+      const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16);
+      uint16_t* orow = out + (t * Cp + c0) * G;
+#pragma unroll
+      for (int col = half * (kLtN / 2); col < (half + 1) * (kLtN / 2); col += 64) {
+        uint32_t v0[32], v1[32];
+        tc::tmem_ld32(trow + col, v0);
+        tc::tmem_ld32(trow + col + 32, v1);
+        tc::tmem_ld_wait();
+        if (t < T) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int x = 0; x < 16; ++x) {
+            // exact integers < 2^16: adding 2^23 puts them in the low mantissa bits
+            pk[x] = __byte_perm(__float_as_uint(__uint_as_float(v0[2 * x]) + 8388608.0f),
+                                __float_as_uint(__uint_as_float(v0[2 * x + 1]) + 8388608.0f), 0x5410);
+            pk[16 + x] = __byte_perm(__float_as_uint(__uint_as_float(v1[2 * x]) + 8388608.0f),
+                                     __float_as_uint(__uint_as_float(v1[2 * x + 1]) + 8388608.0f), 0x5410);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(orow + col);  // G | 256: whole 64-column chunks
+#pragma unroll
+          for (int x = 0; x < 8; ++x) dst[x] = make_uint4(pk[4 * x], pk[4 * x + 1], pk[4 * x + 2], pk[4 * x + 3]);
+        }
+      }
+    }
+    tc::tc_fence_before();
+    __syncthreads();  // TMEM and the H tile are free for tile i+1
+  }
+  if (warp == 0) tc::tmem_dealloc<kLtN>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// pass 2: thread = (candidate, layer of the batch), serial over t
+constexpr int kEpiThreads = 1024;  // one CTA per SM: the table window takes most of shared memory
+
+template <int GM>
+__global__ void __launch_bounds__(kEpiThreads, 1)
+score_epi_kernel(const uint16_t* __restrict__ loads, int64_t T, int G, int64_t C, int64_t Cp, int64_t L,
+                 int64_t layer0, int W, const float* __restrict__ lut32w, const double* __restrict__ lut,
+                 int64_t nmax, double* __restrict__ layer_scores, int32_t* __restrict__ err) {
+  extern __shared__ float s_lut[];  // [G][W]
+  for (int i = threadIdx.x; i < G * W; i += blockDim.x) s_lut[i] = lut32w[i];
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t lb = blockIdx.y;
+  if (c >= C) return;
+  const int64_t width = nmax + 1;
+  const uint16_t* p = loads + (lb * T * Cp + c) * G;
+  const int64_t stride = Cp * G;
+  const bool vec = GM == 8 && G == 8;
+  // table row g of the window starts at s_lut + roff[g]; the fp64 row at lut + goff[g]
+  int roff[GM];
+  int64_t goff[GM];
+#pragma unroll
+  for (int g = 0; g < GM; ++g) {
+    roff[g] = g < G ? g * W : 0;
+    goff[g] = g < G ? g * width : 0;
+  }
+  auto fetch = [&](int64_t t) -> uint4 {
+    return t < T ? *reinterpret_cast<const uint4*>(p + t * stride) : make_uint4(0u, 0u, 0u, 0u);
+  };
+  // exact per-step maximum of step t from its loads (issues the fp64 table read):
+  // branch-free arg-max of the fp32 window values, `second` = best of the others
+  auto step_max = [&](int64_t t, uint4 v) -> double {
+    uint32_t n[GM];
+    if (vec) {
+      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { n[2 * q] = w4[q] & 0xffffu; n[2 * q + 1] = w4[q] >> 16; }
+    } else {
+#pragma unroll
+      for (int g = 0; g < GM; ++g) n[g] = g < G ? p[t * stride + g] : 0u;
+    }
+    float best = s_lut[roff[0] + n[0]];
+    float second = -1.0f;
+    int64_t off = goff[0] + n[0];
+#pragma unroll
+    for (int g = 1; g < GM; ++g) {
+      if (g < G) {  // G is uniform: no divergence
+        const float x = s_lut[roff[g] + n[g]];
+        const bool gt = x > best;
+        second = gt ? best : fmaxf(second, x);
+        off = gt ? goff[g] + n[g] : off;
+        best = fmaxf(best, x);
+      }
+    }
+    double m = __ldg(lut + off);
+    if (second == best) {  // rare: several GPUs share the fp32 maximum -> exact maximum among them
+#pragma unroll
+      for (int g = 0; g < GM; ++g) {
+        if (g < G && s_lut[roff[g] + n[g]] == best) {
+          const double v2 = __ldg(lut + goff[g] + n[g]);
+          m = v2 > m ? v2 : m;
+        }
+      }
+    }
+    return m;
+  };
+  // software pipeline: loads four steps ahead, the table value one step ahead of
+  // the serial fp64 chain (which stays in t order); unrolled by 4 so the load
+  // ring needs no register moves
+  uint4 q0 = vec ? fetch(0) : uint4{}, q1 = vec ? fetch(1) : uint4{}, q2 = vec ? fetch(2) : uint4{},
+        q3 = vec ? fetch(3) : uint4{};
+  double m_next = step_max(0, q0);
+  double s = 0.0;
+  int64_t t = 0;
+  for (; t + 4 <= T; t += 4) {
+    double m = m_next;
+    if (vec) q0 = fetch(t + 4);
+    m_next = step_max(t + 1, q1);
+    s = dadd(s, m);
+    m = m_next;
+    if (vec) q1 = fetch(t + 5);
+    m_next = step_max(t + 2, q2);
+    s = dadd(s, m);
+    m = m_next;
+    if (vec) q2 = fetch(t + 6);
+    m_next = step_max(t + 3, q3);
+    s = dadd(s, m);
+    m = m_next;
+    if (vec) q3 = fetch(t + 7);
+    if (t + 4 < T) m_next = step_max(t + 4, q0);
+    s = dadd(s, m);
+  }
+  // tail (T % 4 steps): q0..q2 hold steps t+1.. already fetched; m_next is step t
+  for (int r = 0; t < T; ++t, ++r) {
+    const double m = m_next;
+    if (t + 1 < T) m_next = step_max(t + 1, r == 0 ? q1 : (r == 1 ? q2 : q3));
+    s = dadd(s, m);
+  }
+  layer_scores[c * L + layer0 + lb] = s;
+}
+
+}  // namespace gem
+
+using namespace gem;
+
+// The tensor-core scorer. Returns GEM_OK when it ran, 1 when its preconditions
+// do not hold (the caller then runs the CUDA-core scorer), <0 on error.
+extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G, const int8_t* cand,
+                                  int64_t C, const double* lut, int64_t nmax, double* layer_scores,
+                                  int32_t* err_flag, void* stream) {
+  if (!(E == 64 || E == 128) || G < 1 || G > 32 || (kLtN % G) != 0) return 1;
+  if (T < 1 || C < 1 || nmax < 0) return 1;
+  cudaStream_t st = as_stream(stream);
+  keep_pool();
+  int dev = 0, optin = 0;
+  GEM_CHECK_CUDA(cudaGetDevice(&dev));
+  GEM_CHECK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  // ---- bounds: experts per GPU, load window, largest count (one host sync)
+  int32_t* scratch = nullptr;  // [2] cand stats, [L] top-maxcnt bound, [L] max count
+  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), (size_t)(2 + 2 * L) * 4, st));
+  struct Free {
+    int32_t* p;
+    cudaStream_t s;
+    ~Free() { cudaFreeAsync(p, s); }
+  } free_scratch{scratch, st};
+  GEM_CHECK_CUDA(cudaMemsetAsync(scratch, 0, (size_t)(2 + 2 * L) * 4, st));
+  cand_stats_kernel<<<(unsigned)imin64((C * L + 7) / 8, 16 * num_sms()), 256, (size_t)8 * G * 4, st>>>(
+      cand, C * L, E, G, scratch);
+  GEM_CHECK_LAUNCH("cand_stats_kernel");
+  int32_t cs[2] = {0, 0};
+  GEM_CHECK_CUDA(cudaMemcpyAsync(cs, scratch, 8, cudaMemcpyDeviceToHost, st));
+  GEM_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (cs[1]) return 1;  // invalid entries: the CUDA-core scorer reports them
+  const int maxcnt = cs[0] < 1 ? 1 : cs[0];
+  const int warps = 8;
+  const unsigned tb_grid = (unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms());
+  topn_bound_kernel<<<tb_grid, warps * 32, (size_t)warps * E * 4, st>>>(hist, L, T, E, maxcnt, scratch + 2);
+  GEM_CHECK_LAUNCH("topn_bound_kernel");
+  topn_bound_kernel<<<tb_grid, warps * 32, (size_t)warps * E * 4, st>>>(hist, L, T, E, 1, scratch + 2 + L);
+  GEM_CHECK_LAUNCH("topn_bound_kernel");
+  std::vector<int32_t> bnd((size_t)2 * L);
+  GEM_CHECK_CUDA(cudaMemcpyAsync(bnd.data(), scratch + 2, (size_t)2 * L * 4, cudaMemcpyDeviceToHost, st));
+  GEM_CHECK_CUDA(cudaStreamSynchronize(st));
+  int64_t U = 0, hmax = 0;
+  for (int64_t l = 0; l < L; ++l) {
+    U = imax64(U, bnd[l]);
+    hmax = imax64(hmax, bnd[L + l]);
+  }
+  if (hmax > 2048 || U > nmax || U >= 65536) return 1;  // fp16 / uint16 exactness, table range
+  const int W = (int)U + 1;
+  const size_t epi_smem = (size_t)G * W * 4;
+  if (epi_smem > (size_t)optin) return 1;
+
+  // ---- fp32 table window
+  float* lut32w = nullptr;
+  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&lut32w), epi_smem, st));
+  struct FreeF {
+    float* p;
+    cudaStream_t s;
+    ~FreeF() { cudaFreeAsync(p, s); }
+  } free_lut{lut32w, st};
+  lut_window_f32_kernel<<<(unsigned)imin64(((int64_t)G * W + 255) / 256, 4096), 256, 0, st>>>(lut, G, nmax + 1, W,
+                                                                                             lut32w);
+  GEM_CHECK_LAUNCH("lut_window_f32_kernel");
+
+  // ---- layer batches: P layers of uint16 loads [P][T][Cp][G] in flight (<= ~24 GB)
+  const int CT = kLtN / G;
+  const int64_t ntile = (C + CT - 1) / CT;
+  const int64_t Cp = ntile * CT;
+  const size_t per_layer = (size_t)T * Cp * G * 2;
+  // enough layers in flight that pass 2 (one 1024-thread CTA per SM) fills every SM
+  int64_t P = (int64_t)(40ull << 30) / (int64_t)per_layer;
+  const int64_t ctas_per_layer = (C + kEpiThreads - 1) / kEpiThreads;
+  const int64_t want = (num_sms() + ctas_per_layer - 1) / ctas_per_layer;
+  P = imin64(imin64(P, want), L);
+  if (P < 1) return 1;
+  uint16_t* loads = nullptr;
+  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&loads), per_layer * P, st));
+  struct FreeU {
+    uint16_t* p;
+    cudaStream_t s;
+    ~FreeU() { cudaFreeAsync(p, s); }
+  } free_loads{loads, st};
+
+  const size_t lt_smem = (size_t)128 * E * 2 + (size_t)kLtN * E * 2 + sizeof(LoadsTcShared);
+  auto k1 = E == 128 ? loads_tc_kernel<128> : loads_tc_kernel<64>;
+  GEM_CHECK_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lt_smem));
+  const int GM = G <= 8 ? 8 : (G <= 16 ? 16 : 32);
+  auto k2 = GM == 8 ? score_epi_kernel<8> : (GM == 16 ? score_epi_kernel<16> : score_epi_kernel<32>);
+  GEM_CHECK_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)epi_smem));
+  for (int64_t l0 = 0; l0 < L; l0 += P) {
+    const int64_t nb = imin64(P, L - l0);
+    k1<<<dim3((unsigned)ntile, (unsigned)nb), kLtThreads, lt_smem, st>>>(hist, T, G, cand, C, L, l0, Cp, loads);
+    GEM_CHECK_LAUNCH("loads_tc_kernel");
+    k2<<<dim3((unsigned)ctas_per_layer, (unsigned)nb), kEpiThreads, epi_smem, st>>>(loads, T, G, C, Cp, L, l0, W, lut32w,
+                                                                               lut, nmax, layer_scores, err_flag);
+    GEM_CHECK_LAUNCH("score_epi_kernel");
+  }
+  return GEM_OK;
+}

@@ -1172,6 +1172,7 @@ struct Screen {
 static int prepare_screen(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G, const double* lut,
                           int64_t nmax, Screen& sc, SearchWs& ws, cudaStream_t st) {
   sc.st = st;
+  keep_pool();
   if (G < 2 || T > (1LL << 24)) return GEM_OK;
   const int64_t n = (int64_t)G * (nmax + 1);
   GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.lut32), (size_t)n * sizeof(float), st));

@@ -218,6 +218,54 @@ def test_score_candidates_batch_matches_oracle(oracle):
         assert total[c] == s
 
 
+@pytest.mark.parametrize("L,T,E,G,C,high,balanced", [(2, 300, 128, 8, 100, 120, True), (3, 129, 64, 8, 70, 400, True),
+                                                      (1, 1000, 128, 4, 33, 60, True), (2, 77, 64, 16, 40, 300, True),
+                                                      (2, 200, 128, 8, 45, 90, False), (1, 64, 128, 1, 5, 50, True)])
+def test_score_batch_tensor_cores_vs_cuda_cores(oracle, L, T, E, G, C, high, balanced):
+    """K5 v2 (tcgen05 one-hot loads + screened exact maximum) == K5 v1 == oracle, bit for bit:
+    ragged T and candidate tiles, G = 1/4/8/16, unbalanced candidate tables."""
+    from paper_2605_19945_b200 import _device, _lib
+
+    rng = np.random.default_rng(L * 1000 + T + E + G)
+    tok = np.stack([random_counts(rng, T, E, high=high) for _ in range(L)])
+    p = mixed_profile(gem, rng, G) if G > 1 else staircase_profile(gem, rng, 1, tile=64, tiles=256)
+    if balanced:
+        cand = np.stack([[balanced_assignment(rng, E, G) for _ in range(L)] for _ in range(C)])
+    else:
+        cand = rng.integers(0, G, (C, L, E))
+    hist, nmax = _device.counts_to_device_int32(tok)
+    dc = _device.DeviceCurves.from_profile(p)
+    lut = dc.lut(nmax)
+    cd = torch.from_numpy(cand.astype(np.int8)).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    out = {}
+    for fn in ("gem_score_batch_tc", "gem_score_batch_v1"):
+        ls = torch.zeros((C, L), dtype=torch.float64, device="cuda")
+        err = torch.zeros((1,), dtype=torch.int32, device="cuda")
+        rc = getattr(_lib.lib(), fn)(hist.data_ptr(), L, T, E, G, cd.data_ptr(), C, lut.data_ptr(), dc.lut_nmax,
+                                     ls.data_ptr(), err.data_ptr(), st)
+        assert rc == 0, (fn, rc, _lib.lib().gem_last_error())
+        assert int(err.item()) == 0
+        out[fn] = ls.cpu().numpy()
+    assert np.array_equal(out["gem_score_batch_tc"], out["gem_score_batch_v1"])
+    cv = oracle.Curves.from_profile(p)
+    for c in range(0, C, 11):
+        assert out["gem_score_batch_tc"][c].tolist() == [oracle.score(tok[l], cand[c, l], cv) for l in range(L)]
+
+
+def test_score_batch_tc_declines_unsupported_shapes():
+    from paper_2605_19945_b200 import _device, _lib
+
+    tok = np.ones((1, 10, 32), dtype=np.int64)
+    hist, nmax = _device.counts_to_device_int32(tok)
+    cd = torch.zeros((3, 1, 32), dtype=torch.int8, device="cuda")
+    lut = torch.zeros((4, nmax + 1), dtype=torch.float64, device="cuda")
+    ls = torch.zeros((3, 1), dtype=torch.float64, device="cuda")
+    err = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    assert _lib.lib().gem_score_batch_tc(hist.data_ptr(), 1, 10, 32, 4, cd.data_ptr(), 3, lut.data_ptr(), nmax,
+                                         ls.data_ptr(), err.data_ptr(), None) == 1  # E = 32: not on this path
+
+
 # ------------------------------------------------------ protocol (tier 1 ABI)
 
 def test_protocol_golden():
