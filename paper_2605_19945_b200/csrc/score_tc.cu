@@ -93,14 +93,20 @@ __global__ void __launch_bounds__(kLtThreads, 2)
 loads_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int G, const int8_t* __restrict__ cand, int64_t C,
                 int64_t L, int64_t layer0, int64_t Cp, uint16_t* __restrict__ loads) {
   constexpr int KCH = E / 8;                // 16-byte K chunks (8 fp16 experts)
-  constexpr uint32_t LBO_A = 128 * 16;      // A: [KCH][128 rows][16 B]
+  constexpr uint32_t LBO_A = 128 * 16 + 16; // A: [KCH][128 rows][16 B], K slices padded by 16 B (bank spread)
   constexpr uint32_t LBO_B = kLtN * 16;     // B: [KCH][N rows][16 B]
-  constexpr int A_BYTES = 128 * E * 2;
+  constexpr int A_BYTES = (int)LBO_A * KCH;
   constexpr int B_BYTES = kLtN * E * 2;
+  constexpr int STG_ROW = 80;                // epilogue staging row: 64 B + 16 B pad (conflict-free)
   extern __shared__ __align__(1024) unsigned char lt_smem[];
   unsigned char* sa = lt_smem;
   unsigned char* sb = lt_smem + A_BYTES;
+  // epilogue staging [8 warps][32 rows][STG_ROW]: the H tile's space (free once the
+  // tile's MMAs completed) when it is large enough, else its own block
+  constexpr int STG_BYTES = 8 * 32 * STG_ROW;
+  constexpr bool STG_IN_A = STG_BYTES <= A_BYTES;
   LoadsTcShared* sh = reinterpret_cast<LoadsTcShared*>(sb + B_BYTES);
+  unsigned char* stg = STG_IN_A ? sa : sb + B_BYTES + 64;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int CT = kLtN / G;                  // candidates per CTA
@@ -139,33 +145,28 @@ loads_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int G, const int8_t
   const int lg = warp & 3, half = warp >> 2;
 
   for (int i = 0; i < ntiles; ++i) {
-    // ---- H tile i: all loads in flight, then fp16 convert + K-major 16-byte stores
+    // ---- H tile i: each warp reads whole 512-byte rows (coalesced), all of its
+    // rows in flight, then fp16 convert + 8-byte K-major stores
     {
-      constexpr int PER = 128 * KCH / kLtThreads;  // chunks per thread (8 for E = 128)
-      int4 x[PER][2];
+      constexpr int RPW = 128 / (kLtThreads / 32);  // rows per warp (16)
+      constexpr int LPR = E / 4;                     // lanes per row (4 experts each)
+      constexpr int RPI = 32 / LPR;                  // rows per warp instruction
+      int4 x[RPW / RPI];
 #pragma unroll
-      for (int v = 0; v < PER; ++v) {
-        const int u = tid + v * kLtThreads;
-        const int row = u % 128, q = u / 128;  // lanes = consecutive rows -> 512 B contiguous stores
+      for (int v = 0; v < RPW / RPI; ++v) {
+        const int row = warp * RPW + v * RPI + lane / LPR;
         const int64_t t = (int64_t)i * 128 + row;
-        if (t < T) {
-          const int4* src = reinterpret_cast<const int4*>(hl + t * E + q * 8);
-          x[v][0] = __ldg(src);
-          x[v][1] = __ldg(src + 1);
-        } else {
-          x[v][0] = x[v][1] = make_int4(0, 0, 0, 0);
-        }
+        x[v] = t < T ? __ldg(reinterpret_cast<const int4*>(hl + t * E) + (lane % LPR)) : make_int4(0, 0, 0, 0);
       }
 #pragma unroll
-      for (int v = 0; v < PER; ++v) {
-        const int u = tid + v * kLtThreads;
-        const int row = u % 128, q = u / 128;
+      for (int v = 0; v < RPW / RPI; ++v) {
+        const int row = warp * RPW + v * RPI + lane / LPR;
+        const int e4 = lane % LPR;  // experts 4*e4 .. 4*e4+3
         auto h2 = [](int a, int b) {
           return (uint32_t)__half_as_ushort(__int2half_rn(a)) | ((uint32_t)__half_as_ushort(__int2half_rn(b)) << 16);
         };
-        const uint4 w = make_uint4(h2(x[v][0].x, x[v][0].y), h2(x[v][0].z, x[v][0].w), h2(x[v][1].x, x[v][1].y),
-                                   h2(x[v][1].z, x[v][1].w));
-        *reinterpret_cast<uint4*>(sa + (size_t)q * LBO_A + (size_t)row * 16) = w;
+        *reinterpret_cast<uint2*>(sa + (size_t)(e4 >> 1) * LBO_A + (size_t)row * 16 + (e4 & 1) * 8) =
+            make_uint2(h2(x[v].x, x[v].y), h2(x[v].z, x[v].w));
       }
     }
     tc::fence_async_smem();
@@ -182,32 +183,36 @@ loads_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int G, const int8_t
     }
     tc::mbar_wait(&sh->mma_bar, (uint32_t)(i & 1));
     tc::tc_fence_after();
-    // ---- epilogue: warp w drains TMEM lanes 32(w%4).. and column half w/4, two
-    // 32-column loads in flight, exact fp32 integers -> uint16 pairs
+    // ---- epilogue: warp w drains TMEM lanes 32(w%4).. and column half w/4 in
+    // 32-column chunks (exact fp32 integers -> uint16 pairs), transposes each
+    // chunk through its shared staging block and writes 8 rows x 64 B per store
     {
-      const int64_t t = (int64_t)i * 128 + lg * 32 + lane;
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16);
-      uint16_t* orow = out + (t * Cp + c0) * G;
-#pragma unroll
-      for (int col = half * (kLtN / 2); col < (half + 1) * (kLtN / 2); col += 64) {
-        uint32_t v0[32], v1[32];
-        tc::tmem_ld32(trow + col, v0);
-        tc::tmem_ld32(trow + col + 32, v1);
+      unsigned char* wst = stg + warp * 32 * STG_ROW;
+      const int64_t tbase = (int64_t)i * 128 + lg * 32;
+#pragma unroll 1
+      for (int col = half * (kLtN / 2); col < (half + 1) * (kLtN / 2); col += 32) {
+        uint32_t v[32];
+        tc::tmem_ld32(trow + col, v);
         tc::tmem_ld_wait();
-        if (t < T) {
-          uint32_t pk[32];
+        uint32_t pk[16];
 #pragma unroll
-          for (int x = 0; x < 16; ++x) {
-            // exact integers < 2^16: adding 2^23 puts them in the low mantissa bits
-            pk[x] = __byte_perm(__float_as_uint(__uint_as_float(v0[2 * x]) + 8388608.0f),
-                                __float_as_uint(__uint_as_float(v0[2 * x + 1]) + 8388608.0f), 0x5410);
-            pk[16 + x] = __byte_perm(__float_as_uint(__uint_as_float(v1[2 * x]) + 8388608.0f),
-                                     __float_as_uint(__uint_as_float(v1[2 * x + 1]) + 8388608.0f), 0x5410);
-          }
-          uint4* dst = reinterpret_cast<uint4*>(orow + col);  // G | 256: whole 64-column chunks
+        for (int x = 0; x < 16; ++x)  // exact integers < 2^16: + 2^23 puts them in the low mantissa bits
+          pk[x] = __byte_perm(__float_as_uint(__uint_as_float(v[2 * x]) + 8388608.0f),
+                              __float_as_uint(__uint_as_float(v[2 * x + 1]) + 8388608.0f), 0x5410);
 #pragma unroll
-          for (int x = 0; x < 8; ++x) dst[x] = make_uint4(pk[4 * x], pk[4 * x + 1], pk[4 * x + 2], pk[4 * x + 3]);
+        for (int x = 0; x < 4; ++x)
+          *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x * 16) =
+              make_uint4(pk[4 * x], pk[4 * x + 1], pk[4 * x + 2], pk[4 * x + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = j * 8 + lane / 4, piece = lane % 4;
+          const int64_t t = tbase + r;
+          const uint4 w = *reinterpret_cast<const uint4*>(wst + r * STG_ROW + piece * 16);
+          if (t < T) *reinterpret_cast<uint4*>(out + (t * Cp + c0) * G + col + piece * 8) = w;
         }
+        __syncwarp();
       }
     }
     tc::tc_fence_before();
@@ -401,7 +406,8 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
     ~FreeU() { cudaFreeAsync(p, s); }
   } free_loads{loads, st};
 
-  const size_t lt_smem = (size_t)128 * E * 2 + (size_t)kLtN * E * 2 + sizeof(LoadsTcShared);
+  const size_t a_bytes = (size_t)(128 * 16 + 16) * (E / 8), stg_bytes = 8 * 32 * 80;
+  const size_t lt_smem = a_bytes + (size_t)kLtN * E * 2 + 64 + (stg_bytes <= a_bytes ? 0 : stg_bytes);
   auto k1 = E == 128 ? loads_tc_kernel<128> : loads_tc_kernel<64>;
   GEM_CHECK_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lt_smem));
   const int GM = G <= 8 ? 8 : (G <= 16 ? 16 : 32);
