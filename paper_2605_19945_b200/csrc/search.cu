@@ -15,6 +15,8 @@
 //    exactly eval_one(g, n), so lat == C_g(loads) as in latency_matrix();
 //  * convergence: stop unless found && cand < score && 1-cand/score >= thr,
 //    then the full rescore must equal cand bit for bit (search.py:236).
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "gem_common.cuh"
@@ -54,6 +56,8 @@ struct SearchWs {
   int64_t Tp;          // T rounded up to 32 (whole 16-byte pieces for every chunk of the transposed arrays)
   const float* lut32;  // [G][nmax+1] fp32 rounding of the latency table (set by the driver)
   const uint16_t* ht16;  // [L][E][Tp] transposed counts (set by the driver when every count < 65536)
+  const uint16_t* ht16s; // [L][E][Tp] the same counts times 4 (byte offsets into fp32 rows; 4U < 65536)
+  int32_t lut_monotone;  // every fp32 table row is nondecreasing (set by the driver)
 };
 
 constexpr int kLocK = 8;
@@ -91,6 +95,8 @@ static size_t carve(SearchWs* ws, void* base, int64_t R, int64_t T, int G) {
   w.loadT = (uint16_t*)take((size_t)R * G * w.Tp * 2);
   w.lut32 = nullptr;
   w.ht16 = nullptr;
+  w.ht16s = nullptr;
+  w.lut_monotone = 0;
   if (ws) *ws = w;
   return off;
 }
@@ -223,7 +229,7 @@ __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, i
 
 // transposed uint16 copy of the histogram: ht[l][e][t] = hist[l][t][e] for
 // t < T, 0 for T <= t < Tp (every count <= U < 65536 on this path)
-__global__ void hist_t16_kernel(const int32_t* __restrict__ hist, int64_t T, int64_t Tp, int E,
+__global__ void hist_t16_kernel(const int32_t* __restrict__ hist, int64_t T, int64_t Tp, int E, int shift,
                                 uint16_t* __restrict__ ht) {
   __shared__ uint16_t tile[32][33];
   const int64_t l = blockIdx.z;
@@ -233,7 +239,7 @@ __global__ void hist_t16_kernel(const int32_t* __restrict__ hist, int64_t T, int
   for (int k = ty; k < 32; k += 8) {
     const int64_t t = t0 + k;
     const int e = e0 + tx;
-    tile[k][tx] = (t < T && e < E) ? (uint16_t)hist[(l * T + t) * E + e] : (uint16_t)0;
+    tile[k][tx] = (t < T && e < E) ? (uint16_t)(hist[(l * T + t) * E + e] << shift) : (uint16_t)0;
   }
   __syncthreads();
   for (int k = ty; k < 32; k += 8) {
@@ -844,14 +850,291 @@ approx_scan_kernel(int64_t T, int E, int G, int64_t nmax, const int32_t* __restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// K6 v5: the screened scan with fp32 chunk sums and conflict-free staging.
+//
+// ncu on v4: shared-memory wavefronts at 95% of peak, 8.1 wavefronts per warp
+// pair-step, of which the two table gathers are 5.4 (random rows: ~2.7-way
+// bank conflicts) and the count-row loads 2.2 (64-byte row stride puts the
+// rows of one warp on the same banks); 15.5 instructions per pair-step
+// (address arithmetic, u16 unpacking, F2F + DADD per term).
+//
+// v5 keeps v4's CTA layout and the exact second pass, and changes the inner loop:
+//  * count rows are staged with an 80-byte stride and a thread's y experts are
+//    interleaved (y = yg + q*ng), so the 8 x rows and the 4 y rows a warp reads
+//    at one step sit on distinct banks; 4 steps per 64-bit load;
+//  * counts are pre-scaled by 4 (byte offsets: ht16s), so a gather address is
+//    ONE add: (table base + 4 l_a - 4 h_x) + 4 h_y;
+//  * each term m' = fl32(m) (exact rounding of the exact maximum, as in v4) is
+//    summed in fp32 over a 32-step chunk and the chunk sum is added to an
+//    fp64 chain: |cand' - cand| <= (32 * 2^-24 + (T/32) 2^-53) cand < 2^-18.9
+//    cand for nonnegative tables, so the exact winner lies inside
+//    cand' <= min' * (1 + 2^-16) (kWindow5). Steps past T are zero rows and
+//    add exactly 0 (C_g(0) = 0, pother' = 0).
+constexpr double kWindow5 = 1.0 + 1.0 / 65536.0;
+constexpr int kSwap5RowU16 = kSwap3TChunk + 8;  // staged count row: 32 steps + 16-byte pad (80 B)
+
+__host__ __device__ inline size_t swap5_buf_bytes(const Swap3Geom& g, int G) {
+  return (size_t)g.rpc * ((size_t)(g.n + g.nb_pad) * kSwap5RowU16 * 2 + 2 * (size_t)kSwap3TChunk * 2 +
+                          4 * ((size_t)G + 3) * kSwap3TChunk);
+}
+
+__host__ __device__ inline size_t swap5_smem(int E, int G, int64_t nmax) {
+  const Swap3Geom g = swap3_geom(E, G);
+  const size_t lut = ((size_t)2 * (size_t)(nmax + 1) * 4 + 15) & ~size_t(15);
+  const size_t fixed = (size_t)g.rpc * (8 + 8 + 8 + 8 + 2 * g.n * 2) + 64;
+  return lut + 2 * swap5_buf_bytes(g, G) + fixed;
+}
+
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
+__global__ void __launch_bounds__(kSwap3Threads, 2)
+approx_scan5_kernel(int E, int G, int64_t nmax, int monotone, const int32_t* __restrict__ run_layer,
+                    const int8_t* __restrict__ assign, int32_t n_active, SearchWs ws) {
+  extern __shared__ __align__(16) unsigned char s5[];
+  const Swap3Geom geo = swap3_geom(E, G);
+  const int n = geo.n, ng = geo.ng, RPC = geo.rpc, nb_pad = geo.nb_pad;
+  const int NP = G * (G - 1) / 2;
+  const int slot0 = blockIdx.y * RPC;
+  if (slot0 >= n_active) return;
+  const int nruns = min(RPC, n_active - slot0);
+  int p = blockIdx.x, a = 0;
+  while (p >= G - 1 - a) { p -= G - 1 - a; ++a; }
+  const int b = a + 1 + p;
+  const int64_t width = nmax + 1;
+  const int64_t Tp = ws.Tp;
+  constexpr int TC = kSwap3TChunk;
+  constexpr int RS = kSwap5RowU16;
+  constexpr int V = TC * 2 / 16;  // 16-byte pieces per uint16 row of a chunk
+  constexpr int VF = TC * 4 / 16; // 16-byte pieces per fp32 row of a chunk
+  const int hrows = n + nb_pad;   // a-expert rows, then b-expert rows (zero padded)
+
+  float* lut_a = reinterpret_cast<float*>(s5);
+  float* lut_b = lut_a + width;
+  unsigned char* cur = s5 + (((size_t)2 * width * 4 + 15) & ~size_t(15));
+  const size_t buf_bytes = swap5_buf_bytes(geo, G);
+  unsigned char* bufs = cur;
+  cur += 2 * buf_bytes;
+  unsigned long long* smin = reinterpret_cast<unsigned long long*>(cur);  cur += (size_t)RPC * 8;
+  const uint16_t** hsrc = reinterpret_cast<const uint16_t**>(cur);       cur += (size_t)RPC * 8;
+  const uint16_t** lsrc = reinterpret_cast<const uint16_t**>(cur);       cur += (size_t)RPC * 8;
+  const float** fsrc = reinterpret_cast<const float**>(cur);             cur += (size_t)RPC * 8;
+  int16_t* lists = reinterpret_cast<int16_t*>(cur);                       // [RPC][2][n]
+  struct Buf {
+    uint16_t* h;   // [RPC][hrows][RS]  4 * count
+    uint16_t* l;   // [RPC][2][TC]      l_a, l_b
+    float* lat;    // [RPC][G][TC]
+    float* po;     // [RPC][TC]
+    uint32_t* th;  // [RPC][2][TC]  clamp addresses into the a and b rows
+  };
+  auto buf_at = [&](int k) {
+    unsigned char* c = bufs + k * buf_bytes;
+    Buf B;
+    B.h = reinterpret_cast<uint16_t*>(c);  c += (size_t)RPC * hrows * RS * 2;
+    B.l = reinterpret_cast<uint16_t*>(c);  c += (size_t)RPC * 2 * TC * 2;
+    B.lat = reinterpret_cast<float*>(c);   c += (size_t)RPC * G * TC * 4;
+    B.po = reinterpret_cast<float*>(c);    c += (size_t)RPC * TC * 4;
+    B.th = reinterpret_cast<uint32_t*>(c);
+    return B;
+  };
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  {
+    const float* la32 = ws.lut32 + (int64_t)a * width;
+    const float* lb32 = ws.lut32 + (int64_t)b * width;
+    for (int64_t i = tid; i < width; i += blockDim.x) {
+      lut_a[i] = __ldg(la32 + i);
+      lut_b[i] = __ldg(lb32 + i);
+    }
+  }
+  if (tid < RPC) smin[tid] = ord_bits(__longlong_as_double(0x7ff0000000000000LL));
+  if (tid < nruns) {
+    const int r = ws.run_list[slot0 + tid];
+    hsrc[tid] = ws.ht16s + (int64_t)run_layer[r] * E * Tp;
+    lsrc[tid] = ws.loadT + (int64_t)r * G * Tp;
+    fsrc[tid] = ws.latT + (int64_t)r * G * Tp;
+  }
+  for (int w = wid; w < nruns; w += nw) {
+    const int r = ws.run_list[slot0 + w];
+    const int8_t* as = assign + (int64_t)r * E;
+    int base_a = 0, base_b = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      const int g = e < E ? as[e] : -1;
+      const unsigned ma = __ballot_sync(0xffffffffu, g == a), mb = __ballot_sync(0xffffffffu, g == b);
+      const unsigned below = (1u << lane) - 1u;
+      if (g == a) lists[(w * 2 + 0) * n + base_a + __popc(ma & below)] = (int16_t)e;
+      if (g == b) lists[(w * 2 + 1) * n + base_b + __popc(mb & below)] = (int16_t)e;
+      base_a += __popc(ma);
+      base_b += __popc(mb);
+    }
+  }
+  for (int k = 0; k < 2; ++k) {
+    const Buf B = buf_at(k);
+    for (int i = tid; i < RPC * hrows * RS; i += blockDim.x) B.h[i] = 0;
+  }
+  __syncthreads();
+
+  const int pieces_h = 2 * n * V, pieces_l = 2 * V, pieces_f = G * VF;
+  const int pieces_run = pieces_h + pieces_l + pieces_f;
+  auto issue = [&](int64_t t0, int k) {
+    const Buf B = buf_at(k);
+    for (int i = tid; i < nruns * pieces_run; i += blockDim.x) {
+      const int ss = i / pieces_run;
+      int q = i - ss * pieces_run;
+      if (q < pieces_h) {
+        const int row = q / V, v = q - row * V;  // rows [0, n): a experts; [n, 2n): b experts
+        const int e = row < n ? lists[(ss * 2 + 0) * n + row] : lists[(ss * 2 + 1) * n + row - n];
+        cp_async16(B.h + ((size_t)ss * hrows + row) * RS + v * 8, hsrc[ss] + (int64_t)e * Tp + t0 + v * 8);
+      } else if ((q -= pieces_h) < pieces_l) {
+        const int which = q / V, v = q - which * V;
+        cp_async16(B.l + ((size_t)ss * 2 + which) * TC + v * 8,
+                   lsrc[ss] + (int64_t)(which ? b : a) * Tp + t0 + v * 8);
+      } else {
+        q -= pieces_l;
+        const int g = q / VF, v = q - g * VF;
+        cp_async16(B.lat + ((size_t)ss * G + g) * TC + v * 4, fsrc[ss] + (int64_t)g * Tp + t0 + v * 4);
+      }
+    }
+  };
+
+  const uint32_t base_a = (uint32_t)__cvta_generic_to_shared(lut_a);
+  const uint32_t base_b = (uint32_t)__cvta_generic_to_shared(lut_b);
+  const int units_total = nruns * geo.units_per_run;
+  for (int pass0 = 0; pass0 < units_total; pass0 += blockDim.x) {
+    const int u = pass0 + tid;
+    const bool live = u < units_total;
+    const int s = live ? u / geo.units_per_run : 0;
+    const int ur = live ? u % geo.units_per_run : 0;
+    const int x = ur / ng, yg = ur % ng;  // y experts of this thread: yg + q*ng
+    double acc[kSwapY];
+#pragma unroll
+    for (int q = 0; q < kSwapY; ++q) acc[q] = 0.0;
+
+    issue(0, 0);
+    cp_async_commit();
+    int k = 0;
+    for (int64_t t0 = 0; t0 < Tp; t0 += TC, k ^= 1) {
+      if (t0 + TC < Tp) issue(t0 + TC, k ^ 1);
+      cp_async_commit();
+      cp_async_wait1();
+      __syncthreads();
+      const Buf B = buf_at(k);
+      // pother' and, per side, the clamp point: the largest n whose table
+      // value (monotone rows) is <= pother'. Indices below it read the clamp
+      // point instead -- a value <= pother', so every term is unchanged -- and
+      // all such lanes of a warp hit one address (broadcast, no conflict).
+      for (int rr = tid; rr < 2 * nruns * TC; rr += blockDim.x) {
+        const int side = rr >= nruns * TC;
+        const int r2 = side ? rr - nruns * TC : rr;
+        const int ss = r2 / TC, tt = r2 % TC;
+        const float* lat = B.lat + (size_t)ss * G * TC + tt;
+        float m = __int_as_float(0xff800000);  // -inf when G == 2
+        for (int g = 0; g < G; ++g)
+          if (g != a && g != b) m = fmaxf(m, lat[g * TC]);
+        if (!side) B.po[ss * TC + tt] = m;
+        const float* tab = side ? lut_b : lut_a;
+        int lo = 0;
+        if (monotone && tab[0] <= m) {
+          int hi = (int)nmax;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (tab[mid] <= m) lo = mid; else hi = mid - 1;
+          }
+        }
+        B.th[(ss * 2 + side) * TC + tt] = (side ? base_b : base_a) + 4u * (uint32_t)lo;
+      }
+      __syncthreads();
+      if (live) {
+        const float* pos = B.po + s * TC;
+        const uint32_t* tha = B.th + s * 2 * TC;
+        const uint32_t* thb = tha + TC;
+        const uint16_t* las = B.l + (size_t)s * 2 * TC;
+        const uint16_t* lbs = las + TC;
+        const uint16_t* hAs = B.h + ((size_t)s * hrows + x) * RS;
+        const uint16_t* hBs = B.h + ((size_t)s * hrows + n + yg) * RS;
+        float c[kSwapY];
+#pragma unroll
+        for (int q = 0; q < kSwapY; ++q) c[q] = 0.0f;
+#pragma unroll 2
+        for (int tt = 0; tt < TC; tt += 4) {
+          const uint2 hx2 = *reinterpret_cast<const uint2*>(hAs + tt);
+          const uint2 la2 = *reinterpret_cast<const uint2*>(las + tt);
+          const uint2 lb2 = *reinterpret_cast<const uint2*>(lbs + tt);
+          const float4 p4 = *reinterpret_cast<const float4*>(pos + tt);
+          const uint4 ta4 = *reinterpret_cast<const uint4*>(tha + tt);
+          const uint4 tb4 = *reinterpret_cast<const uint4*>(thb + tt);
+          const uint32_t taj[4] = {ta4.x, ta4.y, ta4.z, ta4.w}, tbj[4] = {tb4.x, tb4.y, tb4.z, tb4.w};
+          uint2 hy2[kSwapY];
+#pragma unroll
+          for (int q = 0; q < kSwapY; ++q) hy2[q] = *reinterpret_cast<const uint2*>(hBs + (size_t)q * ng * RS + tt);
+          const float pj[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t wx = (j < 2) ? hx2.x : hx2.y, wa = (j < 2) ? la2.x : la2.y, wb = (j < 2) ? lb2.x : lb2.y;
+            const uint32_t hx = (j & 1) ? (wx >> 16) : (wx & 0xffffu);
+            const uint32_t la = (j & 1) ? (wa >> 16) : (wa & 0xffffu);
+            const uint32_t lb = (j & 1) ? (wb >> 16) : (wb & 0xffffu);
+            const uint32_t ra = base_a + la * 4u - hx, rb = base_b + lb * 4u + hx;
+#pragma unroll
+            for (int q = 0; q < kSwapY; ++q) {
+              const uint32_t wy = (j < 2) ? hy2[q].x : hy2[q].y;
+              const uint32_t hy = (j & 1) ? (wy >> 16) : (wy & 0xffffu);
+              c[q] += fmaxf(fmaxf(pj[j], lds_f32(max(ra + hy, taj[j]))), lds_f32(max(rb - hy, tbj[j])));
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kSwapY; ++q) acc[q] = dadd(acc[q], (double)c[q]);
+      }
+      __syncthreads();  // buffer k is rewritten by the issue of the chunk after next
+    }
+    if (live) {
+      double mn = acc[0];
+#pragma unroll
+      for (int q = 1; q < kSwapY; ++q)
+        if (yg + q * ng < n) mn = fmin(mn, acc[q]);
+      atomicMin(&smin[s], ord_bits(mn));
+    }
+    __syncthreads();
+    if (live) {
+      const int r = ws.run_list[slot0 + s];
+      const int64_t tile = (int64_t)r * NP + blockIdx.x;
+      const double lim = __longlong_as_double((long long)smin[s]) * kWindow5;
+      const int xe = lists[(s * 2 + 0) * n + x];
+#pragma unroll
+      for (int q = 0; q < kSwapY; ++q) {
+        const int yi = yg + q * ng;
+        if (yi >= n || !(acc[q] <= lim)) continue;
+        const int ye = lists[(s * 2 + 1) * n + yi];
+        const int f = xe < ye ? xe * E + ye : ye * E + xe;
+        const int kk = atomicAdd(&ws.loc_cnt[tile], 1);
+        if (kk < kLocK) {
+          ws.loc_cand[tile * kLocK + kk] = acc[q];
+          ws.loc_flat[tile * kLocK + kk] = f;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < nruns) {
+    const int r = ws.run_list[slot0 + tid];
+    ws.loc_min[(int64_t)r * NP + blockIdx.x] = __longlong_as_double((long long)smin[tid]);
+  }
+}
+
 // per active run: the run's window over all GPU-pair tiles -> exact-candidate list
-__global__ void window_kernel(int32_t n_active, int G, SearchWs ws) {
+__global__ void window_kernel(int32_t n_active, int G, double window, SearchWs ws) {
   const int NP = G * (G - 1) / 2;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_active; i += gridDim.x * blockDim.x) {
     const int r = ws.run_list[i];
     double gmin = __longlong_as_double(0x7ff0000000000000LL);
     for (int p = 0; p < NP; ++p) gmin = fmin(gmin, ws.loc_min[(int64_t)r * NP + p]);
-    const double lim = gmin * kWindow;
+    const double lim = gmin * window;
     int cnt = 0, overflow = 0;
     for (int p = 0; p < NP; ++p) {
       const int64_t tile = (int64_t)r * NP + p;
@@ -950,6 +1233,15 @@ __global__ void state_t_kernel(int64_t R, int64_t T, int G, int64_t width, Searc
     }
     ws.loadT[i] = (uint16_t)l;
     ws.latT[i] = v;
+  }
+}
+
+// flag[0] = 1 when some fp32 table row decreases somewhere
+__global__ void lut_monotone_kernel(const float* __restrict__ lut32, int G, int64_t width, int32_t* __restrict__ flag) {
+  const int64_t n = (int64_t)G * width;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i % width;
+    if (k + 1 < width && !(lut32[i] <= lut32[i + 1])) atomicExch(flag, 1);
   }
 }
 
@@ -1101,12 +1393,22 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   compact_runs_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(R, ws);
   GEM_CHECK_LAUNCH("compact_runs_kernel");
   GEM_CHECK_CUDA(cudaMemsetAsync(ws.loc_cnt, 0, (size_t)R * NP * 4, st));
-  GEM_CHECK_CUDA(cudaFuncSetAttribute(approx_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   const Swap3Geom g = swap3_geom(E, G);
   dim3 grid((unsigned)NP, (unsigned)((n_active + g.rpc - 1) / g.rpc));
-  approx_scan_kernel<<<grid, kSwap3Threads, smem3, st>>>(T, E, G, nmax, run_layer, assign, (int32_t)n_active, ws);
-  GEM_CHECK_LAUNCH("approx_scan_kernel");
-  window_kernel<<<(unsigned)((n_active + 127) / 128), 128, 0, st>>>((int32_t)n_active, G, ws);
+  const size_t smem5 = swap5_smem(E, G, nmax);
+  double window = kWindow;
+  if (ws.ht16s != nullptr && smem5 <= (size_t)optin && !std::getenv("GEM_SCAN_V4")) {
+    GEM_CHECK_CUDA(cudaFuncSetAttribute(approx_scan5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
+    approx_scan5_kernel<<<grid, kSwap3Threads, smem5, st>>>(E, G, nmax, ws.lut_monotone && !std::getenv("GEM_SCAN_NOCLAMP"),
+                                                             run_layer, assign, (int32_t)n_active, ws);
+    GEM_CHECK_LAUNCH("approx_scan5_kernel");
+    window = kWindow5;
+  } else {
+    GEM_CHECK_CUDA(cudaFuncSetAttribute(approx_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+    approx_scan_kernel<<<grid, kSwap3Threads, smem3, st>>>(T, E, G, nmax, run_layer, assign, (int32_t)n_active, ws);
+    GEM_CHECK_LAUNCH("approx_scan_kernel");
+  }
+  window_kernel<<<(unsigned)((n_active + 127) / 128), 128, 0, st>>>((int32_t)n_active, G, window, ws);
   GEM_CHECK_LAUNCH("window_kernel");
   const int64_t warps = n_active * kCandK;
   exact_pairs_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(hist, T, E, G, lut, nmax, run_layer,
@@ -1161,11 +1463,13 @@ static int launch_greedy(const int32_t* hist, int64_t T, int32_t E, int32_t G, c
 struct Screen {
   float* lut32 = nullptr;
   uint16_t* ht16 = nullptr;
+  uint16_t* ht16s = nullptr;
   int64_t U = 0;
   cudaStream_t st = nullptr;
   ~Screen() {
     if (lut32) cudaFreeAsync(lut32, st);
     if (ht16) cudaFreeAsync(ht16, st);
+    if (ht16s) cudaFreeAsync(ht16s, st);
   }
 };
 
@@ -1181,26 +1485,35 @@ static int prepare_screen(const int32_t* hist, int64_t L, int64_t T, int32_t E, 
   ws.lut32 = sc.lut32;
   // U = max over layers and steps of the sum of the E/G largest counts
   int32_t* bound = nullptr;
-  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bound), (size_t)L * 4, st));
-  GEM_CHECK_CUDA(cudaMemsetAsync(bound, 0, (size_t)L * 4, st));
+  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bound), (size_t)(L + 1) * 4, st));
+  GEM_CHECK_CUDA(cudaMemsetAsync(bound, 0, (size_t)(L + 1) * 4, st));
+  lut_monotone_kernel<<<(unsigned)imin64((n + 255) / 256, 4096), 256, 0, st>>>(sc.lut32, G, nmax + 1, bound + L);
+  GEM_CHECK_LAUNCH("lut_monotone_kernel");
   const int warps = 8;
   topn_bound_kernel<<<(unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms()), warps * 32,
                       (size_t)warps * E * 4, st>>>(hist, L, T, E, E / G, bound);
-  std::vector<int32_t> ub((size_t)L);
+  std::vector<int32_t> ub((size_t)L + 1);
   cudaError_t e1 = cudaGetLastError();
-  cudaError_t e2 = cudaMemcpyAsync(ub.data(), bound, (size_t)L * 4, cudaMemcpyDeviceToHost, st);
+  cudaError_t e2 = cudaMemcpyAsync(ub.data(), bound, (size_t)(L + 1) * 4, cudaMemcpyDeviceToHost, st);
   cudaError_t e3 = cudaStreamSynchronize(st);
   cudaFreeAsync(bound, st);
   if (e1 != cudaSuccess) return fail_cuda(e1, "topn_bound_kernel");
   if (e2 != cudaSuccess) return fail_cuda(e2, "topn bound copy");
   if (e3 != cudaSuccess) return fail_cuda(e3, "topn bound sync");
-  for (int32_t v : ub) sc.U = imax64(sc.U, v);
+  for (int64_t l = 0; l < L; ++l) sc.U = imax64(sc.U, ub[l]);
+  ws.lut_monotone = ub[L] == 0;
   if (sc.U >= 65536) return GEM_OK;
   GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.ht16), (size_t)L * E * ws.Tp * 2, st));
   dim3 tg((unsigned)(ws.Tp / 32), (unsigned)((E + 31) / 32), (unsigned)L);
-  hist_t16_kernel<<<tg, dim3(32, 8), 0, st>>>(hist, T, ws.Tp, E, sc.ht16);
+  hist_t16_kernel<<<tg, dim3(32, 8), 0, st>>>(hist, T, ws.Tp, E, 0, sc.ht16);
   GEM_CHECK_LAUNCH("hist_t16_kernel");
   ws.ht16 = sc.ht16;
+  if (4 * sc.U < 65536) {  // K6 v5: counts as byte offsets into fp32 rows
+    GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.ht16s), (size_t)L * E * ws.Tp * 2, st));
+    hist_t16_kernel<<<tg, dim3(32, 8), 0, st>>>(hist, T, ws.Tp, E, 2, sc.ht16s);
+    GEM_CHECK_LAUNCH("hist_t16_kernel");
+    ws.ht16s = sc.ht16s;
+  }
   return GEM_OK;
 }
 
@@ -1219,6 +1532,12 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
   Screen screen;
   if ((rc = prepare_screen(hist, L, T, E, G, lut, nmax, screen, ws, st))) return rc;
   GEM_CHECK_CUDA(cudaMemsetAsync(ws.counters, 0, 16, st));
+  cudaEvent_t g0 = nullptr, g1 = nullptr;
+  if (std::getenv("GEM_SEARCH_TRACE")) {
+    GEM_CHECK_CUDA(cudaEventCreate(&g0));
+    GEM_CHECK_CUDA(cudaEventCreate(&g1));
+    GEM_CHECK_CUDA(cudaEventRecord(g0, st));
+  }
   rc = launch_greedy(hist, T, E, G, lut, nmax, screen.U, R, run_layer, needs_greedy, order, assign, ws, st);
   if (rc) return rc;
   {
@@ -1234,10 +1553,27 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
     state_t_kernel<<<4 * num_sms(), 256, 0, st>>>(R, T, G, nmax + 1, ws);
     GEM_CHECK_LAUNCH("state_t_kernel");
   }
+  if (g0) {
+    GEM_CHECK_CUDA(cudaEventRecord(g1, st));
+    GEM_CHECK_CUDA(cudaEventSynchronize(g1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g0, g1);
+    std::fprintf(stderr, "gem_search greedy+init (%lld runs): %.3f ms\n", (long long)R, ms);
+    cudaEventDestroy(g0);
+    cudaEventDestroy(g1);
+  }
+  // GEM_SEARCH_TRACE=1: per-round timing (CUDA events) and active-run counts on stderr
+  const bool trace = std::getenv("GEM_SEARCH_TRACE") != nullptr;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  if (trace) {
+    for (auto& e : ev) GEM_CHECK_CUDA(cudaEventCreate(&e));
+  }
   int64_t n_active = R;  // every run is active before its first scan
   for (int64_t it = 0; it < swap_cap; ++it) {
+    if (trace) GEM_CHECK_CUDA(cudaEventRecord(ev[0], st));
     rc = launch_scan(hist, T, E, G, lut, nmax, R, n_active, run_layer, assign, ws, st);
     if (rc) return rc;
+    if (trace) GEM_CHECK_CUDA(cudaEventRecord(ev[1], st));
     if (G < 2) break;  // no cross-GPU pair exists: found == false for every run
     GEM_CHECK_CUDA(cudaMemsetAsync(ws.counters, 0, 4, st));
     apply_swap_kernel<<<(unsigned)R, kSearchThreads, 0, st>>>(hist, T, E, G, lut, nmax, run_layer, assign, ws,
@@ -1246,8 +1582,20 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
     int32_t active = 0;
     GEM_CHECK_CUDA(cudaMemcpyAsync(&active, ws.counters, 4, cudaMemcpyDeviceToHost, st));
     GEM_CHECK_CUDA(cudaStreamSynchronize(st));
+    if (trace) {
+      GEM_CHECK_CUDA(cudaEventRecord(ev[2], st));
+      GEM_CHECK_CUDA(cudaEventSynchronize(ev[2]));
+      float ms_scan = 0.f, ms_all = 0.f;
+      cudaEventElapsedTime(&ms_scan, ev[0], ev[1]);
+      cudaEventElapsedTime(&ms_all, ev[0], ev[2]);
+      std::fprintf(stderr, "gem_search round %lld: active %lld scan %.3f ms apply %.3f ms\n", (long long)it,
+                   (long long)n_active, ms_scan, ms_all - ms_scan);
+    }
     if (active == 0) break;
     n_active = active;
+  }
+  if (trace) {
+    for (auto& e : ev) cudaEventDestroy(e);
   }
   final_copy_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(R, ws, final_score);
   GEM_CHECK_LAUNCH("final_copy_kernel");
