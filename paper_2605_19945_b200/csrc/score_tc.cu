@@ -1,33 +1,33 @@
-// K5 v2: straggler scoring of thousands of candidate mappings on B200.
+// K5 v3: straggler scoring of thousands of candidate mappings on B200.
 //
 //   score[c][l] = sum_t (serial fp64)  max_g C_g( n_g(c,l,t) ),
 //   n_g(c,l,t)  = sum_{e : cand[c][l][e] == g} h[l][t][e]        (mapping.py:146-166)
 //
-// Two passes per batch of P layers:
+// Order keys. Every latency the scorer can meet is a table value lut[g][n]
+// with n in the load window [0, U] (U = max over steps of the sum of the
+// `maxcnt` largest counts, maxcnt = the most experts any candidate puts on one
+// GPU: no load can exceed it). The distinct values of that window, sorted,
+// give each (n, g) a 16-bit key = the rank of lut[g][n]: keys compare exactly
+// like the fp64 values (equal values share a key), so the per-step maximum is
+// an integer max over G keys and its exact value is vals[key].
 //
-//  pass 1 (loads_tc_kernel, tcgen05): the per-GPU loads of every candidate are
-//    a one-hot GEMM  D[t][(c,g)] = sum_e H[t][e] * O[e][(c,g)]  with H in fp16
-//    (counts <= 2048 are exact) and O the 0/1 one-hot of the candidate tables,
-//    accumulated in fp32 in TMEM (loads < 2^24 are exact). M = 128 steps,
-//    N = 256 (candidate, GPU) columns, K = E. The one-hot B tile is built once
-//    per CTA; the H tiles are produced from the int32 histogram by all warps
-//    (fp16 convert, K-major 16-byte stores) into a 2-stage ring; one thread
-//    issues the MMAs; the epilogue drains TMEM (tcgen05.ld) and writes the
-//    loads as uint16 [layer][t][c][g] (each thread a contiguous row segment).
-//
-//  pass 2 (score_epi_kernel, CUDA cores): one thread per (candidate, layer)
-//    walks t in order. The fp32 rounding of the latency table window [0, U]
-//    (U = max over steps of the sum of the `maxcnt` largest counts, maxcnt =
-//    the most experts any candidate puts on one GPU: no load can exceed it)
-//    sits in shared memory and picks the arg-max GPU (rounding is monotone,
-//    so a unique fp32 maximum is the exact maximum's GPU); the exact fp64
-//    value of that GPU alone is read from the L2-resident table (all fp32-tied
-//    GPUs are read when the maximum is not unique) and added to the serial
-//    chain exactly as the reference sums (_util.py:8-18).
+//  pass 1 (maxkey_tc_kernel, tcgen05): the per-GPU loads of every candidate
+//    are a one-hot GEMM  D[t][(c,g)] = sum_e H[t][e] * O[e][(c,g)]  with H in
+//    fp16 (counts <= 2048 are exact) and O the 0/1 one-hot of the candidate
+//    tables, accumulated in fp32 in TMEM (loads < 2^24 are exact). M = 128
+//    steps, N = 256 (candidate, GPU) columns, K = E. The epilogue drains TMEM
+//    (tcgen05.ld: one step per lane), looks every load up in the key table
+//    (shared memory, [g][n] u16: random n spread over all banks) and writes the step's maximum key per
+//    candidate: u16 [layer][t][c] -- 1/G of the bytes of the loads themselves.
+//  pass 2 (keysum_kernel): one thread per (candidate, layer) walks t in order
+//    and adds vals[key] to the fp64 chain exactly as the reference sums
+//    (_util.py:8-18); the low end of vals sits in shared memory.
 //
 // Bit-exact with score_layers_kernel and the oracle by construction.
 #include <cuda_fp16.h>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
 #include <vector>
 
 #include "gem_common.cuh"
@@ -39,7 +39,10 @@ __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, i
                                   int32_t* __restrict__ bound);  // search.cu
 
 constexpr int kLtThreads = 256;
-constexpr int kLtN = 256;  // MMA N (candidate x GPU columns per CTA)
+constexpr int kLtN = 256;        // MMA N (candidate x GPU columns per CTA)
+constexpr int kMaxKeys = 65536;  // u16 keys
+constexpr int kSumThreads = 256;
+constexpr int kSumSmemVals = 4096;  // vals[0, 4096) in shared memory (32 KB)
 
 struct LoadsTcShared {
   uint64_t mma_bar;
@@ -72,55 +75,81 @@ __global__ void cand_stats_kernel(const int8_t* __restrict__ cand, int64_t rows,
   }
 }
 
-__global__ void lut_window_f32_kernel(const double* __restrict__ lut, int G, int64_t width, int W,
-                                      float* __restrict__ out) {
+// bits[g*W + n] = the fp64 pattern of lut[g][n] for n < W (monotone in the
+// value for finite v >= 0); bad = 1 on a negative, NaN or infinite entry
+__global__ void window_bits_kernel(const double* __restrict__ lut, int G, int64_t width, int W,
+                                   unsigned long long* __restrict__ bits, int32_t* __restrict__ bad) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)G * W;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int g = (int)(i / W);
-    const int64_t n = i % W;
-    out[i] = __double2float_rn(lut[g * width + n]);
+    const int64_t n = i - (int64_t)g * W;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(lut[g * width + n]);
+    if (b >= 0x7ff0000000000000ull) atomicExch(bad, 1);  // sign bit, inf or NaN
+    bits[i] = b;
+  }
+}
+
+// keys[g*W + n] = rank of lut[g][n] among the sorted distinct values
+__global__ void key_table_kernel(const unsigned long long* __restrict__ bits, int64_t count,
+                                 const unsigned long long* __restrict__ uniq, const int32_t* __restrict__ nuniq,
+                                 uint16_t* __restrict__ keys) {
+  const int K = *nuniq;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long b = bits[i];
+    int lo = 0, hi = K - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (uniq[mid] < b) lo = mid + 1; else hi = mid;
+    }
+    keys[i] = (uint16_t)lo;
   }
 }
 
 // ---------------------------------------------------------------------------
 // pass 1: CTA = (candidate tile of CT = N/G candidates, layer of the batch);
-// loops over every 128-step tile of the layer: produce the fp16 H tile, one
-// thread issues the E/16 MMAs, all warps drain TMEM. Each CTA is serial; two
-// CTAs per SM (96 KB shared memory, 256 TMEM columns each) overlap one
-// another's load latency with the other's MMA and epilogue.
-template <int E>
-__global__ void __launch_bounds__(kLtThreads, 2)
-loads_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int G, const int8_t* __restrict__ cand, int64_t C,
-                int64_t L, int64_t layer0, int64_t Cp, uint16_t* __restrict__ loads) {
-  constexpr int KCH = E / 8;                // 16-byte K chunks (8 fp16 experts)
-  constexpr uint32_t LBO_A = 128 * 16 + 16; // A: [KCH][128 rows][16 B], K slices padded by 16 B (bank spread)
-  constexpr uint32_t LBO_B = kLtN * 16;     // B: [KCH][N rows][16 B]
+// loops over every 128-step tile of the layer in order: produce the fp16 H
+// tile, one thread issues the E/16 MMAs, all warps drain TMEM into keys.
+template <int E, int G>
+__global__ void __launch_bounds__(kLtThreads, 1)
+maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __restrict__ cand, int64_t C,
+                 int64_t L, int64_t layer0, int64_t Cp, const uint16_t* __restrict__ gkeys, int W,
+                 uint16_t* __restrict__ out_keys) {
+  constexpr int KCH = E / 8;                 // 16-byte K chunks (8 fp16 experts)
+  constexpr uint32_t LBO_A = 128 * 16 + 16;  // A: [KCH][128 rows][16 B], K slices padded by 16 B (bank spread)
+  constexpr uint32_t LBO_B = kLtN * 16;      // B: [KCH][N rows][16 B]
   constexpr int A_BYTES = (int)LBO_A * KCH;
   constexpr int B_BYTES = kLtN * E * 2;
-  constexpr int STG_ROW = 80;                // epilogue staging row: 64 B + 16 B pad (conflict-free)
+  constexpr int CT = kLtN / G;               // candidates per CTA
+  constexpr int KPT = CT / 2;                // keys per thread per tile (one column half)
+  constexpr int CPL = 32 / G;                // candidates per 32-column TMEM load
+  constexpr int STG_ROW = KPT * 2 + 16;      // staging row: the thread's keys + 16 B pad
+  constexpr int STG_BYTES = 8 * 32 * STG_ROW;
+  static_assert(STG_BYTES <= A_BYTES, "key staging must fit the H tile");
+  static_assert(G >= 4 && G <= 32 && (kLtN % G) == 0, "G in {4, 8, 16, 32}");
   extern __shared__ __align__(1024) unsigned char lt_smem[];
   unsigned char* sa = lt_smem;
   unsigned char* sb = lt_smem + A_BYTES;
-  // epilogue staging [8 warps][32 rows][STG_ROW]: the H tile's space (free once the
-  // tile's MMAs completed) when it is large enough, else its own block
-  constexpr int STG_BYTES = 8 * 32 * STG_ROW;
-  constexpr bool STG_IN_A = STG_BYTES <= A_BYTES;
   LoadsTcShared* sh = reinterpret_cast<LoadsTcShared*>(sb + B_BYTES);
-  unsigned char* stg = STG_IN_A ? sa : sb + B_BYTES + 64;
+  uint16_t* skeys = reinterpret_cast<uint16_t*>(sb + B_BYTES + 64);  // [G][W]
+  unsigned char* stg = sa;  // the H tile's space, free once the tile's MMAs completed
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int CT = kLtN / G;                  // candidates per CTA
   const int64_t c0 = (int64_t)blockIdx.x * CT;
-  const int64_t lb = blockIdx.y;            // layer within the batch
+  const int64_t lb = blockIdx.y;  // layer within the batch
   const int64_t l = layer0 + lb;
   const int32_t* hl = hist + l * T * E;
-  uint16_t* out = loads + lb * T * Cp * G;
+  uint16_t* out = out_keys + lb * T * Cp;
 
   if (tid == 0) {
     tc::mbar_init(&sh->mma_bar, 1);
     tc::fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc<kLtN>(&sh->tmem_base);
+  {  // key table -> shared memory (16-byte pieces)
+    const int pieces = (W * G * 2 + 15) / 16;
+    for (int i = tid; i < pieces; i += blockDim.x)
+      reinterpret_cast<uint4*>(skeys)[i] = __ldg(reinterpret_cast<const uint4*>(gkeys) + i);
+  }
   // one-hot B: row r = j*G + g (candidate j of the tile, GPU g), 1.0 where cand == g
   for (int i = tid; i < kLtN * KCH; i += blockDim.x) {
     const int r = i / KCH, q = i % KCH;
@@ -140,34 +169,43 @@ loads_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int G, const int8_t
   tc::tc_fence_after();
   const uint32_t tmem = sh->tmem_base;
   const uint32_t sa_addr = tc::smem_u32(sa), sb_addr = tc::smem_u32(sb);
+  const uint32_t sk_addr = tc::smem_u32(skeys);
   const uint32_t idesc = tc::instr_desc(/*F32*/ 1, /*F16*/ 0, /*F16*/ 0, 128, kLtN);
   const int ntiles = (int)((T + 127) / 128);
   const int lg = warp & 3, half = warp >> 2;
 
+  // H rows: each warp reads whole rows (coalesced), the next tile's rows are in
+  // flight during the current tile's MMA and epilogue
+  constexpr int RPW = 128 / (kLtThreads / 32);  // rows per warp (16)
+  constexpr int LPR = E / 4;                     // lanes per row (4 experts each)
+  constexpr int RPI = 32 / LPR;                  // rows per warp instruction
+  constexpr int NX = RPW / RPI;
+  int4 x[NX];
+  auto load_rows = [&](int i) {
+#pragma unroll
+    for (int v = 0; v < NX; ++v) {
+      const int row = warp * RPW + v * RPI + lane / LPR;
+      const int64_t t = (int64_t)i * 128 + row;
+      x[v] = t < T ? __ldg(reinterpret_cast<const int4*>(hl + t * E) + (lane % LPR)) : make_int4(0, 0, 0, 0);
+    }
+  };
+  // per-GPU row offsets into the key table (bytes), biased by the fp32 exponent
+  // pattern so that (bits of n + 2^23) * 2 + off[g] addresses key[g][n]
+  uint32_t koff[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) koff[g] = sk_addr + 2u * (uint32_t)g * (uint32_t)W - 2u * 0x4B000000u;
+  load_rows(0);
   for (int i = 0; i < ntiles; ++i) {
-    // ---- H tile i: each warp reads whole 512-byte rows (coalesced), all of its
-    // rows in flight, then fp16 convert + 8-byte K-major stores
-    {
-      constexpr int RPW = 128 / (kLtThreads / 32);  // rows per warp (16)
-      constexpr int LPR = E / 4;                     // lanes per row (4 experts each)
-      constexpr int RPI = 32 / LPR;                  // rows per warp instruction
-      int4 x[RPW / RPI];
+    // ---- H tile i: exact int -> fp32 (2^23 trick) -> packed fp16 pairs, 8-byte K-major stores
 #pragma unroll
-      for (int v = 0; v < RPW / RPI; ++v) {
-        const int row = warp * RPW + v * RPI + lane / LPR;
-        const int64_t t = (int64_t)i * 128 + row;
-        x[v] = t < T ? __ldg(reinterpret_cast<const int4*>(hl + t * E) + (lane % LPR)) : make_int4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int v = 0; v < RPW / RPI; ++v) {
-        const int row = warp * RPW + v * RPI + lane / LPR;
-        const int e4 = lane % LPR;  // experts 4*e4 .. 4*e4+3
-        auto h2 = [](int a, int b) {
-          return (uint32_t)__half_as_ushort(__int2half_rn(a)) | ((uint32_t)__half_as_ushort(__int2half_rn(b)) << 16);
-        };
-        *reinterpret_cast<uint2*>(sa + (size_t)(e4 >> 1) * LBO_A + (size_t)row * 16 + (e4 & 1) * 8) =
-            make_uint2(h2(x[v].x, x[v].y), h2(x[v].z, x[v].w));
-      }
+    for (int v = 0; v < NX; ++v) {
+      const int row = warp * RPW + v * RPI + lane / LPR;
+      const int e4 = lane % LPR;  // experts 4*e4 .. 4*e4+3
+      auto f = [](int a) { return __uint_as_float(0x4B000000u | (uint32_t)a) - 8388608.0f; };
+      const __half2 p0 = __floats2half2_rn(f(x[v].x), f(x[v].y));
+      const __half2 p1 = __floats2half2_rn(f(x[v].z), f(x[v].w));
+      *reinterpret_cast<uint2*>(sa + (size_t)(e4 >> 1) * LBO_A + (size_t)row * 16 + (e4 & 1) * 8) =
+          make_uint2(*reinterpret_cast<const uint32_t*>(&p0), *reinterpret_cast<const uint32_t*>(&p1));
     }
     tc::fence_async_smem();
     __syncthreads();
@@ -181,38 +219,62 @@ loads_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int G, const int8_t
       }
       tc::mma_commit(&sh->mma_bar);
     }
+    if (i + 1 < ntiles) load_rows(i + 1);
     tc::mbar_wait(&sh->mma_bar, (uint32_t)(i & 1));
     tc::tc_fence_after();
-    // ---- epilogue: warp w drains TMEM lanes 32(w%4).. and column half w/4 in
-    // 32-column chunks (exact fp32 integers -> uint16 pairs), transposes each
-    // chunk through its shared staging block and writes 8 rows x 64 B per store
+    // ---- epilogue: warp w drains TMEM lanes 32(w%4).. (one step per lane) and
+    // column half w/4 in 32-column chunks; load n of GPU g -> key[g][n]; the
+    // maximum over a candidate's G columns is its step key
     {
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16);
-      unsigned char* wst = stg + warp * 32 * STG_ROW;
-      const int64_t tbase = (int64_t)i * 128 + lg * 32;
-#pragma unroll 1
-      for (int col = half * (kLtN / 2); col < (half + 1) * (kLtN / 2); col += 32) {
+      uint32_t kk[KPT];
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
         uint32_t v[32];
-        tc::tmem_ld32(trow + col, v);
+        tc::tmem_ld32(trow + half * (kLtN / 2) + ch * 32, v);
         tc::tmem_ld_wait();
-        uint32_t pk[16];
 #pragma unroll
-        for (int x = 0; x < 16; ++x)  // exact integers < 2^16: + 2^23 puts them in the low mantissa bits
-          pk[x] = __byte_perm(__float_as_uint(__uint_as_float(v[2 * x]) + 8388608.0f),
-                              __float_as_uint(__uint_as_float(v[2 * x + 1]) + 8388608.0f), 0x5410);
+        for (int j = 0; j < CPL; ++j) {
+          uint32_t m = 0;
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
-          *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x * 16) =
-              make_uint4(pk[4 * x], pk[4 * x + 1], pk[4 * x + 2], pk[4 * x + 3]);
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int r = j * 8 + lane / 4, piece = lane % 4;
-          const int64_t t = tbase + r;
-          const uint4 w = *reinterpret_cast<const uint4*>(wst + r * STG_ROW + piece * 16);
-          if (t < T) *reinterpret_cast<uint4*>(out + (t * Cp + c0) * G + col + piece * 8) = w;
+          for (int g = 0; g < G; ++g) {
+            // exact integer n < 2^16 in fp32: + 2^23 puts it in the low mantissa bits
+            const uint32_t nb = __float_as_uint(__uint_as_float(v[j * G + g]) + 8388608.0f);
+            const uint32_t addr = nb * 2u + koff[g];
+            uint16_t key;
+            asm("ld.shared.u16 %0, [%1];" : "=h"(key) : "r"(addr));
+            m = max(m, (uint32_t)key);
+          }
+          kk[ch * CPL + j] = m;
         }
-        __syncwarp();
+      }
+      // the H tile is free (its MMAs completed): stage the keys, then store rows
+      // of KPT keys (2*KPT bytes) per step, 16-byte pieces
+      unsigned char* wst = stg + warp * 32 * STG_ROW;
+#pragma unroll
+      for (int x = 0; x < KPT / 8; ++x)
+        *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x * 16) =
+            make_uint4(kk[8 * x] | (kk[8 * x + 1] << 16), kk[8 * x + 2] | (kk[8 * x + 3] << 16),
+                       kk[8 * x + 4] | (kk[8 * x + 5] << 16), kk[8 * x + 6] | (kk[8 * x + 7] << 16));
+      if (KPT % 8 == 4)
+        *reinterpret_cast<uint2*>(wst + lane * STG_ROW + (KPT / 8) * 16) =
+            make_uint2(kk[KPT - 4] | (kk[KPT - 3] << 16), kk[KPT - 2] | (kk[KPT - 1] << 16));
+      __syncwarp();
+      const int64_t tbase = (int64_t)i * 128 + lg * 32;
+      const int64_t cbase = c0 + half * KPT;
+      if (KPT >= 8) {
+        constexpr int PPR = KPT / 8;  // 16-byte pieces per row
+        for (int q = lane; q < 32 * PPR; q += 32) {
+          const int r = q / PPR, piece = q % PPR;
+          const int64_t t = tbase + r;
+          if (t < T)
+            *reinterpret_cast<uint4*>(out + t * Cp + cbase + piece * 8) =
+                *reinterpret_cast<const uint4*>(wst + r * STG_ROW + piece * 16);
+        }
+      } else {  // KPT == 4: one 8-byte piece per row
+        const int64_t t = tbase + lane;
+        if (t < T)
+          *reinterpret_cast<uint2*>(out + t * Cp + cbase) = *reinterpret_cast<const uint2*>(wst + lane * STG_ROW);
       }
     }
     tc::tc_fence_before();
@@ -223,104 +285,55 @@ loads_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int G, const int8_t
 
 // ---------------------------------------------------------------------------
 // pass 2: thread = (candidate, layer of the batch), serial over t
-constexpr int kEpiThreads = 1024;  // one CTA per SM: the table window takes most of shared memory
-
-template <int GM>
-__global__ void __launch_bounds__(kEpiThreads, 1)
-score_epi_kernel(const uint16_t* __restrict__ loads, int64_t T, int G, int64_t C, int64_t Cp, int64_t L,
-                 int64_t layer0, int W, const float* __restrict__ lut32w, const double* __restrict__ lut,
-                 int64_t nmax, double* __restrict__ layer_scores, int32_t* __restrict__ err) {
-  extern __shared__ float s_lut[];  // [G][W]
-  for (int i = threadIdx.x; i < G * W; i += blockDim.x) s_lut[i] = lut32w[i];
+__global__ void __launch_bounds__(kSumThreads)
+keysum_kernel(const uint16_t* __restrict__ keys, int64_t T, int64_t C, int64_t Cp, int64_t L, int64_t layer0,
+              const double* __restrict__ vals, const int32_t* __restrict__ nvals, double* __restrict__ layer_scores) {
+  __shared__ double s_vals[kSumSmemVals];
+  const int K = min(*nvals, kSumSmemVals);
+  for (int i = threadIdx.x; i < K; i += blockDim.x) s_vals[i] = vals[i];
   __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t lb = blockIdx.y;
   if (c >= C) return;
-  const int64_t width = nmax + 1;
-  const uint16_t* p = loads + (lb * T * Cp + c) * G;
-  const int64_t stride = Cp * G;
-  const bool vec = GM == 8 && G == 8;
-  // table row g of the window starts at s_lut + roff[g]; the fp64 row at lut + goff[g]
-  int roff[GM];
-  int64_t goff[GM];
+  const uint16_t* p = keys + lb * T * Cp + c;
+  auto val = [&](uint32_t k) -> double { return k < (uint32_t)kSumSmemVals ? s_vals[k] : __ldg(vals + k); };
+  // keys 8 steps ahead of the serial fp64 chain (which stays in t order)
+  constexpr int D = 8;
+  uint32_t q[D];
 #pragma unroll
-  for (int g = 0; g < GM; ++g) {
-    roff[g] = g < G ? g * W : 0;
-    goff[g] = g < G ? g * width : 0;
-  }
-  auto fetch = [&](int64_t t) -> uint4 {
-    return t < T ? *reinterpret_cast<const uint4*>(p + t * stride) : make_uint4(0u, 0u, 0u, 0u);
-  };
-  // exact per-step maximum of step t from its loads (issues the fp64 table read):
-  // branch-free arg-max of the fp32 window values, `second` = best of the others
-  auto step_max = [&](int64_t t, uint4 v) -> double {
-    uint32_t n[GM];
-    if (vec) {
-      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) { n[2 * q] = w4[q] & 0xffffu; n[2 * q + 1] = w4[q] >> 16; }
-    } else {
-#pragma unroll
-      for (int g = 0; g < GM; ++g) n[g] = g < G ? p[t * stride + g] : 0u;
-    }
-    float best = s_lut[roff[0] + n[0]];
-    float second = -1.0f;
-    int64_t off = goff[0] + n[0];
-#pragma unroll
-    for (int g = 1; g < GM; ++g) {
-      if (g < G) {  // G is uniform: no divergence
-        const float x = s_lut[roff[g] + n[g]];
-        const bool gt = x > best;
-        second = gt ? best : fmaxf(second, x);
-        off = gt ? goff[g] + n[g] : off;
-        best = fmaxf(best, x);
-      }
-    }
-    double m = __ldg(lut + off);
-    if (second == best) {  // rare: several GPUs share the fp32 maximum -> exact maximum among them
-#pragma unroll
-      for (int g = 0; g < GM; ++g) {
-        if (g < G && s_lut[roff[g] + n[g]] == best) {
-          const double v2 = __ldg(lut + goff[g] + n[g]);
-          m = v2 > m ? v2 : m;
-        }
-      }
-    }
-    return m;
-  };
-  // software pipeline: loads four steps ahead, the table value one step ahead of
-  // the serial fp64 chain (which stays in t order); unrolled by 4 so the load
-  // ring needs no register moves
-  uint4 q0 = vec ? fetch(0) : uint4{}, q1 = vec ? fetch(1) : uint4{}, q2 = vec ? fetch(2) : uint4{},
-        q3 = vec ? fetch(3) : uint4{};
-  double m_next = step_max(0, q0);
+  for (int d = 0; d < D; ++d) q[d] = d < T ? p[(int64_t)d * Cp] : 0u;
   double s = 0.0;
   int64_t t = 0;
-  for (; t + 4 <= T; t += 4) {
-    double m = m_next;
-    if (vec) q0 = fetch(t + 4);
-    m_next = step_max(t + 1, q1);
-    s = dadd(s, m);
-    m = m_next;
-    if (vec) q1 = fetch(t + 5);
-    m_next = step_max(t + 2, q2);
-    s = dadd(s, m);
-    m = m_next;
-    if (vec) q2 = fetch(t + 6);
-    m_next = step_max(t + 3, q3);
-    s = dadd(s, m);
-    m = m_next;
-    if (vec) q3 = fetch(t + 7);
-    if (t + 4 < T) m_next = step_max(t + 4, q0);
-    s = dadd(s, m);
+  for (; t + D <= T; t += D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double v = val(q[d]);
+      q[d] = t + D + d < T ? p[(t + D + d) * Cp] : 0u;
+      s = dadd(s, v);
+    }
   }
-  // tail (T % 4 steps): q0..q2 hold steps t+1.. already fetched; m_next is step t
-  for (int r = 0; t < T; ++t, ++r) {
-    const double m = m_next;
-    if (t + 1 < T) m_next = step_max(t + 1, r == 0 ? q1 : (r == 1 ? q2 : q3));
-    s = dadd(s, m);
-  }
+  for (int d = 0; t < T; ++t, ++d) s = dadd(s, val(q[d]));
   layer_scores[c * L + layer0 + lb] = s;
+}
+
+template <int E>
+static int launch_maxkey(int G, dim3 grid, size_t smem, cudaStream_t st, const int32_t* hist, int64_t T,
+                         const int8_t* cand, int64_t C, int64_t L, int64_t l0, int64_t Cp, const uint16_t* keys,
+                         int W, uint16_t* out) {
+  auto pick = [&](auto kern) -> int {
+    GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, kLtThreads, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, W, out);
+    GEM_CHECK_LAUNCH("maxkey_tc_kernel");
+    return GEM_OK;
+  };
+  switch (G) {
+    case 4:
+      if constexpr (E == 128) return pick(maxkey_tc_kernel<E, 4>);
+      else return 1;
+    case 8: return pick(maxkey_tc_kernel<E, 8>);
+    case 16: return pick(maxkey_tc_kernel<E, 16>);
+    default: return pick(maxkey_tc_kernel<E, 32>);
+  }
 }
 
 }  // namespace gem
@@ -332,94 +345,106 @@ using namespace gem;
 extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G, const int8_t* cand,
                                   int64_t C, const double* lut, int64_t nmax, double* layer_scores,
                                   int32_t* err_flag, void* stream) {
-  if (!(E == 64 || E == 128) || G < 1 || G > 32 || (kLtN % G) != 0) return 1;
+  (void)err_flag;
+  if (!(E == 64 || E == 128) || !(G == 4 || G == 8 || G == 16 || G == 32) || (E == 64 && G == 4)) return 1;
   if (T < 1 || C < 1 || nmax < 0) return 1;
   cudaStream_t st = as_stream(stream);
   keep_pool();
   int dev = 0, optin = 0;
   GEM_CHECK_CUDA(cudaGetDevice(&dev));
   GEM_CHECK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  // ---- bounds: experts per GPU, load window, largest count (one host sync)
-  int32_t* scratch = nullptr;  // [2] cand stats, [L] top-maxcnt bound, [L] max count
-  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), (size_t)(2 + 2 * L) * 4, st));
+  // stream-ordered scratch, freed on every exit path
+  std::vector<void*> scratch;
   struct Free {
-    int32_t* p;
+    std::vector<void*>& v;
     cudaStream_t s;
-    ~Free() { cudaFreeAsync(p, s); }
-  } free_scratch{scratch, st};
-  GEM_CHECK_CUDA(cudaMemsetAsync(scratch, 0, (size_t)(2 + 2 * L) * 4, st));
+    ~Free() {
+      for (void* p : v) cudaFreeAsync(p, s);
+    }
+  } free_all{scratch, st};
+  auto alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) return nullptr;
+    scratch.push_back(p);
+    return p;
+  };
+  // ---- bounds: experts per GPU, load window, largest count (one host sync)
+  int32_t* bnd_d = static_cast<int32_t*>(alloc((size_t)(2 + 2 * L) * 4));  // [2] cand stats, [L] top-n, [L] max
+  if (!bnd_d) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc scratch");
+  GEM_CHECK_CUDA(cudaMemsetAsync(bnd_d, 0, (size_t)(2 + 2 * L) * 4, st));
   cand_stats_kernel<<<(unsigned)imin64((C * L + 7) / 8, 16 * num_sms()), 256, (size_t)8 * G * 4, st>>>(
-      cand, C * L, E, G, scratch);
+      cand, C * L, E, G, bnd_d);
   GEM_CHECK_LAUNCH("cand_stats_kernel");
   int32_t cs[2] = {0, 0};
-  GEM_CHECK_CUDA(cudaMemcpyAsync(cs, scratch, 8, cudaMemcpyDeviceToHost, st));
+  GEM_CHECK_CUDA(cudaMemcpyAsync(cs, bnd_d, 8, cudaMemcpyDeviceToHost, st));
   GEM_CHECK_CUDA(cudaStreamSynchronize(st));
   if (cs[1]) return 1;  // invalid entries: the CUDA-core scorer reports them
   const int maxcnt = cs[0] < 1 ? 1 : cs[0];
   const int warps = 8;
   const unsigned tb_grid = (unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms());
-  topn_bound_kernel<<<tb_grid, warps * 32, (size_t)warps * E * 4, st>>>(hist, L, T, E, maxcnt, scratch + 2);
+  topn_bound_kernel<<<tb_grid, warps * 32, (size_t)warps * E * 4, st>>>(hist, L, T, E, maxcnt, bnd_d + 2);
   GEM_CHECK_LAUNCH("topn_bound_kernel");
-  topn_bound_kernel<<<tb_grid, warps * 32, (size_t)warps * E * 4, st>>>(hist, L, T, E, 1, scratch + 2 + L);
+  topn_bound_kernel<<<tb_grid, warps * 32, (size_t)warps * E * 4, st>>>(hist, L, T, E, 1, bnd_d + 2 + L);
   GEM_CHECK_LAUNCH("topn_bound_kernel");
   std::vector<int32_t> bnd((size_t)2 * L);
-  GEM_CHECK_CUDA(cudaMemcpyAsync(bnd.data(), scratch + 2, (size_t)2 * L * 4, cudaMemcpyDeviceToHost, st));
+  GEM_CHECK_CUDA(cudaMemcpyAsync(bnd.data(), bnd_d + 2, (size_t)2 * L * 4, cudaMemcpyDeviceToHost, st));
   GEM_CHECK_CUDA(cudaStreamSynchronize(st));
   int64_t U = 0, hmax = 0;
   for (int64_t l = 0; l < L; ++l) {
     U = imax64(U, bnd[l]);
     hmax = imax64(hmax, bnd[L + l]);
   }
-  if (hmax > 2048 || U > nmax || U >= 65536) return 1;  // fp16 / uint16 exactness, table range
+  if (hmax > 2048 || U > nmax || U >= 65536) return 1;  // fp16 exactness, table range
   const int W = (int)U + 1;
-  const size_t epi_smem = (size_t)G * W * 4;
-  if (epi_smem > (size_t)optin) return 1;
+  const size_t key_bytes = (((size_t)W * G * 2) + 15) & ~size_t(15);
+  const size_t a_bytes = (size_t)(128 * 16 + 16) * (E / 8);
+  const size_t lt_smem = a_bytes + (size_t)kLtN * E * 2 + 64 + key_bytes;
+  if (lt_smem > (size_t)optin) return 1;
 
-  // ---- fp32 table window
-  float* lut32w = nullptr;
-  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&lut32w), epi_smem, st));
-  struct FreeF {
-    float* p;
-    cudaStream_t s;
-    ~FreeF() { cudaFreeAsync(p, s); }
-  } free_lut{lut32w, st};
-  lut_window_f32_kernel<<<(unsigned)imin64(((int64_t)G * W + 255) / 256, 4096), 256, 0, st>>>(lut, G, nmax + 1, W,
-                                                                                             lut32w);
-  GEM_CHECK_LAUNCH("lut_window_f32_kernel");
+  // ---- order keys of the load window: sort the distinct fp64 values
+  const int64_t cnt = (int64_t)G * W;
+  auto* bits = static_cast<unsigned long long*>(alloc((size_t)cnt * 8));
+  auto* sorted = static_cast<unsigned long long*>(alloc((size_t)cnt * 8));
+  auto* uniq = static_cast<unsigned long long*>(alloc((size_t)cnt * 8));
+  auto* nu = static_cast<int32_t*>(alloc(8));  // [0] distinct count, [1] bad entry flag
+  auto* keys = static_cast<uint16_t*>(alloc(key_bytes));
+  if (!bits || !sorted || !uniq || !nu || !keys) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc keys");
+  GEM_CHECK_CUDA(cudaMemsetAsync(nu, 0, 8, st));
+  window_bits_kernel<<<(unsigned)imin64((cnt + 255) / 256, 4096), 256, 0, st>>>(lut, G, nmax + 1, W, bits, nu + 1);
+  GEM_CHECK_LAUNCH("window_bits_kernel");
+  size_t t1 = 0, t2 = 0;
+  GEM_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, t1, bits, sorted, (int)cnt, 0, 64, st));
+  GEM_CHECK_CUDA(cub::DeviceSelect::Unique(nullptr, t2, sorted, uniq, nu, (int)cnt, st));
+  void* tmp = alloc(t1 > t2 ? t1 : t2);
+  if (!tmp) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc cub");
+  GEM_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t1, bits, sorted, (int)cnt, 0, 64, st));
+  GEM_CHECK_CUDA(cub::DeviceSelect::Unique(tmp, t2, sorted, uniq, nu, (int)cnt, st));
+  int32_t nk[2] = {0, 0};
+  GEM_CHECK_CUDA(cudaMemcpyAsync(nk, nu, 8, cudaMemcpyDeviceToHost, st));
+  GEM_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (nk[1] || nk[0] < 1 || nk[0] > kMaxKeys) return 1;
+  key_table_kernel<<<(unsigned)imin64((cnt + 255) / 256, 4096), 256, 0, st>>>(bits, cnt, uniq, nu, keys);
+  GEM_CHECK_LAUNCH("key_table_kernel");
+  const double* vals = reinterpret_cast<const double*>(uniq);  // the bit patterns are the values
 
-  // ---- layer batches: P layers of uint16 loads [P][T][Cp][G] in flight (<= ~24 GB)
+  // ---- layer batches: P layers of u16 step keys [P][T][Cp] in flight (<= ~8 GB)
   const int CT = kLtN / G;
   const int64_t ntile = (C + CT - 1) / CT;
   const int64_t Cp = ntile * CT;
-  const size_t per_layer = (size_t)T * Cp * G * 2;
-  // enough layers in flight that pass 2 (one 1024-thread CTA per SM) fills every SM
-  int64_t P = (int64_t)(40ull << 30) / (int64_t)per_layer;
-  const int64_t ctas_per_layer = (C + kEpiThreads - 1) / kEpiThreads;
-  const int64_t want = (num_sms() + ctas_per_layer - 1) / ctas_per_layer;
-  P = imin64(imin64(P, want), L);
+  const size_t per_layer = (size_t)T * Cp * 2;
+  int64_t P = imin64((int64_t)(8ull << 30) / (int64_t)per_layer, L);
   if (P < 1) return 1;
-  uint16_t* loads = nullptr;
-  GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&loads), per_layer * P, st));
-  struct FreeU {
-    uint16_t* p;
-    cudaStream_t s;
-    ~FreeU() { cudaFreeAsync(p, s); }
-  } free_loads{loads, st};
-
-  const size_t a_bytes = (size_t)(128 * 16 + 16) * (E / 8), stg_bytes = 8 * 32 * 80;
-  const size_t lt_smem = a_bytes + (size_t)kLtN * E * 2 + 64 + (stg_bytes <= a_bytes ? 0 : stg_bytes);
-  auto k1 = E == 128 ? loads_tc_kernel<128> : loads_tc_kernel<64>;
-  GEM_CHECK_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lt_smem));
-  const int GM = G <= 8 ? 8 : (G <= 16 ? 16 : 32);
-  auto k2 = GM == 8 ? score_epi_kernel<8> : (GM == 16 ? score_epi_kernel<16> : score_epi_kernel<32>);
-  GEM_CHECK_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)epi_smem));
+  auto* kbuf = static_cast<uint16_t*>(alloc(per_layer * P));
+  if (!kbuf) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc key buffer");
   for (int64_t l0 = 0; l0 < L; l0 += P) {
     const int64_t nb = imin64(P, L - l0);
-    k1<<<dim3((unsigned)ntile, (unsigned)nb), kLtThreads, lt_smem, st>>>(hist, T, G, cand, C, L, l0, Cp, loads);
-    GEM_CHECK_LAUNCH("loads_tc_kernel");
-    k2<<<dim3((unsigned)ctas_per_layer, (unsigned)nb), kEpiThreads, epi_smem, st>>>(loads, T, G, C, Cp, L, l0, W, lut32w,
-                                                                               lut, nmax, layer_scores, err_flag);
-    GEM_CHECK_LAUNCH("score_epi_kernel");
+    const dim3 g1((unsigned)ntile, (unsigned)nb);
+    const int rc = E == 128 ? launch_maxkey<128>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, W, kbuf)
+                            : launch_maxkey<64>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, W, kbuf);
+    if (rc) return rc;
+    keysum_kernel<<<dim3((unsigned)((C + kSumThreads - 1) / kSumThreads), (unsigned)nb), kSumThreads, 0, st>>>(
+        kbuf, T, C, Cp, L, l0, vals, nu, layer_scores);
+    GEM_CHECK_LAUNCH("keysum_kernel");
   }
   return GEM_OK;
 }
