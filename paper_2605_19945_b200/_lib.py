@@ -15,7 +15,9 @@ from pathlib import Path
 from .errors import GemapError
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "_lib" / "libgemcore.so"
+# GEM_LIB_VARIANT=<name> loads _lib/libgemcore-<name>.so (kernel experiments built by tools/)
+LIB_PATH = _PKG / "_lib" / ("libgemcore-%s.so" % os.environ["GEM_LIB_VARIANT"] if os.environ.get("GEM_LIB_VARIANT")
+                            else "libgemcore.so")
 CSRC = _PKG / "csrc"
 
 GEM_OK = 0

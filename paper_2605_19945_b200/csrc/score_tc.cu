@@ -36,7 +36,7 @@
 namespace gem {
 
 __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, int64_t T, int E, int n,
-                                  int32_t* __restrict__ bound);  // search.cu
+                                  int32_t* __restrict__ bound, int32_t* __restrict__ top1);  // search.cu
 
 constexpr int kLtThreads = 256;
 constexpr int kLtN = 256;        // MMA N (candidate x GPU columns per CTA)
@@ -382,9 +382,8 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   const int maxcnt = cs[0] < 1 ? 1 : cs[0];
   const int warps = 8;
   const unsigned tb_grid = (unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms());
-  topn_bound_kernel<<<tb_grid, warps * 32, (size_t)warps * E * 4, st>>>(hist, L, T, E, maxcnt, bnd_d + 2);
-  GEM_CHECK_LAUNCH("topn_bound_kernel");
-  topn_bound_kernel<<<tb_grid, warps * 32, (size_t)warps * E * 4, st>>>(hist, L, T, E, 1, bnd_d + 2 + L);
+  topn_bound_kernel<<<tb_grid, warps * 32, (size_t)warps * E * 4, st>>>(hist, L, T, E, maxcnt, bnd_d + 2,
+                                                                        bnd_d + 2 + L);
   GEM_CHECK_LAUNCH("topn_bound_kernel");
   std::vector<int32_t> bnd((size_t)2 * L);
   GEM_CHECK_CUDA(cudaMemcpyAsync(bnd.data(), bnd_d + 2, (size_t)2 * L * 4, cudaMemcpyDeviceToHost, st));

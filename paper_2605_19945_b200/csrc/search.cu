@@ -199,7 +199,7 @@ constexpr int kG2Threads = 512;
 
 // U[l] = max_t (sum of the n largest counts of step t): one warp per step row
 __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, int64_t T, int E, int n,
-                                  int32_t* __restrict__ bound) {
+                                  int32_t* __restrict__ bound, int32_t* __restrict__ top1) {
   extern __shared__ int32_t tb_rows[];  // [warps][E]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int32_t* row = tb_rows + (size_t)w * E;
@@ -219,6 +219,7 @@ __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, i
         if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
       }
       sum += best;
+      if (k == 0 && top1 != nullptr && lane == 0) atomicMax(&top1[rr / T], best);
       if (lane == 0) row[bi] = -1;
       __syncwarp();
     }
@@ -1491,7 +1492,7 @@ static int prepare_screen(const int32_t* hist, int64_t L, int64_t T, int32_t E, 
   GEM_CHECK_LAUNCH("lut_monotone_kernel");
   const int warps = 8;
   topn_bound_kernel<<<(unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms()), warps * 32,
-                      (size_t)warps * E * 4, st>>>(hist, L, T, E, E / G, bound);
+                      (size_t)warps * E * 4, st>>>(hist, L, T, E, E / G, bound, nullptr);
   std::vector<int32_t> ub((size_t)L + 1);
   cudaError_t e1 = cudaGetLastError();
   cudaError_t e2 = cudaMemcpyAsync(ub.data(), bound, (size_t)(L + 1) * 4, cudaMemcpyDeviceToHost, st);
