@@ -21,7 +21,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -63,99 +62,82 @@ def parse():
 
 
 class Clocks:
-    """SM clock and throttle reasons sampled every 5 ms through NVML while the
-    timed region runs (nvidia-smi as a fallback when NVML is unavailable)."""
+    """SM clock and throttle reasons sampled DURING the timed region by an
+    `nvidia-smi -lms` child process (a separate process: a sampling thread in
+    this interpreter would take the GIL from the launch loop and open host gaps
+    between kernels). The first sample is awaited before the timed region starts."""
 
-    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
-               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
-               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
-               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
-               "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
+    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, index: int, period: float = 0.005):
+    def __init__(self, index: int, period_ms: int = 5):
         self.index = index
-        self.period = period
-        self.samples = []  # (sm_mhz, reason bitmask)
-        self.max_mhz = None
-        self.source = None
-        self._stop = threading.Event()
-        self._t = None
+        self.period_ms = period_ms
+        self.proc = None
+        self.path = None
+        self.samples = []  # (sm_mhz, max_mhz, [active reason names])
 
-    def _nvml_handle(self):
-        """The NVML handle of torch's cuda:index, matched by UUID (NVML and CUDA orders can differ)."""
-        import pynvml
-
-        pynvml.nvmlInit()
+    def _gpu_id(self) -> str:
         try:
             import torch
 
-            want = str(torch.cuda.get_device_properties(self.index).uuid)
-            for i in range(pynvml.nvmlDeviceGetCount()):
-                h = pynvml.nvmlDeviceGetHandleByIndex(i)
-                u = pynvml.nvmlDeviceGetUUID(h)
-                u = u.decode() if isinstance(u, bytes) else str(u)
-                if u.lower().removeprefix("gpu-") == want.lower():
-                    return pynvml, h
+            u = str(torch.cuda.get_device_properties(self.index).uuid)
+            return u if u.startswith("GPU-") else "GPU-" + u
         except Exception:
-            pass
-        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            return str(self.index)
+
+    def _lines(self):
+        try:
+            return [ln for ln in Path(self.path).read_text().splitlines() if ln.strip()]
+        except OSError:
+            return []
 
     def __enter__(self):
+        import tempfile
+
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
         try:
-            nv, h = self._nvml_handle()
-            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            self.source = "nvml"
-
-            def sample():
-                return (nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), nv.nvmlDeviceGetCurrentClocksEventReasons(h))
-        except Exception:
-            self.source = "nvidia-smi"
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-            def sample():
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip().split(",")
-                self.max_mhz = float(out[1])
-                mask = sum(1 << i for i in range(4) if out[2 + i].strip().lower() == "active")
-                return float(out[0]), ("smi", mask)
-
-        def run():
-            while not self._stop.is_set():
-                try:
-                    self.samples.append(sample())
-                except Exception:
-                    pass
-                self._stop.wait(self.period)
-
-        self._t = threading.Thread(target=run, daemon=True)
-        self._t.start()
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self._gpu_id(), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            t_end = time.time() + 10.0
+            while time.time() < t_end and not self._lines() and self.proc.poll() is None:
+                time.sleep(0.02)
+        except OSError:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=6)
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        for ln in self._lines():
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                self.samples.append((float(f[0]), float(f[1]),
+                                     [n for n, v in zip(self.NAMES, f[2:6]) if v.lower() == "active"]))
+            except (ValueError, IndexError):
+                continue
+        try:
+            os.unlink(self.path)
+        except OSError:
+            pass
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no clock samples"], "samples": 0}
-        sm = sorted(float(s[0]) for s in self.samples)
-        reasons = set()
-        if self.source == "nvml":
-            import pynvml
-
-            for _, mask in self.samples:
-                for name, attr in self.REASONS.items():
-                    if mask & getattr(pynvml, attr, 0):
-                        reasons.add(name)
-        else:
-            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-            for _, (_, mask) in self.samples:
-                reasons.update(names[i] for i in range(4) if mask >> i & 1)
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
-                "samples": len(self.samples), "source": self.source}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0,
+                    "source": "nvidia-smi -lms"}
+        sm = sorted(s[0] for s in self.samples)
+        reasons = sorted({r for s in self.samples for r in s[2]})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvidia-smi -lms %d (child process)" % self.period_ms}
 
 
 # ---------------------------------------------------------------------------
