@@ -58,6 +58,7 @@ struct SearchWs {
   const uint16_t* ht16;  // [L][E][Tp] transposed counts (set by the driver when every count < 65536)
   const uint16_t* ht16s; // [L][E][Tp] the same counts times 4 (byte offsets into fp32 rows; 4U < 65536)
   int32_t lut_monotone;  // every fp32 table row is nondecreasing (set by the driver)
+  int32_t win;           // loads never exceed win - 1 (= min(U, nmax)): table window of the screened scan
 };
 
 constexpr int kLocK = 8;
@@ -97,6 +98,7 @@ static size_t carve(SearchWs* ws, void* base, int64_t R, int64_t T, int G) {
   w.ht16 = nullptr;
   w.ht16s = nullptr;
   w.lut_monotone = 0;
+  w.win = 0;
   if (ws) *ws = w;
   return off;
 }
@@ -873,16 +875,24 @@ approx_scan_kernel(int64_t T, int E, int G, int64_t nmax, const int32_t* __restr
 //    cand' <= min' * (1 + 2^-16) (kWindow5). Steps past T are zero rows and
 //    add exactly 0 (C_g(0) = 0, pother' = 0).
 constexpr double kWindow5 = 1.0 + 1.0 / 65536.0;
-constexpr int kSwap5RowU16 = kSwap3TChunk + 8;  // staged count row: 32 steps + 16-byte pad (80 B)
+#ifndef GEM_SCAN_TC
+#define GEM_SCAN_TC 32
+#endif
+#ifndef GEM_SCAN_MINB
+#define GEM_SCAN_MINB 2
+#endif
+constexpr int kSwap5TChunk = GEM_SCAN_TC;
+constexpr int kSwap5RowU16 = kSwap5TChunk + 8;  // staged count row: the chunk's steps + 16-byte pad
 
 __host__ __device__ inline size_t swap5_buf_bytes(const Swap3Geom& g, int G) {
-  return (size_t)g.rpc * ((size_t)(g.n + g.nb_pad) * kSwap5RowU16 * 2 + 2 * (size_t)kSwap3TChunk * 2 +
-                          4 * ((size_t)G + 3) * kSwap3TChunk);
+  return (size_t)g.rpc * ((size_t)(g.n + g.nb_pad) * kSwap5RowU16 * 2 + 2 * (size_t)kSwap5TChunk * 2 +
+                          4 * ((size_t)G + 3) * kSwap5TChunk);
 }
 
-__host__ __device__ inline size_t swap5_smem(int E, int G, int64_t nmax) {
+// W = table window (loads never exceed W - 1)
+__host__ __device__ inline size_t swap5_smem(int E, int G, int64_t W) {
   const Swap3Geom g = swap3_geom(E, G);
-  const size_t lut = ((size_t)2 * (size_t)(nmax + 1) * 4 + 15) & ~size_t(15);
+  const size_t lut = ((size_t)2 * (size_t)W * 4 + 15) & ~size_t(15);
   const size_t fixed = (size_t)g.rpc * (8 + 8 + 8 + 8 + 2 * g.n * 2) + 64;
   return lut + 2 * swap5_buf_bytes(g, G) + fixed;
 }
@@ -893,8 +903,8 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
   return v;
 }
 
-__global__ void __launch_bounds__(kSwap3Threads, 2)
-approx_scan5_kernel(int E, int G, int64_t nmax, int monotone, const int32_t* __restrict__ run_layer,
+__global__ void __launch_bounds__(kSwap3Threads, GEM_SCAN_MINB)
+approx_scan5_kernel(int E, int G, int64_t nmax, int W, int monotone, const int32_t* __restrict__ run_layer,
                     const int8_t* __restrict__ assign, int32_t n_active, SearchWs ws) {
   extern __shared__ __align__(16) unsigned char s5[];
   const Swap3Geom geo = swap3_geom(E, G);
@@ -908,15 +918,15 @@ approx_scan5_kernel(int E, int G, int64_t nmax, int monotone, const int32_t* __r
   const int b = a + 1 + p;
   const int64_t width = nmax + 1;
   const int64_t Tp = ws.Tp;
-  constexpr int TC = kSwap3TChunk;
+  constexpr int TC = kSwap5TChunk;
   constexpr int RS = kSwap5RowU16;
   constexpr int V = TC * 2 / 16;  // 16-byte pieces per uint16 row of a chunk
   constexpr int VF = TC * 4 / 16; // 16-byte pieces per fp32 row of a chunk
   const int hrows = n + nb_pad;   // a-expert rows, then b-expert rows (zero padded)
 
   float* lut_a = reinterpret_cast<float*>(s5);
-  float* lut_b = lut_a + width;
-  unsigned char* cur = s5 + (((size_t)2 * width * 4 + 15) & ~size_t(15));
+  float* lut_b = lut_a + W;
+  unsigned char* cur = s5 + (((size_t)2 * W * 4 + 15) & ~size_t(15));
   const size_t buf_bytes = swap5_buf_bytes(geo, G);
   unsigned char* bufs = cur;
   cur += 2 * buf_bytes;
@@ -947,7 +957,7 @@ approx_scan5_kernel(int E, int G, int64_t nmax, int monotone, const int32_t* __r
   {
     const float* la32 = ws.lut32 + (int64_t)a * width;
     const float* lb32 = ws.lut32 + (int64_t)b * width;
-    for (int64_t i = tid; i < width; i += blockDim.x) {
+    for (int i = tid; i < W; i += blockDim.x) {
       lut_a[i] = __ldg(la32 + i);
       lut_b[i] = __ldg(lb32 + i);
     }
@@ -1041,7 +1051,7 @@ approx_scan5_kernel(int E, int G, int64_t nmax, int monotone, const int32_t* __r
         const float* tab = side ? lut_b : lut_a;
         int lo = 0;
         if (monotone && tab[0] <= m) {
-          int hi = (int)nmax;
+          int hi = W - 1;
           while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (tab[mid] <= m) lo = mid; else hi = mid - 1;
@@ -1396,11 +1406,13 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   GEM_CHECK_CUDA(cudaMemsetAsync(ws.loc_cnt, 0, (size_t)R * NP * 4, st));
   const Swap3Geom g = swap3_geom(E, G);
   dim3 grid((unsigned)NP, (unsigned)((n_active + g.rpc - 1) / g.rpc));
-  const size_t smem5 = swap5_smem(E, G, nmax);
+  const int W5 = ws.win > 0 ? ws.win : (int)(nmax + 1);
+  const size_t smem5 = swap5_smem(E, G, W5);
   double window = kWindow;
   if (ws.ht16s != nullptr && smem5 <= (size_t)optin && !std::getenv("GEM_SCAN_V4")) {
     GEM_CHECK_CUDA(cudaFuncSetAttribute(approx_scan5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
-    approx_scan5_kernel<<<grid, kSwap3Threads, smem5, st>>>(E, G, nmax, ws.lut_monotone && !std::getenv("GEM_SCAN_NOCLAMP"),
+    approx_scan5_kernel<<<grid, kSwap3Threads, smem5, st>>>(E, G, nmax, W5,
+                                                             ws.lut_monotone && !std::getenv("GEM_SCAN_NOCLAMP"),
                                                              run_layer, assign, (int32_t)n_active, ws);
     GEM_CHECK_LAUNCH("approx_scan5_kernel");
     window = kWindow5;
@@ -1503,6 +1515,7 @@ static int prepare_screen(const int32_t* hist, int64_t L, int64_t T, int32_t E, 
   if (e3 != cudaSuccess) return fail_cuda(e3, "topn bound sync");
   for (int64_t l = 0; l < L; ++l) sc.U = imax64(sc.U, ub[l]);
   ws.lut_monotone = ub[L] == 0;
+  ws.win = (int32_t)imin64(sc.U, nmax) + 1;
   if (sc.U >= 65536) return GEM_OK;
   GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.ht16), (size_t)L * E * ws.Tp * 2, st));
   dim3 tg((unsigned)(ws.Tp / 32), (unsigned)((E + 31) / 32), (unsigned)L);
