@@ -29,6 +29,14 @@ constexpr int kSwapTChunk = 64;
 constexpr int kSwapPairsPerThread = 4;
 // screening window: exact winners satisfy approx <= min(approx) * (1 + 2^-20) (see K6 v3 / K7 v2)
 constexpr double kWindow = 1.0 + 1.0 / 1048576.0;
+// window of the fp32-chunk-sum screens (K6 v5, K7 v3): error <= 2^-18.9 relative
+constexpr double kWindow5 = 1.0 + 1.0 / 65536.0;
+
+__device__ __forceinline__ float lds_f32(uint32_t addr) {  // 32-bit shared-window address
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
 
 struct SearchWs {
   int32_t* loads;      // [R][T][G]
@@ -252,14 +260,17 @@ __global__ void hist_t16_kernel(const int32_t* __restrict__ hist, int64_t T, int
   }
 }
 
-template <int GM>
+// FULL: G == GM (no padded GPU columns: the per-GPU guards vanish at compile time)
+template <int GM, bool FULL>
 __global__ void __launch_bounds__(kG2Threads, 1)
-greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G,
+greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
                const double* __restrict__ lut, int64_t nmax, int W, const int32_t* __restrict__ run_layer,
                const uint8_t* __restrict__ needs_greedy, const int16_t* __restrict__ order,
                int8_t* __restrict__ assign, uint16_t* __restrict__ loads16, SearchWs ws) {
+  const int G = FULL ? GM : G_;
   extern __shared__ __align__(16) unsigned char g2s[];
   float* s_lut = reinterpret_cast<float*>(g2s);                                        // [G][W]
+  const uint32_t lut_base = (uint32_t)__cvta_generic_to_shared(s_lut);
   double* red = reinterpret_cast<double*>(g2s + (((size_t)G * W * 4 + 15) & ~size_t(15)));  // [warps][GM]
   double* buf = red + (kG2Threads / 32) * GM;                                           // [kGreedyTChunk]
   __shared__ int counts[GM];
@@ -287,40 +298,51 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G,
     unsigned avail = 0;
     for (int g = 0; g < G; ++g)
       if (counts[g] < cap) avail |= 1u << g;
-    // ---- approximate scores of every GPU with capacity (any summation order)
+    // ---- approximate scores of every GPU (any summation order; GPUs without
+    // capacity are computed too and ignored by the selection). Per step: the
+    // current fp32 latencies of all GPUs (8 gathers), the max over the others
+    // of each GPU from prefix/suffix maxima (branch-free), the candidate
+    // latency C'_g(l_g + h) (one gather per GPU); every fp32 term is added to
+    // an fp64 partial sum (any order: relative error <= 2^-24 + T 2^-53, the
+    // kWindow screen -- a wider window would send more near-ties of cold
+    // experts to the exact re-score).
     double acc[GM];
+    uint32_t row_addr[GM];
 #pragma unroll
-    for (int g = 0; g < GM; ++g) acc[g] = 0.0;
+    for (int g = 0; g < GM; ++g) {
+      acc[g] = 0.0;
+      row_addr[g] = lut_base + 4u * (uint32_t)(g < G ? g : G - 1) * (uint32_t)W;
+    }
 #pragma unroll 2
     for (int64_t t = tid; t < T; t += blockDim.x) {
-      const int hv = hcol[t];
-      uint16_t lrow[GM];
+      const uint32_t hv = (uint32_t)hcol[t];
+      uint32_t lrow[GM];
       if (GM == 8) {
         const uint4 v = *reinterpret_cast<const uint4*>(ld + t * GM);
         const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) { lrow[2 * q] = (uint16_t)(w4[q] & 0xffffu); lrow[2 * q + 1] = (uint16_t)(w4[q] >> 16); }
+        for (int q = 0; q < 4; ++q) { lrow[2 * q] = w4[q] & 0xffffu; lrow[2 * q + 1] = w4[q] >> 16; }
       } else {
 #pragma unroll
         for (int g = 0; g < GM; ++g) lrow[g] = ld[t * GM + g];
       }
-      float m1 = __int_as_float(0xff800000), m2 = m1;
-      int i1 = -1;
+      // rows of GPUs g >= G (GM padding) read row G-1 and are masked by select: no branches
+      float cur[GM], pre[GM + 1], suf[GM + 1];
 #pragma unroll
       for (int g = 0; g < GM; ++g) {
-        if (g < G) {
-          const float v = s_lut[g * W + lrow[g]];
-          if (v > m1) { m2 = m1; m1 = v; i1 = g; }
-          else if (v > m2) { m2 = v; }
-        }
+        const float v = lds_f32(row_addr[g] + 4u * lrow[g]);
+        cur[g] = g < G ? v : __int_as_float(0xff800000);
       }
+      pre[0] = __int_as_float(0xff800000);
+      suf[GM] = __int_as_float(0xff800000);
+#pragma unroll
+      for (int g = 0; g < GM; ++g) pre[g + 1] = fmaxf(pre[g], cur[g]);
+#pragma unroll
+      for (int g = GM - 1; g >= 0; --g) suf[g] = fmaxf(suf[g + 1], cur[g]);
 #pragma unroll
       for (int g = 0; g < GM; ++g) {
-        if (g < G && (avail >> g & 1u)) {
-          const float cl = s_lut[g * W + lrow[g] + hv];
-          const float others = (i1 == g) ? m2 : m1;
-          acc[g] += (double)fmaxf(others, cl);
-        }
+        const float cl = lds_f32(row_addr[g] + 4u * (lrow[g] + hv));
+        acc[g] += (double)fmaxf(fmaxf(pre[g], suf[g + 1]), cl);  // g >= G: ignored by the selection
       }
     }
 #pragma unroll
@@ -349,40 +371,51 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G,
     }
     __syncthreads();
     if (s_ncand > 1) {
-      // ---- exact serial scores of the window's GPUs (v1 arithmetic, t order)
-      double best = 0.0;
-      int bg = -1;
-      for (int c = 0; c < s_ncand; ++c) {
-        const int g = s_cand[c];
-        double sum = 0.0;
-        for (int64_t t0 = 0; t0 < T; t0 += kGreedyTChunk) {
-          const int tn = (int)imin64(kGreedyTChunk, T - t0);
-          for (int tt = tid; tt < tn; tt += blockDim.x) {
-            const int64_t t = t0 + tt;
-            const uint16_t* lrow = ld + t * GM;
-            double m1 = -1.0, m2 = -1.0;
-            int i1 = -1;
-            for (int q = 0; q < G; ++q) {
-              const double v = __ldg(lut + q * width + lrow[q]);
-              if (v > m1) { m2 = m1; m1 = v; i1 = q; }
-              else if (v > m2) { m2 = v; }
-            }
-            const double cl = __ldg(lut + g * width + (int64_t)lrow[g] + h[t * E + e]);
+      // ---- exact serial scores of the window's GPUs (v1 arithmetic, t order):
+      // per chunk all threads fill the exact terms of every window GPU (one
+      // exact top-2 per step), then thread c extends candidate c's serial chain
+      const int nc = s_ncand;
+      double chain = 0.0;
+      for (int64_t t0 = 0; t0 < T; t0 += kGreedyTChunk) {
+        const int tn = (int)imin64(kGreedyTChunk, T - t0);
+        for (int tt = tid; tt < tn; tt += blockDim.x) {
+          const int64_t t = t0 + tt;
+          const uint16_t* lrow = ld + t * GM;
+          double m1 = -1.0, m2 = -1.0;
+          int i1 = -1;
+          for (int q = 0; q < G; ++q) {
+            const double v = __ldg(lut + q * width + lrow[q]);
+            if (v > m1) { m2 = m1; m1 = v; i1 = q; }
+            else if (v > m2) { m2 = v; }
+          }
+          const int hv = h[t * E + e];
+          for (int c = 0; c < nc; ++c) {
+            const int g = s_cand[c];
+            const double cl = __ldg(lut + g * width + (int64_t)lrow[g] + hv);
             double scv = cl;
             if (G > 1) {
               const double others = (i1 == g) ? m2 : m1;
               scv = others > cl ? others : cl;
             }
-            buf[tt] = scv;
+            buf[c * kGreedyTChunk + tt] = scv;
           }
-          __syncthreads();
-          if (tid == 0)
-            for (int tt = 0; tt < tn; ++tt) sum = dadd(sum, buf[tt]);
-          __syncthreads();
         }
-        if (tid == 0 && (bg < 0 || sum < best)) { best = sum; bg = g; }
+        __syncthreads();
+        if (tid < nc) {
+          const double* bc = buf + tid * kGreedyTChunk;
+          for (int tt = 0; tt < tn; ++tt) chain = dadd(chain, bc[tt]);
+        }
+        __syncthreads();
       }
-      if (tid == 0) s_best = bg;
+      if (tid < nc) red[tid] = chain;  // red[] is free again (the approximate scores are consumed)
+      __syncthreads();
+      if (tid == 0) {  // strict < in ascending GPU order (search.py:156)
+        double best = red[0];
+        int bg = s_cand[0];
+        for (int c = 1; c < nc; ++c)
+          if (red[c] < best) { best = red[c]; bg = s_cand[c]; }
+        s_best = bg;
+      }
       __syncthreads();
     }
     const int bg = s_best;
@@ -874,7 +907,6 @@ approx_scan_kernel(int64_t T, int E, int G, int64_t nmax, const int32_t* __restr
 //    cand for nonnegative tables, so the exact winner lies inside
 //    cand' <= min' * (1 + 2^-16) (kWindow5). Steps past T are zero rows and
 //    add exactly 0 (C_g(0) = 0, pother' = 0).
-constexpr double kWindow5 = 1.0 + 1.0 / 65536.0;
 #ifndef GEM_SCAN_TC
 #define GEM_SCAN_TC 32
 #endif
@@ -897,11 +929,6 @@ __host__ __device__ inline size_t swap5_smem(int E, int G, int64_t W) {
   return lut + 2 * swap5_buf_bytes(g, G) + fixed;
 }
 
-__device__ __forceinline__ float lds_f32(uint32_t addr) {
-  float v;
-  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-  return v;
-}
 
 __global__ void __launch_bounds__(kSwap3Threads, GEM_SCAN_MINB)
 approx_scan5_kernel(int E, int G, int64_t nmax, int W, int monotone, const int32_t* __restrict__ run_layer,
@@ -1443,7 +1470,7 @@ static int launch_greedy(const int32_t* hist, int64_t T, int32_t E, int32_t G, c
     const int W = (int)imin64(U, nmax) + 1;
     const int GM = G <= 8 ? 8 : (G <= 16 ? 16 : 32);
     const size_t smem = (((size_t)G * W * 4 + 15) & ~size_t(15)) + (size_t)(kG2Threads / 32) * GM * 8 +
-                        (size_t)kGreedyTChunk * 8;
+                        (size_t)GM * kGreedyTChunk * 8;
     if (smem <= (size_t)optin) {
       uint16_t* l16 = nullptr;  // uint16 per-run loads, stream-ordered scratch
       GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&l16), (size_t)R * T * GM * 2, st));
@@ -1455,7 +1482,10 @@ static int launch_greedy(const int32_t* hist, int64_t T, int32_t E, int32_t G, c
         return cudaGetLastError();
       };
       const cudaError_t ek =
-          GM == 8 ? go(greedy2_kernel<8>) : (GM == 16 ? go(greedy2_kernel<16>) : go(greedy2_kernel<32>));
+          GM == G ? (GM == 8 ? go(greedy2_kernel<8, true>) : (GM == 16 ? go(greedy2_kernel<16, true>)
+                                                                        : go(greedy2_kernel<32, true>)))
+                  : (GM == 8 ? go(greedy2_kernel<8, false>) : (GM == 16 ? go(greedy2_kernel<16, false>)
+                                                                        : go(greedy2_kernel<32, false>)));
       cudaFreeAsync(l16, st);
       if (ek != cudaSuccess) return fail_cuda(ek, "greedy2_kernel");
       return GEM_OK;
@@ -1572,7 +1602,10 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
     GEM_CHECK_CUDA(cudaEventSynchronize(g1));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, g0, g1);
-    std::fprintf(stderr, "gem_search greedy+init (%lld runs): %.3f ms\n", (long long)R, ms);
+    int32_t nex = 0;
+    cudaMemcpy(&nex, ws.counters + 2, 4, cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "gem_search greedy+init (%lld runs): %.3f ms, exact greedy re-scores %d\n", (long long)R, ms,
+                 nex);
     cudaEventDestroy(g0);
     cudaEventDestroy(g1);
   }
