@@ -357,3 +357,97 @@ def test_refine_matches_oracle(oracle):
         got, swaps = gem.refine(gem.ExpertMapping(a, 3), gem.ExpertTrace(tok), p, gem.SearchConfig())
         wa, _, wswaps, _ = oracle.refine(tok, a, oracle.Curves.from_profile(p), 1e-3, 120)
         assert swaps == wswaps and got.assignment.tolist() == wa.tolist()
+
+
+def _generated_counts(L, steps, E, k, B, seed):
+    """Router-like counts from the K9 generator (Zipf popularity, planted groups) via the oracle twin."""
+    from oracle import oracle as orc
+
+    spec = ingest.TopkTraceSpec(num_layers=L, num_tokens=steps * B, top_k=k, num_experts=E, tokens_per_step=B,
+                                seed=seed)
+    w, role = ingest.planted_layout(spec)
+    ids = orc.gen_topk(L, spec.num_tokens, k, B, E, w, role, ingest._prob_u32(spec.consistent_probability),
+                       ingest._prob_u32(spec.burst_probability), spec.burst_multiplier, seed)
+    hist, _ = orc.topk_hist(ids, B, E)
+    return hist.astype(np.int64)
+
+
+def test_search_router_like_trace_matches_oracle(oracle):
+    """K6 v5 (clamped fp32 screen, 2^-16 window), K7 v3 and K8 at a router-like shape:
+    E = 64, G = 8, 512 steps of 1024 tokens x top-8 from the synthetic generator,
+    the moderate variability profile; every restart's trajectory bit for bit."""
+    tok = _generated_counts(1, 512, 64, 8, 1024, seed=3)[0]
+    p = gem.generate_profile(gem.VariabilitySetupSpec(num_gpus=8, setup="moderate", tile_size=64, max_tokens=8192,
+                                                      rng_seed=2))
+    res = gem.search(gem.ExpertTrace(tok), p, gem.SearchConfig(restarts=3, rng_seed=11))
+    want = oracle.search(tok, oracle.Curves.from_profile(p), restarts=3, rng_seed=11)
+    assert res.best_score == want["best_score"]
+    assert res.best_mapping.assignment.tolist() == want["best_assignment"].tolist()
+    assert [r.trajectory for r in res.per_restart] == [tuple(r["trajectory"]) for r in want["records"]]
+
+
+def test_search_exact_ties_follow_reference_rules(oracle):
+    """Duplicated expert columns and GPUs with identical curves make many greedy placements
+    and swap candidates tie exactly: lowest GPU in greedy, first (i, j) in the scan."""
+    rng = np.random.default_rng(21)
+    base = random_counts(rng, 96, 16, high=120)
+    tok = np.concatenate([base, base], axis=1)  # experts e and e+16 identical
+    xs = np.arange(1, 65, dtype=np.int64) * 32
+    ys = np.cumsum(rng.uniform(0.05, 0.5, 64))
+    curve = gem.CostCurve(xs, ys, 32, int(xs[-1]))
+    p = gem.VariabilityProfile(tuple([curve] * 4), label="identical")  # four identical GPUs
+    res = gem.search(gem.ExpertTrace(tok), p, gem.SearchConfig(restarts=4, rng_seed=5))
+    want = oracle.search(tok, oracle.Curves.from_profile(p), restarts=4, rng_seed=5)
+    assert res.best_score == want["best_score"]
+    assert res.best_mapping.assignment.tolist() == want["best_assignment"].tolist()
+    assert [r.trajectory for r in res.per_restart] == [tuple(r["trajectory"]) for r in want["records"]]
+    assert [r.provenance for r in res.per_restart] == [r["provenance"] for r in want["records"]]
+
+
+def test_best_swap_screen_versions_agree(monkeypatch):
+    """One best-swap scan over many random runs: K6 v5 (default), v5 without the gather
+    clamp and v4 (GEM_SCAN_V4) return the same pair and the same exact candidate score."""
+    from paper_2605_19945_b200 import _device, _lib
+
+    L, T, E, G, R = 2, 700, 64, 8, 40
+    tok = _generated_counts(L, T, E, 8, 1024, seed=9)
+    hist, nmax = _device.counts_to_device_int32(tok)
+    p = gem.generate_profile(gem.VariabilitySetupSpec(num_gpus=G, setup="moderate", tile_size=64, max_tokens=8192,
+                                                      rng_seed=4))
+    dc = _device.DeviceCurves.from_profile(p)
+    lut = dc.lut(nmax)
+    rng = np.random.default_rng(0)
+    assign = torch.from_numpy(np.stack([balanced_assignment(rng, E, G) for _ in range(R)]).astype(np.int8)).cuda()
+    run_layer = torch.from_numpy(np.arange(R, dtype=np.int32) % L).cuda()
+    wsb = int(_lib.lib().gem_search_workspace_bytes(R, T, E, G))
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+
+    def scan():
+        found = torch.empty(R, dtype=torch.int32, device="cuda")
+        bi, bj = torch.empty_like(found), torch.empty_like(found)
+        bc = torch.empty(R, dtype=torch.float64, device="cuda")
+        _lib.call("gem_best_swap_runs", hist.data_ptr(), L, T, E, G, lut.data_ptr(), dc.lut_nmax, R,
+                  run_layer.data_ptr(), assign.data_ptr(), found.data_ptr(), bi.data_ptr(), bj.data_ptr(),
+                  bc.data_ptr(), ws.data_ptr(), wsb, torch.cuda.current_stream().cuda_stream)
+        return found.cpu().numpy(), bi.cpu().numpy(), bj.cpu().numpy(), bc.cpu().numpy()
+
+    v5 = scan()
+    monkeypatch.setenv("GEM_SCAN_NOCLAMP", "1")
+    v5n = scan()
+    monkeypatch.delenv("GEM_SCAN_NOCLAMP")
+    monkeypatch.setenv("GEM_SCAN_V4", "1")
+    v4 = scan()
+    for a, b in ((v5, v5n), (v5, v4)):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    # and one run against the reference kernel protocol (oracle best_swap)
+    from oracle import oracle as orc
+
+    r = 3
+    a0 = assign[r].cpu().numpy().astype(np.int64)
+    t0 = tok[r % L]
+    loads = orc.load_matrix(t0, a0, G)
+    cv = orc.Curves.from_profile(p)
+    lat = orc.latency_matrix(cv, loads)
+    found, i, j, cand = orc.best_swap(t0, a0, loads, lat, cv)
+    assert (bool(v5[0][r]), int(v5[1][r]), int(v5[2][r]), float(v5[3][r])) == (bool(found), i, j, cand)
