@@ -42,7 +42,7 @@ constexpr int kLtThreads = 256;
 constexpr int kLtN = 256;        // MMA N (candidate x GPU columns per CTA)
 constexpr int kMaxKeys = 65536;  // u16 keys
 constexpr int kSumThreads = 256;
-constexpr int kSumSmemVals = 4096;  // vals[0, 4096) in shared memory (32 KB)
+constexpr int kSumSmemVals = 8192;  // vals[0, 8192) in shared memory (64 KB)
 
 struct LoadsTcShared {
   uint64_t mma_bar;
@@ -284,36 +284,53 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
 }
 
 // ---------------------------------------------------------------------------
-// pass 2: thread = (candidate, layer of the batch), serial over t
-__global__ void __launch_bounds__(kSumThreads)
+// pass 2: thread = (4 consecutive candidates, layer of the batch), four
+// serial chains over t; one 8-byte load carries the 4 step keys (Cp is a
+// multiple of 8: candidate tiles are 256/G >= 8 wide). vals[0, kSumSmemVals)
+// sits in shared memory (99.9% of step maxima at C4 rank below 8,192); a
+// miss goes to L2 on the chain's critical path.
+__global__ void __launch_bounds__(kSumThreads, 3)
 keysum_kernel(const uint16_t* __restrict__ keys, int64_t T, int64_t C, int64_t Cp, int64_t L, int64_t layer0,
               const double* __restrict__ vals, const int32_t* __restrict__ nvals, double* __restrict__ layer_scores) {
-  __shared__ double s_vals[kSumSmemVals];
+  extern __shared__ double s_vals[];  // [kSumSmemVals]
   const int K = min(*nvals, kSumSmemVals);
   for (int i = threadIdx.x; i < K; i += blockDim.x) s_vals[i] = vals[i];
   __syncthreads();
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int64_t lb = blockIdx.y;
-  if (c >= C) return;
-  const uint16_t* p = keys + lb * T * Cp + c;
+  if (c0 >= C) return;
+  const uint2* p = reinterpret_cast<const uint2*>(keys + lb * T * Cp + c0);
+  const int64_t stride = Cp / 4;  // uint2 per step
   auto val = [&](uint32_t k) -> double { return k < (uint32_t)kSumSmemVals ? s_vals[k] : __ldg(vals + k); };
-  // keys 8 steps ahead of the serial fp64 chain (which stays in t order)
+  // keys 8 steps ahead of the serial fp64 chains (which stay in t order)
   constexpr int D = 8;
-  uint32_t q[D];
+  uint2 q[D];
 #pragma unroll
-  for (int d = 0; d < D; ++d) q[d] = d < T ? p[(int64_t)d * Cp] : 0u;
-  double s = 0.0;
+  for (int d = 0; d < D; ++d) q[d] = d < T ? __ldcs(p + (int64_t)d * stride) : make_uint2(0u, 0u);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int64_t t = 0;
   for (; t + D <= T; t += D) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const double v = val(q[d]);
-      q[d] = t + D + d < T ? p[(t + D + d) * Cp] : 0u;
-      s = dadd(s, v);
+      const uint2 k = q[d];
+      q[d] = t + D + d < T ? __ldcs(p + (t + D + d) * stride) : make_uint2(0u, 0u);
+      s0 = dadd(s0, val(k.x & 0xffffu));
+      s1 = dadd(s1, val(k.x >> 16));
+      s2 = dadd(s2, val(k.y & 0xffffu));
+      s3 = dadd(s3, val(k.y >> 16));
     }
   }
-  for (int d = 0; t < T; ++t, ++d) s = dadd(s, val(q[d]));
-  layer_scores[c * L + layer0 + lb] = s;
+  for (int d = 0; t < T; ++t, ++d) {
+    const uint2 k = q[d];
+    s0 = dadd(s0, val(k.x & 0xffffu));
+    s1 = dadd(s1, val(k.x >> 16));
+    s2 = dadd(s2, val(k.y & 0xffffu));
+    s3 = dadd(s3, val(k.y >> 16));
+  }
+  const double sv[4] = {s0, s1, s2, s3};
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (c0 + j < C) layer_scores[(c0 + j) * L + layer0 + lb] = sv[j];
 }
 
 template <int E>
@@ -426,22 +443,27 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   GEM_CHECK_LAUNCH("key_table_kernel");
   const double* vals = reinterpret_cast<const double*>(uniq);  // the bit patterns are the values
 
-  // ---- layer batches: P layers of u16 step keys [P][T][Cp] in flight (<= ~8 GB)
+  // ---- layer batches: P layers of u16 step keys [P][T][Cp] in flight (<= ~32 GB)
   const int CT = kLtN / G;
   const int64_t ntile = (C + CT - 1) / CT;
   const int64_t Cp = ntile * CT;
   const size_t per_layer = (size_t)T * Cp * 2;
-  int64_t P = imin64((int64_t)(8ull << 30) / (int64_t)per_layer, L);
+  int64_t P = imin64((int64_t)(32ull << 30) / (int64_t)per_layer, L);
   if (P < 1) return 1;
   auto* kbuf = static_cast<uint16_t*>(alloc(per_layer * P));
   if (!kbuf) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc key buffer");
+  GEM_CHECK_CUDA(cudaFuncSetAttribute(keysum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSumSmemVals * 8));
+  GEM_CHECK_CUDA(cudaFuncSetAttribute(keysum_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      cudaSharedmemCarveoutMaxShared));  // 3 CTAs x 64 KB per SM
   for (int64_t l0 = 0; l0 < L; l0 += P) {
     const int64_t nb = imin64(P, L - l0);
     const dim3 g1((unsigned)ntile, (unsigned)nb);
     const int rc = E == 128 ? launch_maxkey<128>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, W, kbuf)
                             : launch_maxkey<64>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, W, kbuf);
     if (rc) return rc;
-    keysum_kernel<<<dim3((unsigned)((C + kSumThreads - 1) / kSumThreads), (unsigned)nb), kSumThreads, 0, st>>>(
+    keysum_kernel<<<dim3((unsigned)((C + 4 * kSumThreads - 1) / (4 * kSumThreads)), (unsigned)nb), kSumThreads,
+                    (size_t)kSumSmemVals * 8, st>>>(
         kbuf, T, C, Cp, L, l0, vals, nu, layer_scores);
     GEM_CHECK_LAUNCH("keysum_kernel");
   }
