@@ -105,6 +105,14 @@ int gem_topk_hist(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32
                   int32_t B, int32_t E, int32_t* hist, int64_t* colsum, int32_t* active,
                   int64_t* dropped, void* stream);
 
+/* The same for one chunk of a longer trace (streamed router dumps, token-range
+ * shards written into a full-length histogram): the chunk's ceil(N/B) step
+ * rows of layer l go to hist + l*hist_rows*E (pass hist + t0*E for a chunk
+ * that starts at step t0); hist_rows >= ceil(N/B). */
+int gem_topk_hist_rows(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k,
+                       int32_t B, int32_t E, int32_t* hist, int64_t hist_rows, int64_t* colsum,
+                       int32_t* active, int64_t* dropped, void* stream);
+
 /* hist [L,T,E] (int32) -> colsum/active (accumulated) — for traces given as
  * counts (ExpertTrace) instead of ids. */
 int gem_hist_colstats(const int32_t* hist, int64_t L, int64_t T, int32_t E,

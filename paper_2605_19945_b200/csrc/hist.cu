@@ -82,7 +82,7 @@ __device__ __forceinline__ void count_scalar(uint32_t* cnt_lane, uint32_t id, ui
 // layer. MAXR = histogram rows owned per lane in the reduction (rows/32).
 template <typename IdT, bool WIDE, int MAXR>
 __global__ void __launch_bounds__(kHistWarps * 32, WIDE ? 3 : 2)
-topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B, int E, int64_t T,
+topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
                  int32_t* __restrict__ hist, int64_t* __restrict__ colsum, int32_t* __restrict__ active,
                  int64_t* __restrict__ dropped_out) {
   extern __shared__ __align__(16) uint32_t hsm[];
@@ -143,7 +143,7 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
         if (++in_step == bps) {
           in_step = 0;
           __syncwarp();
-          int32_t* hrow = hist + (l * T + t) * E;
+          int32_t* hrow = hist + (l * HT + t) * E;
 #pragma unroll
           for (int q = 0; q < MAXR; ++q) {
             const int row = lane + q * 32;
@@ -219,7 +219,7 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
       // Reduce the 32 lane-private columns of every row. Lane owns rows
       // lane + 32q and reads them as 8 x 128-bit chunks, chunk (c+lane)&7 in
       // iteration c (4 wavefronts per LDS.128: conflict-free), zeroing as it goes.
-      int32_t* hrow = hist + (l * T + t) * E;
+      int32_t* hrow = hist + (l * HT + t) * E;
 #pragma unroll
       for (int q = 0; q < MAXR; ++q) {
         const int row = lane + q * 32;
@@ -291,7 +291,8 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
 }
 
 template <typename IdT, bool WIDE, int MAXR>
-static int launch_hist_t(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int32_t* hist,
+static int launch_hist_t(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
+                         int32_t* hist,
                          int64_t* colsum, int32_t* active, int64_t* dropped, cudaStream_t st) {
   const int rows = WIDE ? E + 1 : (E + 2) / 2;
   const size_t smem = (size_t)kHistWarps * rows * 32 * sizeof(uint32_t);
@@ -305,39 +306,55 @@ static int launch_hist_t(const void* ids, int64_t L, int64_t N, int k, int B, in
   const int64_t need = (units + kHistWarps - 1) / kHistWarps;
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, kHistWarps * 32, smem, st>>>((const IdT*)ids, L, N, k, B, E, T, hist, colsum, active,
+  kern<<<(unsigned)blocks, kHistWarps * 32, smem, st>>>((const IdT*)ids, L, N, k, B, E, T, HT, hist, colsum, active,
                                                          dropped);
   GEM_CHECK_LAUNCH("topk_hist_kernel");
   return GEM_OK;
 }
 
 template <typename IdT>
-static int dispatch_hist(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int32_t* hist,
+static int dispatch_hist(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
+                         int32_t* hist,
                          int64_t* colsum, int32_t* active, int64_t* dropped, cudaStream_t st) {
-  if (E <= 64) return launch_hist_t<IdT, true, 2>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
-  if (E <= 128) return launch_hist_t<IdT, true, 4>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
-  if (E <= kWideMaxE) return launch_hist_t<IdT, true, 5>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
-  if (E <= 256) return launch_hist_t<IdT, false, 4>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
-  return launch_hist_t<IdT, false, 8>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
+  if (E <= 64) return launch_hist_t<IdT, true, 2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+  if (E <= 128) return launch_hist_t<IdT, true, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+  if (E <= kWideMaxE) return launch_hist_t<IdT, true, 5>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+  if (E <= 256) return launch_hist_t<IdT, false, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+  return launch_hist_t<IdT, false, 8>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
 }
 
 }  // namespace gem
 
 using namespace gem;
 
+static int topk_hist_rows(const char* who, const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k,
+                          int32_t B, int32_t E, int32_t* hist, int64_t hist_rows, int64_t* colsum, int32_t* active,
+                          int64_t* dropped, void* stream) {
+  GEM_REQUIRE(id_bytes == 2 || id_bytes == 4, "%s: id_bytes must be 2 or 4", who);
+  GEM_REQUIRE(L >= 1 && N >= 1 && k >= 1 && B >= 1 && E >= 1 && E <= 512,
+              "%s: bad shape L=%lld N=%lld k=%d B=%d E=%d (E <= 512)", who, (long long)L, (long long)N, k, B, E);
+  GEM_REQUIRE(ids && hist && colsum && active && dropped, "%s: null pointer", who);
+  // a lane's u32 (wide) or u16 (packed) counter must not wrap within one step
+  GEM_REQUIRE(E <= kWideMaxE || (int64_t)B * k <= 65535, "%s: E > %d needs at most 65535 ids per step", who,
+              kWideMaxE);
+  const int64_t T = (N + B - 1) / B;
+  GEM_REQUIRE(hist_rows >= T, "%s: %lld histogram rows per layer cannot hold %lld steps", who, (long long)hist_rows,
+              (long long)T);
+  cudaStream_t st = as_stream(stream);
+  if (id_bytes == 2) return dispatch_hist<int16_t>(ids, L, N, k, B, E, T, hist_rows, hist, colsum, active, dropped, st);
+  return dispatch_hist<int32_t>(ids, L, N, k, B, E, T, hist_rows, hist, colsum, active, dropped, st);
+}
+
 extern "C" int gem_topk_hist(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k, int32_t B,
                              int32_t E, int32_t* hist, int64_t* colsum, int32_t* active, int64_t* dropped,
                              void* stream) {
-  GEM_REQUIRE(id_bytes == 2 || id_bytes == 4, "gem_topk_hist: id_bytes must be 2 or 4");
-  GEM_REQUIRE(L >= 1 && N >= 1 && k >= 1 && B >= 1 && E >= 1 && E <= 512,
-              "gem_topk_hist: bad shape L=%lld N=%lld k=%d B=%d E=%d (E <= 512)", (long long)L, (long long)N, k,
-              B, E);
-  GEM_REQUIRE(ids && hist && colsum && active && dropped, "gem_topk_hist: null pointer");
-  // a lane's u32 (wide) or u16 (packed) counter must not wrap within one step
-  GEM_REQUIRE(E <= kWideMaxE || (int64_t)B * k <= 65535,
-              "gem_topk_hist: E > %d needs at most 65535 ids per step", kWideMaxE);
-  const int64_t T = (N + B - 1) / B;
-  cudaStream_t st = as_stream(stream);
-  if (id_bytes == 2) return dispatch_hist<int16_t>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
-  return dispatch_hist<int32_t>(ids, L, N, k, B, E, T, hist, colsum, active, dropped, st);
+  return topk_hist_rows("gem_topk_hist", ids, id_bytes, L, N, k, B, E, hist, (N + B - 1) / B, colsum, active,
+                        dropped, stream);
+}
+
+extern "C" int gem_topk_hist_rows(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k, int32_t B,
+                                  int32_t E, int32_t* hist, int64_t hist_rows, int64_t* colsum, int32_t* active,
+                                  int64_t* dropped, void* stream) {
+  return topk_hist_rows("gem_topk_hist_rows", ids, id_bytes, L, N, k, B, E, hist, hist_rows, colsum, active,
+                        dropped, stream);
 }

@@ -83,13 +83,14 @@ def test_cli_matches_reference_gpu(case, tmp_path, capsys):
 
 
 def test_cli_parser_surface():
-    """Every reference sub-command exists with the reference's flags."""
+    """Every reference sub-command exists with the reference's flags (plus the
+    router-dump `ingest` addition)."""
     from paper_2605_19945_b200 import cli
 
     parser = cli.build_parser()
     sub = next(a for a in parser._actions if a.dest == "command")
     assert set(sub.choices) == {"gen-trace", "gen-profile", "optimize", "score", "replay", "compare", "baseline",
-                                "scale-study", "multi-layer", "stats"}
+                                "scale-study", "multi-layer", "stats", "ingest"}
     opt = sub.choices["optimize"]
     flags = {s for a in opt._actions for s in a.option_strings}
     assert {"--trace", "--profile", "--mapping-out", "--restarts", "--noise", "--threshold", "--max-swaps",
