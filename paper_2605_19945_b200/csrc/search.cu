@@ -29,6 +29,7 @@ constexpr int kSwapTChunk = 64;
 constexpr int kSwapPairsPerThread = 4;
 // screening window: exact winners satisfy approx <= min(approx) * (1 + 2^-20) (see K6 v3 / K7 v2)
 constexpr double kWindow = 1.0 + 1.0 / 1048576.0;
+constexpr int kBuckets = 1024;  // value buckets of the clamp-point search (K6 v5)
 // window of the fp32-chunk-sum screens (K6 v5, K7 v3): error <= 2^-18.9 relative
 constexpr double kWindow5 = 1.0 + 1.0 / 65536.0;
 
@@ -67,6 +68,8 @@ struct SearchWs {
   const uint16_t* ht16s; // [L][E][Tp] the same counts times 4 (byte offsets into fp32 rows; 4U < 65536)
   int32_t lut_monotone;  // every fp32 table row is nondecreasing (set by the driver)
   int32_t win;           // loads never exceed win - 1 (= min(U, nmax)): table window of the screened scan
+  const uint16_t* first;  // [G][kBuckets + 2] first n whose value bucket is >= b (clamp-point search hints)
+  const float* bscale;    // [G] buckets per unit latency: bucket(v) = min(kBuckets, (int)(v * bscale[g]))
 };
 
 constexpr int kLocK = 8;
@@ -107,6 +110,8 @@ static size_t carve(SearchWs* ws, void* base, int64_t R, int64_t T, int G) {
   w.ht16s = nullptr;
   w.lut_monotone = 0;
   w.win = 0;
+  w.first = nullptr;
+  w.bscale = nullptr;
   if (ws) *ws = w;
   return off;
 }
@@ -925,15 +930,19 @@ __host__ __device__ inline size_t swap5_buf_bytes(const Swap3Geom& g, int G) {
 __host__ __device__ inline size_t swap5_smem(int E, int G, int64_t W) {
   const Swap3Geom g = swap3_geom(E, G);
   const size_t lut = ((size_t)2 * (size_t)W * 4 + 15) & ~size_t(15);
-  const size_t fixed = (size_t)g.rpc * (8 + 8 + 8 + 8 + 2 * g.n * 2) + 64;
+  const size_t fixed = (size_t)g.rpc * (8 + 8 + 8 + 8) + ((((size_t)g.rpc * 2 * g.n * 2) + 15) & ~size_t(15)) +
+                       2 * (kBuckets + 2) * 2 + 64;
   return lut + 2 * swap5_buf_bytes(g, G) + fixed;
 }
 
 
+// GT > 0: instantiated for exactly GT GPUs (the pother pass unrolls); 0: any G
+template <int GT>
 __global__ void __launch_bounds__(kSwap3Threads, GEM_SCAN_MINB)
-approx_scan5_kernel(int E, int G, int64_t nmax, int W, int monotone, const int32_t* __restrict__ run_layer,
+approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int32_t* __restrict__ run_layer,
                     const int8_t* __restrict__ assign, int32_t n_active, SearchWs ws) {
   extern __shared__ __align__(16) unsigned char s5[];
+  const int G = GT > 0 ? GT : G_;
   const Swap3Geom geo = swap3_geom(E, G);
   const int n = geo.n, ng = geo.ng, RPC = geo.rpc, nb_pad = geo.nb_pad;
   const int NP = G * (G - 1) / 2;
@@ -962,6 +971,9 @@ approx_scan5_kernel(int E, int G, int64_t nmax, int W, int monotone, const int32
   const uint16_t** lsrc = reinterpret_cast<const uint16_t**>(cur);       cur += (size_t)RPC * 8;
   const float** fsrc = reinterpret_cast<const float**>(cur);             cur += (size_t)RPC * 8;
   int16_t* lists = reinterpret_cast<int16_t*>(cur);                       // [RPC][2][n]
+  cur += (((size_t)RPC * 2 * n * 2) + 15) & ~size_t(15);
+  uint16_t* first_a = reinterpret_cast<uint16_t*>(cur);                   // [kBuckets + 2] x 2
+  uint16_t* first_b = first_a + (kBuckets + 2);
   struct Buf {
     uint16_t* h;   // [RPC][hrows][RS]  4 * count
     uint16_t* l;   // [RPC][2][TC]      l_a, l_b
@@ -987,6 +999,10 @@ approx_scan5_kernel(int E, int G, int64_t nmax, int W, int monotone, const int32
     for (int i = tid; i < W; i += blockDim.x) {
       lut_a[i] = __ldg(la32 + i);
       lut_b[i] = __ldg(lb32 + i);
+    }
+    for (int i = tid; i < kBuckets + 2; i += blockDim.x) {
+      first_a[i] = ws.first[a * (kBuckets + 2) + i];
+      first_b[i] = ws.first[b * (kBuckets + 2) + i];
     }
   }
   if (tid < RPC) smin[tid] = ord_bits(__longlong_as_double(0x7ff0000000000000LL));
@@ -1019,27 +1035,67 @@ approx_scan5_kernel(int E, int G, int64_t nmax, int W, int monotone, const int32
 
   const int pieces_h = 2 * n * V, pieces_l = 2 * V, pieces_f = G * VF;
   const int pieces_run = pieces_h + pieces_l + pieces_f;
-  auto issue = [&](int64_t t0, int k) {
-    const Buf B = buf_at(k);
-    for (int i = tid; i < nruns * pieces_run; i += blockDim.x) {
-      const int ss = i / pieces_run;
-      int q = i - ss * pieces_run;
-      if (q < pieces_h) {
-        const int row = q / V, v = q - row * V;  // rows [0, n): a experts; [n, 2n): b experts
-        const int e = row < n ? lists[(ss * 2 + 0) * n + row] : lists[(ss * 2 + 1) * n + row - n];
-        cp_async16(B.h + ((size_t)ss * hrows + row) * RS + v * 8, hsrc[ss] + (int64_t)e * Tp + t0 + v * 8);
-      } else if ((q -= pieces_h) < pieces_l) {
-        const int which = q / V, v = q - which * V;
-        cp_async16(B.l + ((size_t)ss * 2 + which) * TC + v * 8,
-                   lsrc[ss] + (int64_t)(which ? b : a) * Tp + t0 + v * 8);
-      } else {
-        q -= pieces_l;
-        const int g = q / VF, v = q - g * VF;
-        cp_async16(B.lat + ((size_t)ss * G + g) * TC + v * 4, fsrc[ss] + (int64_t)g * Tp + t0 + v * 4);
+  // this thread's 16-byte cp.async pieces of a chunk (source at t0 = 0, byte
+  // offset in a staging buffer); a chunk at t0 adds t0 * element size
+  constexpr int kMaxPieces = 4;
+  const bool fixed_pieces = nruns * pieces_run <= kMaxPieces * (int)blockDim.x;
+  const char* psrc[kMaxPieces];
+  uint32_t pdst[kMaxPieces], pshift[kMaxPieces];
+  int npieces = 0;
+  auto piece = [&](int i, const char*& src, uint32_t& dst, uint32_t& sh) {
+    const int ss = i / pieces_run;
+    int q = i - ss * pieces_run;
+    const Buf B0 = buf_at(0);
+    const unsigned char* base0 = bufs;
+    if (q < pieces_h) {
+      const int row = q / V, v = q - row * V;  // rows [0, n): a experts; [n, 2n): b experts
+      const int e = row < n ? lists[(ss * 2 + 0) * n + row] : lists[(ss * 2 + 1) * n + row - n];
+      dst = (uint32_t)(reinterpret_cast<unsigned char*>(B0.h + ((size_t)ss * hrows + row) * RS + v * 8) - base0);
+      src = reinterpret_cast<const char*>(hsrc[ss] + (int64_t)e * Tp + v * 8);
+      sh = 1;
+    } else if ((q -= pieces_h) < pieces_l) {
+      const int which = q / V, v = q - which * V;
+      dst = (uint32_t)(reinterpret_cast<unsigned char*>(B0.l + ((size_t)ss * 2 + which) * TC + v * 8) - base0);
+      src = reinterpret_cast<const char*>(lsrc[ss] + (int64_t)(which ? b : a) * Tp + v * 8);
+      sh = 1;
+    } else {
+      q -= pieces_l;
+      const int g = q / VF, v = q - g * VF;
+      dst = (uint32_t)(reinterpret_cast<unsigned char*>(B0.lat + ((size_t)ss * G + g) * TC + v * 4) - base0);
+      src = reinterpret_cast<const char*>(fsrc[ss] + (int64_t)g * Tp + v * 4);
+      sh = 2;
+    }
+  };
+  if (fixed_pieces) {
+#pragma unroll
+    for (int j = 0; j < kMaxPieces; ++j) {
+      const int i = tid + j * (int)blockDim.x;
+      psrc[j] = nullptr;
+      pdst[j] = 0;
+      pshift[j] = 0;
+      if (i < nruns * pieces_run) {
+        piece(i, psrc[j], pdst[j], pshift[j]);
+        npieces = j + 1;
       }
+    }
+  }
+  auto issue = [&](int64_t t0, int k) {
+    unsigned char* bk = bufs + k * buf_bytes;
+    if (fixed_pieces) {
+#pragma unroll
+      for (int j = 0; j < kMaxPieces; ++j)
+        if (j < npieces) cp_async16(bk + pdst[j], psrc[j] + (t0 << pshift[j]));
+      return;
+    }
+    for (int i = tid; i < nruns * pieces_run; i += blockDim.x) {
+      const char* src;
+      uint32_t dst, sh;
+      piece(i, src, dst, sh);
+      cp_async16(bk + dst, src + (t0 << sh));
     }
   };
 
+  const float bscale_a = ws.bscale[a], bscale_b = ws.bscale[b];
   const uint32_t base_a = (uint32_t)__cvta_generic_to_shared(lut_a);
   const uint32_t base_b = (uint32_t)__cvta_generic_to_shared(lut_b);
   const int units_total = nruns * geo.units_per_run;
@@ -1078,7 +1134,13 @@ approx_scan5_kernel(int E, int G, int64_t nmax, int W, int monotone, const int32
         const float* tab = side ? lut_b : lut_a;
         int lo = 0;
         if (monotone && tab[0] <= m) {
-          int hi = W - 1;
+          // the clamp point lies in [first[q] - 1, first[q+1] - 1], q = bucket(m):
+          // values in lower buckets are < m, values in higher buckets are > m
+          const uint16_t* fb = side ? first_b : first_a;
+          const float sc = side ? bscale_b : bscale_a;
+          const int q = min(kBuckets, (int)(m * sc));
+          lo = max((int)fb[q] - 1, 0);
+          int hi = max((int)fb[q + 1] - 1, lo);
           while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (tab[mid] <= m) lo = mid; else hi = mid - 1;
@@ -1274,6 +1336,34 @@ __global__ void state_t_kernel(int64_t R, int64_t T, int G, int64_t width, Searc
   }
 }
 
+// clamp-point search hints (K6 v5): bscale[g] = kBuckets / (largest value of
+// row g inside the window), bucket(v) = min(kBuckets, (int)(v * bscale[g]))
+__global__ void bucket_scale_kernel(const float* __restrict__ lut32, int G, int64_t width, int W,
+                                    float* __restrict__ bscale) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  const float vmax = lut32[(int64_t)g * width + W - 1];
+  bscale[g] = vmax > 0.0f ? (float)kBuckets / vmax : 0.0f;
+}
+
+// first[g][b] = smallest n in [0, W) with bucket(lut32[g][n]) >= b (W if none),
+// b in [0, kBuckets + 1]; rows are nondecreasing, so n writes the buckets in
+// (bucket(n-1), bucket(n)] and the last n also those above its bucket
+__global__ void bucket_first_kernel(const float* __restrict__ lut32, int G, int64_t width, int W,
+                                    const float* __restrict__ bscale, uint16_t* __restrict__ first) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)G * W;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int g = (int)(i / W), nn = (int)(i - (int64_t)g * W);
+    const float sc = bscale[g];
+    auto bk = [&](int n) { return min(kBuckets, (int)(lut32[(int64_t)g * width + n] * sc)); };
+    const int lo = nn == 0 ? -1 : bk(nn - 1), hi = bk(nn);
+    uint16_t* f = first + (int64_t)g * (kBuckets + 2);
+    for (int b = lo + 1; b <= hi; ++b) f[b] = (uint16_t)nn;
+    if (nn == W - 1)
+      for (int b = hi + 1; b <= kBuckets + 1; ++b) f[b] = (uint16_t)W;
+  }
+}
+
 // flag[0] = 1 when some fp32 table row decreases somewhere
 __global__ void lut_monotone_kernel(const float* __restrict__ lut32, int G, int64_t width, int32_t* __restrict__ flag) {
   const int64_t n = (int64_t)G * width;
@@ -1436,12 +1526,17 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   const int W5 = ws.win > 0 ? ws.win : (int)(nmax + 1);
   const size_t smem5 = swap5_smem(E, G, W5);
   double window = kWindow;
-  if (ws.ht16s != nullptr && smem5 <= (size_t)optin && !std::getenv("GEM_SCAN_V4")) {
-    GEM_CHECK_CUDA(cudaFuncSetAttribute(approx_scan5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
-    approx_scan5_kernel<<<grid, kSwap3Threads, smem5, st>>>(E, G, nmax, W5,
-                                                             ws.lut_monotone && !std::getenv("GEM_SCAN_NOCLAMP"),
-                                                             run_layer, assign, (int32_t)n_active, ws);
-    GEM_CHECK_LAUNCH("approx_scan5_kernel");
+  if (ws.ht16s != nullptr && ws.first != nullptr && smem5 <= (size_t)optin && !std::getenv("GEM_SCAN_V4")) {
+    const int clamp = ws.lut_monotone && !std::getenv("GEM_SCAN_NOCLAMP");
+    auto go5 = [&](auto kern) -> int {
+      GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
+      kern<<<grid, kSwap3Threads, smem5, st>>>(E, G, nmax, W5, clamp, run_layer, assign, (int32_t)n_active, ws);
+      GEM_CHECK_LAUNCH("approx_scan5_kernel");
+      return GEM_OK;
+    };
+    const int rc5 = G == 8 ? go5(approx_scan5_kernel<8>) : (G == 4 ? go5(approx_scan5_kernel<4>)
+                                                                    : go5(approx_scan5_kernel<0>));
+    if (rc5) return rc5;
     window = kWindow5;
   } else {
     GEM_CHECK_CUDA(cudaFuncSetAttribute(approx_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
@@ -1507,9 +1602,13 @@ struct Screen {
   float* lut32 = nullptr;
   uint16_t* ht16 = nullptr;
   uint16_t* ht16s = nullptr;
+  uint16_t* first = nullptr;
+  float* bscale = nullptr;
   int64_t U = 0;
   cudaStream_t st = nullptr;
   ~Screen() {
+    if (first) cudaFreeAsync(first, st);
+    if (bscale) cudaFreeAsync(bscale, st);
     if (lut32) cudaFreeAsync(lut32, st);
     if (ht16) cudaFreeAsync(ht16, st);
     if (ht16s) cudaFreeAsync(ht16s, st);
@@ -1546,6 +1645,17 @@ static int prepare_screen(const int32_t* hist, int64_t L, int64_t T, int32_t E, 
   for (int64_t l = 0; l < L; ++l) sc.U = imax64(sc.U, ub[l]);
   ws.lut_monotone = ub[L] == 0;
   ws.win = (int32_t)imin64(sc.U, nmax) + 1;
+  if (ws.win <= 65535) {  // u16 search hints
+    GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.bscale), (size_t)G * 4, st));
+    GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.first), (size_t)G * (kBuckets + 2) * 2, st));
+    bucket_scale_kernel<<<1, 32 * ((G + 31) / 32), 0, st>>>(sc.lut32, G, nmax + 1, ws.win, sc.bscale);
+    GEM_CHECK_LAUNCH("bucket_scale_kernel");
+    bucket_first_kernel<<<(unsigned)imin64(((int64_t)G * ws.win + 255) / 256, 4096), 256, 0, st>>>(
+        sc.lut32, G, nmax + 1, ws.win, sc.bscale, sc.first);
+    GEM_CHECK_LAUNCH("bucket_first_kernel");
+    ws.first = sc.first;
+    ws.bscale = sc.bscale;
+  }
   if (sc.U >= 65536) return GEM_OK;
   GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.ht16), (size_t)L * E * ws.Tp * 2, st));
   dim3 tg((unsigned)(ws.Tp / 32), (unsigned)((E + 31) / 32), (unsigned)L);
