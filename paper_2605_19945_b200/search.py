@@ -159,6 +159,38 @@ def layer_jobs(mean_util: np.ndarray, num_gpus: int, config: SearchConfig, layer
                     np.asarray(orders, dtype=np.int16), np.asarray(assigns, dtype=np.int8), prov)
 
 
+def all_layer_jobs(mean_util: np.ndarray, num_gpus: int, config: SearchConfig) -> RunBatch:
+    """layer_jobs for every layer of mean_util [L, E] at once, in the same run
+    order. The restart noise comes from default_rng(seed ^ i) -- the same draw
+    for every layer -- so it is drawn once per restart; the keys are the same
+    fp64 products and a stable argsort of -key is the reference's lexsort
+    (descending key, ascending expert index on ties)."""
+    mu = np.asarray(mean_util, dtype=np.float64)
+    L, E = mu.shape
+    K = config.restarts
+    nb = 2 if config.seed_with_baselines else 0
+    per = K + nb
+    order = np.empty((L, per, E), dtype=np.int16)
+    assign = np.zeros((L, per, E), dtype=np.int8)
+    for i in range(K):
+        keys = mu
+        if i > 0:
+            eta = np.random.default_rng(config.rng_seed ^ i).uniform(-1.0, 1.0, E)
+            keys = mu * (1.0 + config.noise_fraction * eta)
+        order[:, i] = np.argsort(-keys, axis=1, kind="stable")
+    prov = [f"greedy:{i}" for i in range(K)]
+    if nb:
+        order[:, K:] = np.arange(E, dtype=np.int16)
+        assign[:, K] = linear_assignment(E, num_gpus)
+        for l in range(L):
+            assign[l, K + 1] = eplb_assignment(mu[l], num_gpus)
+        prov += ["baseline:linear", "baseline:eplb"]
+    greedy = np.zeros(per, dtype=np.uint8)
+    greedy[:K] = 1
+    return RunBatch(np.repeat(np.arange(L, dtype=np.int32), per), np.tile(greedy, L),
+                    order.reshape(L * per, E), assign.reshape(L * per, E), prov * L)
+
+
 def concat_batches(batches: list[RunBatch]) -> RunBatch:
     return RunBatch(np.concatenate([b.run_layer for b in batches]),
                     np.concatenate([b.needs_greedy for b in batches]),
@@ -285,11 +317,10 @@ def search_hist(hist: torch.Tensor, nmax: int, profile: VariabilityProfile, conf
         ds = device_stats(hist, with_gram=False)
         mu_dev, _, _ = finalize_stats(ds, with_corr=False)
         mean_util = _device.host(mu_dev)
-    batches = [layer_jobs(mean_util[l], G, config, l) for l in range(L)]
-    batch = concat_batches(batches)
+    batch = all_layer_jobs(np.asarray(mean_util).reshape(L, E), G, config)
     res = run_search_device(hist, nmax, profile, batch, config.convergence_threshold, config.swap_cap(E))
     out = []
-    per = len(batches[0].provenance)
+    per = len(batch.provenance) // L
     for l in range(L):
         lo, hi = l * per, (l + 1) * per
         best = _pick_best(res.final_score, lo, hi)

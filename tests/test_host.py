@@ -246,3 +246,24 @@ def test_product_never_imports_the_oracle():
     for f in pkg.rglob("*.py"):
         text = f.read_text()
         assert "import oracle" not in text and "from oracle" not in text, f
+
+
+def test_all_layer_jobs_equals_per_layer_jobs():
+    """The batched job builder reproduces layer_jobs (the reference's restart
+    orders, search.py:134-193) for every layer, including key ties."""
+    import importlib
+
+    S = importlib.import_module("paper_2605_19945_b200.search")
+    rng = np.random.default_rng(3)
+    mu = rng.random((5, 16))
+    mu[2, 3] = mu[2, 7]  # exact tie
+    mu[4] = 1.0 / 16     # all tied
+    for cfg in (gem.SearchConfig(rng_seed=7, restarts=6), gem.SearchConfig(rng_seed=1, restarts=3,
+                                                                            seed_with_baselines=False)):
+        want = S.concat_batches([S.layer_jobs(mu[l], 4, cfg, l) for l in range(5)])
+        got = S.all_layer_jobs(mu, 4, cfg)
+        assert np.array_equal(got.order, want.order)
+        assert np.array_equal(got.assign, want.assign)
+        assert np.array_equal(got.needs_greedy, want.needs_greedy)
+        assert np.array_equal(got.run_layer, want.run_layer)
+        assert got.provenance == want.provenance
