@@ -72,8 +72,14 @@ struct SearchWs {
   const float* bscale;    // [G] buckets per unit latency: bucket(v) = min(kBuckets, (int)(v * bscale[g]))
 };
 
-constexpr int kLocK = 8;
-constexpr int kCandK = 32;
+#ifndef GEM_LOCK
+#define GEM_LOCK 16
+#endif
+#ifndef GEM_CANDK
+#define GEM_CANDK 64
+#endif
+constexpr int kLocK = GEM_LOCK;
+constexpr int kCandK = GEM_CANDK;
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
