@@ -1277,11 +1277,15 @@ __global__ void exact_pairs_kernel(const int32_t* __restrict__ hist, int64_t T, 
   const int64_t width = nmax + 1;
   const int32_t* h = hist + (int64_t)run_layer[r] * T * E;
   const int32_t* ld = ws.loads + (int64_t)r * T * G;
+  // lanes fill 256 exact terms per chunk (coalesced rows), lane 0 extends the
+  // serial fp64 chain from shared memory (no shuffle round trip per term)
+  __shared__ double xbuf[8][256];  // blockDim.x == 256: one row per warp
+  double* xb = xbuf[(threadIdx.x >> 5) & 7];
   double sum = 0.0;
-  for (int64_t t0 = 0; t0 < T; t0 += 32) {
-    const int64_t t = t0 + lane;
-    double m = 0.0;
-    if (t < T) {
+  for (int64_t t0 = 0; t0 < T; t0 += 256) {
+    const int tn = (int)imin64(256, T - t0);
+    for (int q = lane; q < tn; q += 32) {
+      const int64_t t = t0 + q;
       const int32_t* lrow = ld + t * G;
       double po = __longlong_as_double(0xfff0000000000000LL);
       for (int g = 0; g < G; ++g) {
@@ -1292,12 +1296,15 @@ __global__ void exact_pairs_kernel(const int32_t* __restrict__ hist, int64_t T, 
       const int32_t hi = h[t * E + i], hj = h[t * E + j];
       const double va = __ldg(lut + a * width + (lrow[a] - hi + hj));
       const double vb = __ldg(lut + b * width + (lrow[b] - hj + hi));
-      m = po;
+      double m = po;
       m = va > m ? va : m;
       m = vb > m ? vb : m;
+      xb[q] = m;
     }
-    const int tn = (int)imin64(32, T - t0);
-    for (int q = 0; q < tn; ++q) sum = dadd(sum, __shfl_sync(0xffffffffu, m, q));
+    __syncwarp();
+    if (lane == 0)
+      for (int q = 0; q < tn; ++q) sum = dadd(sum, xb[q]);
+    __syncwarp();
   }
   if (lane == 0) ws.cand_exact[(int64_t)r * kCandK + k] = sum;
 }
