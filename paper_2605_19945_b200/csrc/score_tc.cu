@@ -28,6 +28,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
+#include <cstdlib>
 #include <vector>
 
 #include "gem_common.cuh"
@@ -36,7 +37,8 @@
 namespace gem {
 
 __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, int64_t T, int E, int n,
-                                  int32_t* __restrict__ bound, int32_t* __restrict__ top1);  // search.cu
+                                  int32_t* __restrict__ bound, int32_t* __restrict__ top1,
+                                  int32_t* __restrict__ rowmin);  // search.cu
 
 constexpr int kLtThreads = 256;
 constexpr int kLtN = 256;        // MMA N (candidate x GPU columns per CTA)
@@ -105,6 +107,33 @@ __global__ void key_table_kernel(const unsigned long long* __restrict__ bits, in
   }
 }
 
+// Gather clamp (as in K6 v5): every step's maximum is at least
+// LB = min_g key[g][ceil(bmin/G)] (some GPU carries >= 1/G of the step's
+// bmin+ ids, and keys grow with the load), so a load n <= thr[g] (the largest
+// n with key[g][n] <= LB) may read key[g][thr[g]] instead without changing the
+// maximum; those lanes share one address. out[g] = 0x4B000000 + thr[g] (the
+// fp32 bit pattern of 2^23 + thr: the epilogue clamps the pattern directly).
+__global__ void key_clamp_kernel(const uint16_t* __restrict__ keys, int G, int W, const int32_t* __restrict__ bmin,
+                                 uint32_t* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  const int q = min(W - 1, (max(*bmin, 0) + G - 1) / G);
+  int lb = 0x7fffffff;
+  for (int g = 0; g < G; ++g) lb = min(lb, (int)keys[(int64_t)g * W + q]);
+  for (int g = 0; g < G; ++g) {
+    const uint16_t* row = keys + (int64_t)g * W;
+    if (row[0] > lb) {
+      out[g] = 0x4B000000u;
+      continue;
+    }
+    int lo = 0, hi = W - 1;  // largest n with row[n] <= lb
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (row[mid] <= lb) lo = mid; else hi = mid - 1;
+    }
+    out[g] = 0x4B000000u + (uint32_t)lo;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // pass 1: CTA = (candidate tile of CT = N/G candidates, layer of the batch);
 // loops over every 128-step tile of the layer in order: produce the fp16 H
@@ -113,7 +142,7 @@ template <int E, int G>
 __global__ void __launch_bounds__(kLtThreads, 1)
 maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __restrict__ cand, int64_t C,
                  int64_t L, int64_t layer0, int64_t Cp, const uint16_t* __restrict__ gkeys, int W,
-                 uint16_t* __restrict__ out_keys) {
+                 const uint32_t* __restrict__ nbmin_g, uint16_t* __restrict__ out_keys) {
   constexpr int KCH = E / 8;                 // 16-byte K chunks (8 fp16 experts)
   constexpr uint32_t LBO_A = 128 * 16 + 16;  // A: [KCH][128 rows][16 B], K slices padded by 16 B (bank spread)
   constexpr uint32_t LBO_B = kLtN * 16;      // B: [KCH][N rows][16 B]
@@ -191,9 +220,12 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
   };
   // per-GPU row offsets into the key table (bytes), biased by the fp32 exponent
   // pattern so that (bits of n + 2^23) * 2 + off[g] addresses key[g][n]
-  uint32_t koff[G];
+  uint32_t koff[G], nbmin[G];
 #pragma unroll
-  for (int g = 0; g < G; ++g) koff[g] = sk_addr + 2u * (uint32_t)g * (uint32_t)W - 2u * 0x4B000000u;
+  for (int g = 0; g < G; ++g) {
+    koff[g] = sk_addr + 2u * (uint32_t)g * (uint32_t)W - 2u * 0x4B000000u;
+    nbmin[g] = nbmin_g[g];
+  }
   load_rows(0);
   for (int i = 0; i < ntiles; ++i) {
     // ---- H tile i: exact int -> fp32 (2^23 trick) -> packed fp16 pairs, 8-byte K-major stores
@@ -240,7 +272,7 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
           for (int g = 0; g < G; ++g) {
             // exact integer n < 2^16 in fp32: + 2^23 puts it in the low mantissa bits
             const uint32_t nb = __float_as_uint(__uint_as_float(v[j * G + g]) + 8388608.0f);
-            const uint32_t addr = nb * 2u + koff[g];
+            const uint32_t addr = max(nb, nbmin[g]) * 2u + koff[g];
             uint16_t key;
             asm("ld.shared.u16 %0, [%1];" : "=h"(key) : "r"(addr));
             m = max(m, (uint32_t)key);
@@ -336,10 +368,10 @@ keysum_kernel(const uint16_t* __restrict__ keys, int64_t T, int64_t C, int64_t C
 template <int E>
 static int launch_maxkey(int G, dim3 grid, size_t smem, cudaStream_t st, const int32_t* hist, int64_t T,
                          const int8_t* cand, int64_t C, int64_t L, int64_t l0, int64_t Cp, const uint16_t* keys,
-                         int W, uint16_t* out) {
+                         int W, const uint32_t* nbmin, uint16_t* out) {
   auto pick = [&](auto kern) -> int {
     GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, kLtThreads, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, W, out);
+    kern<<<grid, kLtThreads, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, W, nbmin, out);
     GEM_CHECK_LAUNCH("maxkey_tc_kernel");
     return GEM_OK;
   };
@@ -386,9 +418,11 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
     return p;
   };
   // ---- bounds: experts per GPU, load window, largest count (one host sync)
-  int32_t* bnd_d = static_cast<int32_t*>(alloc((size_t)(2 + 2 * L) * 4));  // [2] cand stats, [L] top-n, [L] max
+  // [2] cand stats, [L] top-n, [L] max, [1] smallest step total, [G] gather clamp patterns
+  int32_t* bnd_d = static_cast<int32_t*>(alloc((size_t)(3 + 2 * L + G) * 4));
   if (!bnd_d) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc scratch");
   GEM_CHECK_CUDA(cudaMemsetAsync(bnd_d, 0, (size_t)(2 + 2 * L) * 4, st));
+  GEM_CHECK_CUDA(cudaMemsetAsync(bnd_d + 2 + 2 * L, 0x7f, 4, st));  // rowmin starts at 0x7f7f7f7f
   cand_stats_kernel<<<(unsigned)imin64((C * L + 7) / 8, 16 * num_sms()), 256, (size_t)8 * G * 4, st>>>(
       cand, C * L, E, G, bnd_d);
   GEM_CHECK_LAUNCH("cand_stats_kernel");
@@ -400,7 +434,7 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   const int warps = 8;
   const unsigned tb_grid = (unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms());
   topn_bound_kernel<<<tb_grid, warps * 32, (size_t)warps * E * 4, st>>>(hist, L, T, E, maxcnt, bnd_d + 2,
-                                                                        bnd_d + 2 + L);
+                                                                        bnd_d + 2 + L, bnd_d + 2 + 2 * L);
   GEM_CHECK_LAUNCH("topn_bound_kernel");
   std::vector<int32_t> bnd((size_t)2 * L);
   GEM_CHECK_CUDA(cudaMemcpyAsync(bnd.data(), bnd_d + 2, (size_t)2 * L * 4, cudaMemcpyDeviceToHost, st));
@@ -442,6 +476,14 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   key_table_kernel<<<(unsigned)imin64((cnt + 255) / 256, 4096), 256, 0, st>>>(bits, cnt, uniq, nu, keys);
   GEM_CHECK_LAUNCH("key_table_kernel");
   const double* vals = reinterpret_cast<const double*>(uniq);  // the bit patterns are the values
+  uint32_t* nbmin = reinterpret_cast<uint32_t*>(bnd_d + 3 + 2 * L);
+  if (std::getenv("GEM_SCORE_NOCLAMP")) {
+    std::vector<uint32_t> nb0((size_t)G, 0x4B000000u);
+    GEM_CHECK_CUDA(cudaMemcpyAsync(nbmin, nb0.data(), (size_t)G * 4, cudaMemcpyHostToDevice, st));
+  } else {
+    key_clamp_kernel<<<1, 32, 0, st>>>(keys, G, W, bnd_d + 2 + 2 * L, nbmin);
+    GEM_CHECK_LAUNCH("key_clamp_kernel");
+  }
 
   // ---- layer batches: P layers of u16 step keys [P][T][Cp] in flight (<= ~32 GB)
   const int CT = kLtN / G;
@@ -459,8 +501,8 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   for (int64_t l0 = 0; l0 < L; l0 += P) {
     const int64_t nb = imin64(P, L - l0);
     const dim3 g1((unsigned)ntile, (unsigned)nb);
-    const int rc = E == 128 ? launch_maxkey<128>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, W, kbuf)
-                            : launch_maxkey<64>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, W, kbuf);
+    const int rc = E == 128 ? launch_maxkey<128>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, W, nbmin, kbuf)
+                            : launch_maxkey<64>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, W, nbmin, kbuf);
     if (rc) return rc;
     keysum_kernel<<<dim3((unsigned)((C + 4 * kSumThreads - 1) / (4 * kSumThreads)), (unsigned)nb), kSumThreads,
                     (size_t)kSumSmemVals * 8, st>>>(

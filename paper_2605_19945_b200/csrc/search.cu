@@ -220,14 +220,24 @@ constexpr int kG2Threads = 512;
 
 // U[l] = max_t (sum of the n largest counts of step t): one warp per step row
 __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, int64_t T, int E, int n,
-                                  int32_t* __restrict__ bound, int32_t* __restrict__ top1) {
+                                  int32_t* __restrict__ bound, int32_t* __restrict__ top1,
+                                  int32_t* __restrict__ rowmin) {
   extern __shared__ int32_t tb_rows[];  // [warps][E]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int32_t* row = tb_rows + (size_t)w * E;
   const int64_t rows = L * T;
   for (int64_t rr = (int64_t)blockIdx.x * nw + w; rr < rows; rr += (int64_t)gridDim.x * nw) {
     const int32_t* h = hist + rr * E;
-    for (int e = lane; e < E; e += 32) row[e] = h[e];
+    int64_t rs = 0;  // the step's total (rowmin: smallest over all steps)
+    for (int e = lane; e < E; e += 32) {
+      row[e] = h[e];
+      rs += h[e];
+    }
+    if (rowmin != nullptr) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+      if (lane == 0) atomicMin(rowmin, (int32_t)(rs < 0x7fffffff ? rs : 0x7fffffff));
+    }
     __syncwarp();
     int64_t sum = 0;
     for (int k = 0; k < n; ++k) {
@@ -1646,7 +1656,7 @@ static int prepare_screen(const int32_t* hist, int64_t L, int64_t T, int32_t E, 
   GEM_CHECK_LAUNCH("lut_monotone_kernel");
   const int warps = 8;
   topn_bound_kernel<<<(unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms()), warps * 32,
-                      (size_t)warps * E * 4, st>>>(hist, L, T, E, E / G, bound, nullptr);
+                      (size_t)warps * E * 4, st>>>(hist, L, T, E, E / G, bound, nullptr, nullptr);
   std::vector<int32_t> ub((size_t)L + 1);
   cudaError_t e1 = cudaGetLastError();
   cudaError_t e2 = cudaMemcpyAsync(ub.data(), bound, (size_t)(L + 1) * 4, cudaMemcpyDeviceToHost, st);
