@@ -107,31 +107,37 @@ __global__ void key_table_kernel(const unsigned long long* __restrict__ bits, in
   }
 }
 
-// Gather clamp (as in K6 v5): every step's maximum is at least
-// LB = min_g key[g][ceil(bmin/G)] (some GPU carries >= 1/G of the step's
-// bmin+ ids, and keys grow with the load), so a load n <= thr[g] (the largest
-// n with key[g][n] <= LB) may read key[g][thr[g]] instead without changing the
-// maximum; those lanes share one address. out[g] = 0x4B000000 + thr[g] (the
-// fp32 bit pattern of 2^23 + thr: the epilogue clamps the pattern directly).
+// Gather clamp (as in K6 v5). thr_g(K) = the largest load whose key on GPU g
+// is <= K. If every GPU's key were <= K, the step could hold at most
+// sum_g thr_g(K) ids; so with LB = the smallest K whose sum reaches the
+// smallest step total bmin (the water-filling level), every step's maximum
+// key is >= LB. A load n <= thr_g(LB) may then read key[g][thr_g(LB)]
+// instead without changing the maximum, and all such lanes share one address.
+// out[g] = 0x4B000000 + thr_g(LB) (the fp32 bit pattern of 2^23 + thr: the
+// epilogue clamps the pattern directly).
 __global__ void key_clamp_kernel(const uint16_t* __restrict__ keys, int G, int W, const int32_t* __restrict__ bmin,
                                  uint32_t* __restrict__ out) {
   if (threadIdx.x != 0) return;
-  const int q = min(W - 1, (max(*bmin, 0) + G - 1) / G);
-  int lb = 0x7fffffff;
-  for (int g = 0; g < G; ++g) lb = min(lb, (int)keys[(int64_t)g * W + q]);
-  for (int g = 0; g < G; ++g) {
+  auto thr = [&](int g, int K) {  // largest n with key[g][n] <= K, -1 if none (rows are nondecreasing)
     const uint16_t* row = keys + (int64_t)g * W;
-    if (row[0] > lb) {
-      out[g] = 0x4B000000u;
-      continue;
-    }
-    int lo = 0, hi = W - 1;  // largest n with row[n] <= lb
+    if (row[0] > K) return -1;
+    int lo = 0, hi = W - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (row[mid] <= lb) lo = mid; else hi = mid - 1;
+      if (row[mid] <= K) lo = mid; else hi = mid - 1;
     }
-    out[g] = 0x4B000000u + (uint32_t)lo;
+    return lo;
+  };
+  const int64_t need = max(*bmin, 0);
+  int klo = 0, khi = 0;
+  for (int g = 0; g < G; ++g) khi = max(khi, (int)keys[(int64_t)g * W + W - 1]);
+  while (klo < khi) {  // smallest K with sum_g (thr_g(K) + 1) >= need (K = khi always qualifies)
+    const int mid = (klo + khi) >> 1;
+    int64_t cap = 0;
+    for (int g = 0; g < G; ++g) cap += thr(g, mid) + 1;
+    if (cap >= need) khi = mid; else klo = mid + 1;
   }
+  for (int g = 0; g < G; ++g) out[g] = 0x4B000000u + (uint32_t)max(thr(g, klo), 0);
 }
 
 // ---------------------------------------------------------------------------
