@@ -62,6 +62,7 @@ struct SearchWs {
   double* cand_exact;  // [R][kCandK]
   float* latT;         // [R][G][Tp] fp32 latencies of the current loads (screened scan)
   uint16_t* loadT;     // [R][G][Tp] current loads (screened scan)
+  uint32_t* top3;      // [R][4][Tp] per step: the three largest fp32 latencies (bits) and their GPUs (packed)
   int64_t Tp;          // T rounded up to 32 (whole 16-byte pieces for every chunk of the transposed arrays)
   const float* lut32;  // [G][nmax+1] fp32 rounding of the latency table (set by the driver)
   const uint16_t* ht16;  // [L][E][Tp] transposed counts (set by the driver when every count < 65536)
@@ -111,6 +112,7 @@ static size_t carve(SearchWs* ws, void* base, int64_t R, int64_t T, int G) {
   w.Tp = (T + 31) / 32 * 32;
   w.latT = (float*)take((size_t)R * G * w.Tp * 4);
   w.loadT = (uint16_t*)take((size_t)R * G * w.Tp * 2);
+  w.top3 = (uint32_t*)take((size_t)R * 4 * w.Tp * 4);
   w.lut32 = nullptr;
   w.ht16 = nullptr;
   w.ht16s = nullptr;
@@ -938,8 +940,9 @@ constexpr int kSwap5TChunk = GEM_SCAN_TC;
 constexpr int kSwap5RowU16 = kSwap5TChunk + 8;  // staged count row: the chunk's steps + 16-byte pad
 
 __host__ __device__ inline size_t swap5_buf_bytes(const Swap3Geom& g, int G) {
+  (void)G;
   return (size_t)g.rpc * ((size_t)(g.n + g.nb_pad) * kSwap5RowU16 * 2 + 2 * (size_t)kSwap5TChunk * 2 +
-                          4 * ((size_t)G + 3) * kSwap5TChunk);
+                          4 * ((size_t)4 + 3) * kSwap5TChunk);  // top-3 rows (4), pother', 2 clamp rows
 }
 
 // W = table window (loads never exceed W - 1)
@@ -1002,7 +1005,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
     Buf B;
     B.h = reinterpret_cast<uint16_t*>(c);  c += (size_t)RPC * hrows * RS * 2;
     B.l = reinterpret_cast<uint16_t*>(c);  c += (size_t)RPC * 2 * TC * 2;
-    B.lat = reinterpret_cast<float*>(c);   c += (size_t)RPC * G * TC * 4;
+    B.lat = reinterpret_cast<float*>(c);   c += (size_t)RPC * 4 * TC * 4;  // top-3 values + packed GPUs
     B.po = reinterpret_cast<float*>(c);    c += (size_t)RPC * TC * 4;
     B.th = reinterpret_cast<uint32_t*>(c);
     return B;
@@ -1026,7 +1029,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
     const int r = ws.run_list[slot0 + tid];
     hsrc[tid] = ws.ht16s + (int64_t)run_layer[r] * E * Tp;
     lsrc[tid] = ws.loadT + (int64_t)r * G * Tp;
-    fsrc[tid] = ws.latT + (int64_t)r * G * Tp;
+    fsrc[tid] = reinterpret_cast<const float*>(ws.top3) + (int64_t)r * 4 * Tp;
   }
   for (int w = wid; w < nruns; w += nw) {
     const int r = ws.run_list[slot0 + w];
@@ -1049,7 +1052,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
   }
   __syncthreads();
 
-  const int pieces_h = 2 * n * V, pieces_l = 2 * V, pieces_f = G * VF;
+  const int pieces_h = 2 * n * V, pieces_l = 2 * V, pieces_f = 4 * VF;
   const int pieces_run = pieces_h + pieces_l + pieces_f;
   // this thread's 16-byte cp.async pieces of a chunk (source at t0 = 0, byte
   // offset in a staging buffer); a chunk at t0 adds t0 * element size
@@ -1077,7 +1080,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
     } else {
       q -= pieces_l;
       const int g = q / VF, v = q - g * VF;
-      dst = (uint32_t)(reinterpret_cast<unsigned char*>(B0.lat + ((size_t)ss * G + g) * TC + v * 4) - base0);
+      dst = (uint32_t)(reinterpret_cast<unsigned char*>(B0.lat + ((size_t)ss * 4 + g) * TC + v * 4) - base0);
       src = reinterpret_cast<const char*>(fsrc[ss] + (int64_t)g * Tp + v * 4);
       sh = 2;
     }
@@ -1142,10 +1145,12 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
         const int side = rr >= nruns * TC;
         const int r2 = side ? rr - nruns * TC : rr;
         const int ss = r2 / TC, tt = r2 % TC;
-        const float* lat = B.lat + (size_t)ss * G * TC + tt;
-        float m = __int_as_float(0xff800000);  // -inf when G == 2
-        for (int g = 0; g < G; ++g)
-          if (g != a && g != b) m = fmaxf(m, lat[g * TC]);
+        const float* lat = B.lat + (size_t)ss * 4 * TC + tt;
+        const uint32_t ix = __float_as_uint(lat[3 * TC]);
+        const uint32_t j1 = ix & 0xffu, j2 = (ix >> 8) & 0xffu;
+        // pother' = the first of the top-3 on neither a nor b (-inf when G == 2)
+        const float m = (j1 != (uint32_t)a && j1 != (uint32_t)b) ? lat[0]
+                        : ((j2 != (uint32_t)a && j2 != (uint32_t)b) ? lat[TC] : lat[2 * TC]);
         if (!side) B.po[ss * TC + tt] = m;
         const float* tab = side ? lut_b : lut_a;
         int lo = 0;
@@ -1396,6 +1401,31 @@ __global__ void lut_monotone_kernel(const float* __restrict__ lut32, int G, int6
   }
 }
 
+// per active run and step: the three largest fp32 latencies and their GPUs
+// (-inf / 255 past G). pother of a GPU pair (a, b) is the first of them on
+// neither a nor b, so a scan tile stages 4 rows instead of G.
+__global__ void top3_kernel(int32_t n_active, int64_t Tp, int G, SearchWs ws) {
+  const int64_t total = (int64_t)n_active * Tp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i % Tp;
+    const int r = ws.run_list[i / Tp];
+    const float* lat = ws.latT + (int64_t)r * G * Tp + t;
+    float v1 = __int_as_float(0xff800000), v2 = v1, v3 = v1;
+    uint32_t i1 = 255, i2 = 255, i3 = 255;
+    for (int g = 0; g < G; ++g) {
+      const float v = lat[(int64_t)g * Tp];
+      if (v > v1) { v3 = v2; i3 = i2; v2 = v1; i2 = i1; v1 = v; i1 = g; }
+      else if (v > v2) { v3 = v2; i3 = i2; v2 = v; i2 = g; }
+      else if (v > v3) { v3 = v; i3 = g; }
+    }
+    uint32_t* out = ws.top3 + (int64_t)r * 4 * Tp + t;
+    out[0] = __float_as_uint(v1);
+    out[Tp] = __float_as_uint(v2);
+    out[2 * Tp] = __float_as_uint(v3);
+    out[3 * Tp] = i1 | (i2 << 8) | (i3 << 16);
+  }
+}
+
 // fp64 latency table -> its fp32 rounding (round to nearest: monotone)
 __global__ void lut_to_f32_kernel(const double* __restrict__ lut, int64_t n, float* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -1550,6 +1580,9 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   const size_t smem5 = swap5_smem(E, G, W5);
   double window = kWindow;
   if (ws.ht16s != nullptr && ws.first != nullptr && smem5 <= (size_t)optin && !std::getenv("GEM_SCAN_V4")) {
+    top3_kernel<<<(unsigned)imin64((n_active * ws.Tp + 255) / 256, 16 * num_sms()), 256, 0, st>>>(
+        (int32_t)n_active, ws.Tp, G, ws);
+    GEM_CHECK_LAUNCH("top3_kernel");
     const int clamp = ws.lut_monotone && !std::getenv("GEM_SCAN_NOCLAMP");
     auto go5 = [&](auto kern) -> int {
       GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
