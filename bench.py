@@ -456,7 +456,7 @@ def cpu_stats_run(ids_np, B, E, cores):
 
 def cpu_stats_baseline(spec, ids_dev):
     """Bounded sample: `cores` layer-slices of 4096 steps (4M tokens) each, one process per core."""
-    cores = min(os.cpu_count() or 1, 16)
+    cores = len(os.sched_getaffinity(0)) or 1  # every host core this process may use
     steps = min(spec.num_steps, 4096)
     n = steps * spec.tokens_per_step
     layers = min(spec.num_layers, cores)
@@ -485,7 +485,7 @@ def run_reference(args):
     # same-shape synthetic ids: Zipf(1.1)-popular experts, sampled with numpy (the
     # CPU arm must not run our kernels, and the reference's cost does not depend
     # on which ids are drawn, only on how many)
-    cores = min(os.cpu_count() or 1, 16)
+    cores = len(os.sched_getaffinity(0)) or 1  # every host core this process may use
     layers = min(L, cores)
     sample_tokens = min(N, 4096 * B)
     rng = np.random.default_rng(0)
