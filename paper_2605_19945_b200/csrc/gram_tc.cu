@@ -31,7 +31,12 @@
 
 namespace gem {
 
-constexpr int kGtcThreads = 256;
+#ifndef GEM_GTC_WARPS
+#define GEM_GTC_WARPS 16
+#endif
+constexpr int kGtcWarps = GEM_GTC_WARPS;   // producer warps (all of them also drain TMEM)
+constexpr int kGtcThreads = 32 * kGtcWarps;
+constexpr int kGtcTasksPerWarp = 32 / kGtcWarps;  // (16 steps x 32 experts) tasks per warp and stage
 constexpr int kGtcStages = 4;
 constexpr int64_t kSegSteps = 16384;
 constexpr int kGtcStageBytes = 32768;
@@ -58,7 +63,7 @@ gram_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int64_t total
   constexpr uint32_t LBO = ROWS * 16; // bytes per 16-step K slice
   constexpr int TG = KT / 16;         // 16-step groups per stage
   constexpr int TASKS = TG * 4 * NB;  // (16 steps x 32 experts) tasks per stage
-  static_assert(TASKS == 32, "8 warps x 4 tasks");
+  static_assert(TASKS == 32 && TASKS == kGtcWarps * kGtcTasksPerWarp, "32 tasks per stage");
   static_assert(TG * LBO == kGtcStageBytes, "stage size");
 
   extern __shared__ __align__(1024) unsigned char gtc_smem[];
@@ -99,12 +104,12 @@ gram_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int64_t total
     const int32_t* hl = hist + l * T * E;
     const int nchunks = (int)((seg_len + KT - 1) / KT);
 
-    int4 cur[4][4], nxt[4][4];
-    auto load_chunk = [&](int c, int4 (&buf)[4][4]) {
+    int4 cur[kGtcTasksPerWarp][4], nxt[kGtcTasksPerWarp][4];
+    auto load_chunk = [&](int c, int4 (&buf)[kGtcTasksPerWarp][4]) {
       const int64_t tc0 = t_begin + (int64_t)c * KT;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int task = warp * 4 + q;
+      for (int q = 0; q < kGtcTasksPerWarp; ++q) {
+        const int task = warp * kGtcTasksPerWarp + q;
         const int blk = task / (TG * 4);
         const int rem = task % (TG * 4);
         const int tg = rem >> 2, eg = rem & 3;
@@ -123,8 +128,8 @@ gram_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int64_t total
       if (chunk >= kGtcStages) tc::mbar_wait(&sh->stage_bar[slot], (uint32_t)((chunk / kGtcStages - 1) & 1));
       unsigned char* st = ring + slot * kGtcStageBytes;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int task = warp * 4 + q;
+      for (int q = 0; q < kGtcTasksPerWarp; ++q) {
+        const int task = warp * kGtcTasksPerWarp + q;
         const int blk = task / (TG * 4);
         const int rem = task % (TG * 4);
         const int tg = rem >> 2, eg = rem & 3;
@@ -174,7 +179,7 @@ gram_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int64_t total
       }
       ++chunk;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < kGtcTasksPerWarp; ++q)
 #pragma unroll
         for (int r = 0; r < 4; ++r) cur[q][r] = nxt[q][r];
     }
@@ -183,12 +188,13 @@ gram_tc_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int64_t total
     tc::mbar_wait(&sh->acc_bar, (uint32_t)(seg_no & 1));
     tc::tc_fence_after();
     {
-      const int lg = warp & 3, ch = warp >> 2;
+      const int lg = warp & 3, ch = warp >> 2;  // TMEM lane group, column slice of 128 / (warps / 4)
+      constexpr int CW = 128 / (kGtcWarps / 4);
       const int a = blkA + lg * 32 + lane;
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16);
       int64_t* grow = gram + (l * E + a) * E + blkB;
 #pragma unroll 1
-      for (int b0 = ch * 64; b0 < ch * 64 + 64; b0 += 16) {
+      for (int b0 = ch * CW; b0 < ch * CW + CW; b0 += 16) {
         uint32_t ll[16], lh[16], hl2[16], hh[16];
         tc::tmem_ld16(trow + b0, ll);
         tc::tmem_ld16(trow + 128 + b0, lh);
