@@ -30,8 +30,9 @@ constexpr int kSwapPairsPerThread = 4;
 // screening window: exact winners satisfy approx <= min(approx) * (1 + 2^-20) (see K6 v3 / K7 v2)
 constexpr double kWindow = 1.0 + 1.0 / 1048576.0;
 constexpr int kBuckets = 1024;  // value buckets of the clamp-point search (K6 v5)
-// window of the fp32-chunk-sum screens (K6 v5, K7 v3): error <= 2^-18.9 relative
-constexpr double kWindow5 = 1.0 + 1.0 / 65536.0;
+// window of the fp32-chunk-sum screen (K6 v5): error < 2^-18.9 relative, so the
+// exact winner is within (1 + 2^-18.9) / (1 - 2^-18.9) < 1 + 2^-17.8 of the minimum
+constexpr double kWindow5 = 1.0 + 1.0 / 131072.0;
 
 __device__ __forceinline__ float lds_f32(uint32_t addr) {  // 32-bit shared-window address
   float v;
@@ -928,7 +929,7 @@ approx_scan_kernel(int64_t T, int E, int G, int64_t nmax, const int32_t* __restr
 //    summed in fp32 over a 32-step chunk and the chunk sum is added to an
 //    fp64 chain: |cand' - cand| <= (32 * 2^-24 + (T/32) 2^-53) cand < 2^-18.9
 //    cand for nonnegative tables, so the exact winner lies inside
-//    cand' <= min' * (1 + 2^-16) (kWindow5). Steps past T are zero rows and
+//    cand' <= min' * (1 + 2^-17) (kWindow5). Steps past T are zero rows and
 //    add exactly 0 (C_g(0) = 0, pother' = 0).
 #ifndef GEM_SCAN_TC
 #define GEM_SCAN_TC 32
