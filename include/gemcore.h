@@ -228,6 +228,13 @@ int gem_best_swap_runs(const int32_t* hist, int64_t L, int64_t T, int32_t E, int
                        double* best_cand, void* workspace, size_t workspace_bytes,
                        void* stream);
 
+/* --- scale study (scale.py:100-129) ---------------------------------------
+ * draws [S, nmax] f64 (host-drawn with the reference's generator), sizes [K]
+ * strictly increasing in [1, nmax]: gaps[k][s] = (max - min) / max over
+ * draws[s][0 .. sizes[k]) -- the mean over s is taken by the caller. */
+int gem_scale_gaps(const double* draws, int64_t S, int64_t nmax, const int64_t* sizes, int32_t K,
+                   double* gaps, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -97,9 +97,10 @@ def test_cli_parser_surface():
             "--no-baseline-seeds", "--seed", "--output", "--verbose", "--quiet"} <= flags
 
 
-def test_cli_scale_study_is_reported_out_of_scope(capsys):
+def test_cli_scale_study_rejects_bad_distribution(capsys):
+    """Domain errors exit with code 2 before any kernel runs (cli.py:587-592)."""
     from paper_2605_19945_b200 import cli
 
-    rc = cli.main(["scale-study", "--dist", "uniform", "--params", "0.9,1.1", "--seed", "1"])
+    rc = cli.main(["scale-study", "--dist", "uniform", "--params", "1.2,1.1", "--seed", "1"])
     assert rc == 2
-    assert "scale-study" in capsys.readouterr().err
+    assert "lo <= hi" in capsys.readouterr().err
