@@ -711,6 +711,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __global__ void __launch_bounds__(kSwap3Threads, 2)
 approx_scan_kernel(int64_t T, int E, int G, int64_t nmax, const int32_t* __restrict__ run_layer,
@@ -938,6 +940,11 @@ approx_scan_kernel(int64_t T, int E, int G, int64_t nmax, const int32_t* __restr
 #define GEM_SCAN_MINB 2
 #endif
 constexpr int kSwap5TChunk = GEM_SCAN_TC;
+#ifndef GEM_SCAN_STAGES
+#define GEM_SCAN_STAGES 3
+#endif
+constexpr int kSwap5Stages = GEM_SCAN_STAGES;  // cp.async staging buffers
+static_assert(kSwap5Stages >= 3, "the scan issues chunk c+S-1 after chunk c-1's slot is free");
 constexpr int kSwap5RowU16 = kSwap5TChunk + 8;  // staged count row: the chunk's steps + 16-byte pad
 
 __host__ __device__ inline size_t swap5_buf_bytes(const Swap3Geom& g, int G) {
@@ -952,7 +959,7 @@ __host__ __device__ inline size_t swap5_smem(int E, int G, int64_t W) {
   const size_t lut = ((size_t)2 * (size_t)W * 4 + 15) & ~size_t(15);
   const size_t fixed = (size_t)g.rpc * (8 + 8 + 8 + 8) + ((((size_t)g.rpc * 2 * g.n * 2) + 15) & ~size_t(15)) +
                        2 * (kBuckets + 2) * 2 + 64;
-  return lut + 2 * swap5_buf_bytes(g, G) + fixed;
+  return lut + kSwap5Stages * swap5_buf_bytes(g, G) + fixed;
 }
 
 
@@ -985,7 +992,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
   unsigned char* cur = s5 + (((size_t)2 * W * 4 + 15) & ~size_t(15));
   const size_t buf_bytes = swap5_buf_bytes(geo, G);
   unsigned char* bufs = cur;
-  cur += 2 * buf_bytes;
+  cur += kSwap5Stages * buf_bytes;
   unsigned long long* smin = reinterpret_cast<unsigned long long*>(cur);  cur += (size_t)RPC * 8;
   const uint16_t** hsrc = reinterpret_cast<const uint16_t**>(cur);       cur += (size_t)RPC * 8;
   const uint16_t** lsrc = reinterpret_cast<const uint16_t**>(cur);       cur += (size_t)RPC * 8;
@@ -1047,7 +1054,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
       base_b += __popc(mb);
     }
   }
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < kSwap5Stages; ++k) {
     const Buf B = buf_at(k);
     for (int i = tid; i < RPC * hrows * RS; i += blockDim.x) B.h[i] = 0;
   }
@@ -1129,14 +1136,19 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
 #pragma unroll
     for (int q = 0; q < kSwapY; ++q) acc[q] = 0.0;
 
-    issue(0, 0);
-    cp_async_commit();
-    int k = 0;
-    for (int64_t t0 = 0; t0 < Tp; t0 += TC, k ^= 1) {
-      if (t0 + TC < Tp) issue(t0 + TC, k ^ 1);
+    // kSwap5Stages-deep cp.async ring: chunks c+1 .. c+S-1 in flight while c is scanned
+#pragma unroll
+    for (int c = 0; c < kSwap5Stages - 1; ++c) {
+      if ((int64_t)c * TC < Tp) issue((int64_t)c * TC, c);
       cp_async_commit();
-      cp_async_wait1();
-      __syncthreads();
+    }
+    int k = 0;
+    for (int64_t t0 = 0; t0 < Tp; t0 += TC, k = (k + 1 == kSwap5Stages) ? 0 : k + 1) {
+      cp_async_wait_n<kSwap5Stages - 2>();  // chunk c has landed (c+1 .. may be in flight)
+      __syncthreads();                      // ... for every thread; and chunk c-1 is scanned by all
+      const int kn = (k + kSwap5Stages - 1) % kSwap5Stages;  // the slot freed by chunk c-1
+      if (t0 + (kSwap5Stages - 1) * TC < Tp) issue(t0 + (kSwap5Stages - 1) * TC, kn);
+      cp_async_commit();
       const Buf B = buf_at(k);
       // pother' and, per side, the clamp point: the largest n whose table
       // value (monotone rows) is <= pother'. Indices below it read the clamp
@@ -1213,7 +1225,6 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
 #pragma unroll
         for (int q = 0; q < kSwapY; ++q) acc[q] = dadd(acc[q], (double)c[q]);
       }
-      __syncthreads();  // buffer k is rewritten by the issue of the chunk after next
     }
     if (live) {
       double mn = acc[0];
