@@ -220,6 +220,10 @@ greedy_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, const d
 // decides; otherwise the window's GPUs are scored exactly (v1's serial chain
 // in t order) and the strict-< / lowest-index rule picks among them.
 constexpr int kG2Threads = 512;
+#ifndef GEM_GREEDY_UNROLL
+#define GEM_GREEDY_UNROLL 4
+#endif
+constexpr int kGreedyUnroll = GEM_GREEDY_UNROLL;
 
 // U[l] = max_t (sum of the n largest counts of step t): one warp per step row
 __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, int64_t T, int E, int n,
@@ -337,7 +341,7 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
       acc[g] = 0.0;
       row_addr[g] = lut_base + 4u * (uint32_t)(g < G ? g : G - 1) * (uint32_t)W;
     }
-#pragma unroll 2
+#pragma unroll kGreedyUnroll
     for (int64_t t = tid; t < T; t += blockDim.x) {
       const uint32_t hv = (uint32_t)hcol[t];
       uint32_t lrow[GM];
