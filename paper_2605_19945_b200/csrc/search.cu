@@ -64,6 +64,7 @@ struct SearchWs {
   float* latT;         // [R][G][Tp] fp32 latencies of the current loads (screened scan)
   uint16_t* loadT;     // [R][G][Tp] current loads (screened scan)
   uint32_t* top3;      // [R][4][Tp] per step: the three largest fp32 latencies (bits) and their GPUs (packed)
+  double* split_acc;   // [R][NP][n][n] step-range-split scans: partial approximate sums of every pair
   int64_t Tp;          // T rounded up to 32 (whole 16-byte pieces for every chunk of the transposed arrays)
   const float* lut32;  // [G][nmax+1] fp32 rounding of the latency table (set by the driver)
   const uint16_t* ht16;  // [L][E][Tp] transposed counts (set by the driver when every count < 65536)
@@ -85,7 +86,7 @@ constexpr int kCandK = GEM_CANDK;
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-static size_t carve(SearchWs* ws, void* base, int64_t R, int64_t T, int G) {
+static size_t carve(SearchWs* ws, void* base, int64_t R, int64_t T, int E, int G) {
   const int64_t NP = (int64_t)G * (G - 1) / 2 > 0 ? (int64_t)G * (G - 1) / 2 : 1;
   size_t off = 0;
   char* b = static_cast<char*>(base);
@@ -114,6 +115,7 @@ static size_t carve(SearchWs* ws, void* base, int64_t R, int64_t T, int G) {
   w.latT = (float*)take((size_t)R * G * w.Tp * 4);
   w.loadT = (uint16_t*)take((size_t)R * G * w.Tp * 2);
   w.top3 = (uint32_t*)take((size_t)R * 4 * w.Tp * 4);
+  w.split_acc = (double*)take((size_t)R * NP * (G > 0 ? (size_t)(E / G) * (E / G) : 1) * 8);
   w.lut32 = nullptr;
   w.ht16 = nullptr;
   w.ht16s = nullptr;
@@ -524,9 +526,9 @@ init_score_kernel(int64_t T, int G, const double* __restrict__ lut, int64_t nmax
 __global__ void __launch_bounds__(kSearchThreads)
 best_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, const double* __restrict__ lut,
                  int64_t nmax, const int32_t* __restrict__ run_layer, const int8_t* __restrict__ assign,
-                 SearchWs ws, const int32_t* __restrict__ filter) {
+                 SearchWs ws, const int32_t* __restrict__ filter, const int32_t* __restrict__ rlist) {
   extern __shared__ unsigned char bsm[];
-  const int64_t r = blockIdx.x;
+  const int64_t r = rlist ? rlist[blockIdx.x] : blockIdx.x;  // rlist: the compacted active runs
   if (!ws.run_active[r] || (filter && !filter[r])) return;
   const int NP = G * (G - 1) / 2;
   // pair index -> (a, b), a < b
@@ -971,7 +973,7 @@ __host__ __device__ inline size_t swap5_smem(int E, int G, int64_t W) {
 template <int GT>
 __global__ void __launch_bounds__(kSwap3Threads, GEM_SCAN_MINB)
 approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int32_t* __restrict__ run_layer,
-                    const int8_t* __restrict__ assign, int32_t n_active, SearchWs ws) {
+                    const int8_t* __restrict__ assign, int32_t n_active, SearchWs ws, int64_t tseg) {
   extern __shared__ __align__(16) unsigned char s5[];
   const int G = GT > 0 ? GT : G_;
   const Swap3Geom geo = swap3_geom(E, G);
@@ -984,7 +986,14 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
   while (p >= G - 1 - a) { p -= G - 1 - a; ++a; }
   const int b = a + 1 + p;
   const int64_t width = nmax + 1;
-  const int64_t Tp = ws.Tp;
+  // step range of this CTA: all of [0, Tp), or (split scans, tseg > 0) the
+  // blockIdx.z-th segment of tseg steps; split CTAs add their partial sums to
+  // ws.split_acc and split_window_kernel finishes the tiles
+  const bool split = tseg > 0;
+  const int64_t Tp = ws.Tp;  // row stride of the transposed arrays
+  const int64_t tb = split ? (int64_t)blockIdx.z * tseg : 0;
+  const int64_t te = split ? imin64(Tp, tb + tseg) : Tp;  // this CTA's steps: [tb, te)
+  if (tb >= te) return;
   constexpr int TC = kSwap5TChunk;
   constexpr int RS = kSwap5RowU16;
   constexpr int V = TC * 2 / 16;  // 16-byte pieces per uint16 row of a chunk
@@ -1143,15 +1152,15 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
     // kSwap5Stages-deep cp.async ring: chunks c+1 .. c+S-1 in flight while c is scanned
 #pragma unroll
     for (int c = 0; c < kSwap5Stages - 1; ++c) {
-      if ((int64_t)c * TC < Tp) issue((int64_t)c * TC, c);
+      if (tb + (int64_t)c * TC < te) issue(tb + (int64_t)c * TC, c);
       cp_async_commit();
     }
     int k = 0;
-    for (int64_t t0 = 0; t0 < Tp; t0 += TC, k = (k + 1 == kSwap5Stages) ? 0 : k + 1) {
+    for (int64_t t0 = tb; t0 < te; t0 += TC, k = (k + 1 == kSwap5Stages) ? 0 : k + 1) {
       cp_async_wait_n<kSwap5Stages - 2>();  // chunk c has landed (c+1 .. may be in flight)
       __syncthreads();                      // ... for every thread; and chunk c-1 is scanned by all
       const int kn = (k + kSwap5Stages - 1) % kSwap5Stages;  // the slot freed by chunk c-1
-      if (t0 + (kSwap5Stages - 1) * TC < Tp) issue(t0 + (kSwap5Stages - 1) * TC, kn);
+      if (t0 + (kSwap5Stages - 1) * TC < te) issue(t0 + (kSwap5Stages - 1) * TC, kn);
       cp_async_commit();
       const Buf B = buf_at(k);
       // pother' and, per side, the clamp point: the largest n whose table
@@ -1230,6 +1239,16 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
         for (int q = 0; q < kSwapY; ++q) acc[q] = dadd(acc[q], (double)c[q]);
       }
     }
+    if (split) {  // partial sums of this step range (fp64 adds in any order: within the screen's bound)
+      if (live) {
+        const int r = ws.run_list[slot0 + s];
+        double* pa = ws.split_acc + (((int64_t)r * NP + blockIdx.x) * n + x) * n;
+#pragma unroll
+        for (int q = 0; q < kSwapY; ++q)
+          if (yg + q * ng < n) atomicAdd(pa + yg + q * ng, acc[q]);
+      }
+      continue;
+    }
     if (live) {
       double mn = acc[0];
 #pragma unroll
@@ -1257,11 +1276,61 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
       }
     }
   }
+  if (split) return;
   __syncthreads();
   if (tid < nruns) {
     const int r = ws.run_list[slot0 + tid];
     ws.loc_min[(int64_t)r * NP + blockIdx.x] = __longlong_as_double((long long)smin[tid]);
   }
+}
+
+// split scans: per (GPU-pair tile, active run) the tile minimum of the summed
+// partial scores and the pairs inside the tile's window (as approx_scan5 does)
+__global__ void split_window_kernel(int E, int G, const int8_t* __restrict__ assign, int32_t n_active,
+                                    SearchWs ws) {
+  __shared__ unsigned long long s_min;
+  __shared__ int16_t s_list[2][2048 / 2];
+  const int slot = blockIdx.y;
+  if (slot >= n_active) return;
+  const int r = ws.run_list[slot];
+  const int NP = G * (G - 1) / 2, n = E / G;
+  int p = blockIdx.x, a = 0;
+  while (p >= G - 1 - a) { p -= G - 1 - a; ++a; }
+  const int b = a + 1 + p;
+  const int64_t tile = (int64_t)r * NP + blockIdx.x;
+  const double* pa = ws.split_acc + tile * n * n;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) s_min = ord_bits(__longlong_as_double(0x7ff0000000000000LL));
+  if (tid < 32) {  // ascending expert lists of GPUs a and b
+    const int8_t* as = assign + (int64_t)r * E;
+    int ba = 0, bb = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      const int g = e < E ? as[e] : -1;
+      const unsigned ma = __ballot_sync(0xffffffffu, g == a), mb = __ballot_sync(0xffffffffu, g == b);
+      const unsigned below = (1u << lane) - 1u;
+      if (g == a) s_list[0][ba + __popc(ma & below)] = (int16_t)e;
+      if (g == b) s_list[1][bb + __popc(mb & below)] = (int16_t)e;
+      ba += __popc(ma);
+      bb += __popc(mb);
+    }
+  }
+  __syncthreads();
+  for (int k = tid; k < n * n; k += blockDim.x) atomicMin(&s_min, ord_bits(pa[k]));
+  __syncthreads();
+  const double mn = __longlong_as_double((long long)s_min);
+  const double lim = mn * kWindow5;
+  for (int k = tid; k < n * n; k += blockDim.x) {
+    const double v = pa[k];
+    if (!(v <= lim)) continue;
+    const int xe = s_list[0][k / n], ye = s_list[1][k % n];
+    const int kk = atomicAdd(&ws.loc_cnt[tile], 1);
+    if (kk < kLocK) {
+      ws.loc_cand[tile * kLocK + kk] = v;
+      ws.loc_flat[tile * kLocK + kk] = xe < ye ? xe * E + ye : ye * E + xe;
+    }
+  }
+  if (tid == 0) ws.loc_min[tile] = mn;
 }
 
 // per active run: the run's window over all GPU-pair tiles -> exact-candidate list
@@ -1542,8 +1611,7 @@ static size_t swap_smem(int E) {
 using namespace gem;
 
 extern "C" size_t gem_search_workspace_bytes(int64_t R, int64_t T, int32_t E, int32_t G) {
-  (void)E;
-  return carve(nullptr, nullptr, R, T, G);
+  return carve(nullptr, nullptr, R, T, E, G);
 }
 
 static int check_search_args(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G, const double* lut,
@@ -1559,13 +1627,15 @@ static int check_search_args(const int32_t* hist, int64_t L, int64_t T, int32_t 
   return GEM_OK;
 }
 
+// n_listed > 0: only the n_listed runs of ws.run_list (the active ones) are candidates
 static int launch_exact_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, const double* lut, int64_t nmax,
                              int64_t R, const int32_t* run_layer, const int8_t* assign, const SearchWs& ws,
-                             const int32_t* filter, cudaStream_t st) {
+                             const int32_t* filter, cudaStream_t st, int64_t n_listed = 0) {
   const size_t smem = swap_smem(E);
   GEM_CHECK_CUDA(cudaFuncSetAttribute(best_swap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)R, (unsigned)(G * (G - 1) / 2));
-  best_swap_kernel<<<grid, kSearchThreads, smem, st>>>(hist, T, E, G, lut, nmax, run_layer, assign, ws, filter);
+  dim3 grid((unsigned)(n_listed > 0 ? n_listed : R), (unsigned)(G * (G - 1) / 2));
+  best_swap_kernel<<<grid, kSearchThreads, smem, st>>>(hist, T, E, G, lut, nmax, run_layer, assign, ws, filter,
+                                                       n_listed > 0 ? ws.run_list : nullptr);
   GEM_CHECK_LAUNCH("best_swap_kernel");
   reduce_pairs_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(R, G, E, ws, filter);
   GEM_CHECK_LAUNCH("reduce_pairs_kernel");
@@ -1600,10 +1670,31 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
         (int32_t)n_active, ws.Tp, G, ws);
     GEM_CHECK_LAUNCH("top3_kernel");
     const int clamp = ws.lut_monotone && !std::getenv("GEM_SCAN_NOCLAMP");
+    // few active runs (the late refinement rounds): split every run-scan's
+    // steps over several CTAs so the grid still fills two CTAs per SM
+    const int64_t ctas = (int64_t)grid.x * grid.y;
+    int64_t tseg = 0;
+    const int n = E / G;
+    if (ctas < 2 * (int64_t)num_sms() && E / G * (E / G) <= 2048 && !std::getenv("GEM_SCAN_NOSPLIT")) {
+      const int64_t want = (2 * (int64_t)num_sms() + ctas - 1) / ctas;
+      const int64_t minseg = 16 * (int64_t)kSwap5TChunk;  // >= 16 chunks per segment
+      const int64_t nseg = imin64(want, ws.Tp / minseg);
+      if (nseg > 1) tseg = ((ws.Tp + nseg - 1) / nseg + kSwap5TChunk - 1) / kSwap5TChunk * kSwap5TChunk;
+    }
+    dim3 g5 = grid;
+    if (tseg > 0) {
+      g5.z = (unsigned)((ws.Tp + tseg - 1) / tseg);
+      GEM_CHECK_CUDA(cudaMemsetAsync(ws.split_acc, 0, (size_t)R * NP * n * n * 8, st));
+    }
     auto go5 = [&](auto kern) -> int {
       GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
-      kern<<<grid, kSwap3Threads, smem5, st>>>(E, G, nmax, W5, clamp, run_layer, assign, (int32_t)n_active, ws);
+      kern<<<g5, kSwap3Threads, smem5, st>>>(E, G, nmax, W5, clamp, run_layer, assign, (int32_t)n_active, ws, tseg);
       GEM_CHECK_LAUNCH("approx_scan5_kernel");
+      if (tseg > 0) {
+        split_window_kernel<<<dim3((unsigned)NP, (unsigned)n_active), 256, 0, st>>>(E, G, assign, (int32_t)n_active,
+                                                                                   ws);
+        GEM_CHECK_LAUNCH("split_window_kernel");
+      }
       return GEM_OK;
     };
     const int rc5 = G == 8 ? go5(approx_scan5_kernel<8>) : (G == 4 ? go5(approx_scan5_kernel<4>)
@@ -1623,8 +1714,8 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   GEM_CHECK_LAUNCH("exact_pairs_kernel");
   select_pairs_kernel<<<(unsigned)((n_active + 127) / 128), 128, 0, st>>>((int32_t)n_active, E, ws);
   GEM_CHECK_LAUNCH("select_pairs_kernel");
-  // runs whose window overflowed: the exact scan (CTAs of other runs exit at once)
-  return launch_exact_scan(hist, T, E, G, lut, nmax, R, run_layer, assign, ws, ws.need_exact, st);
+  // runs whose window overflowed: the exact scan (CTAs of other active runs exit at once)
+  return launch_exact_scan(hist, T, E, G, lut, nmax, R, run_layer, assign, ws, ws.need_exact, st, n_active);
 }
 
 static int launch_greedy(const int32_t* hist, int64_t T, int32_t E, int32_t G, const double* lut, int64_t nmax,
@@ -1754,7 +1845,7 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
               "gem_search_runs: bad arguments");
   cudaStream_t st = as_stream(stream);
   SearchWs ws;
-  carve(&ws, workspace, R, T, G);
+  carve(&ws, workspace, R, T, E, G);
   Screen screen;
   if ((rc = prepare_screen(hist, L, T, E, G, lut, nmax, screen, ws, st))) return rc;
   GEM_CHECK_CUDA(cudaMemsetAsync(ws.counters, 0, 16, st));
@@ -1847,7 +1938,7 @@ extern "C" int gem_best_swap_runs(const int32_t* hist, int64_t L, int64_t T, int
   GEM_REQUIRE(assign && found && best_i && best_j && best_cand, "gem_best_swap_runs: null output");
   cudaStream_t st = as_stream(stream);
   SearchWs ws;
-  carve(&ws, workspace, R, T, G);
+  carve(&ws, workspace, R, T, E, G);
   Screen screen;
   if ((rc = prepare_screen(hist, L, T, E, G, lut, nmax, screen, ws, st))) return rc;
   int64_t bx = (T * G + 255) / 256;
