@@ -21,7 +21,7 @@ import torch
 from . import _device, _lib
 from ._device import ptr, stream
 from ._util import serial_sum
-from .baselines import eplb_assignment, linear_assignment
+from .baselines import eplb_assignment, eplb_assignments, linear_assignment
 from .errors import ValidationError
 from .mapping import ExpertMapping, _check_dimensions
 from .profiles import VariabilityProfile
@@ -182,8 +182,7 @@ def all_layer_jobs(mean_util: np.ndarray, num_gpus: int, config: SearchConfig) -
     if nb:
         order[:, K:] = np.arange(E, dtype=np.int16)
         assign[:, K] = linear_assignment(E, num_gpus)
-        for l in range(L):
-            assign[l, K + 1] = eplb_assignment(mu[l], num_gpus)
+        assign[:, K + 1] = eplb_assignments(mu, num_gpus)
         prov += ["baseline:linear", "baseline:eplb"]
     greedy = np.zeros(per, dtype=np.uint8)
     greedy[:K] = 1
@@ -207,9 +206,13 @@ class RunResults:
     trajectory: np.ndarray    # [R, cap+1] fp64
 
     def record(self, r: int, provenance: str) -> RestartRecord:
-        s = int(self.swaps[r])
-        traj = tuple(float(x) for x in self.trajectory[r, : s + 1])
-        return RestartRecord(provenance, traj[0], float(self.final_score[r]), s, traj)
+        if "_lists" not in self.__dict__:  # python floats/ints of every run, converted once
+            width = int(self.swaps.max(initial=0)) + 1
+            self._lists = (self.trajectory[:, :width].tolist(), self.final_score.tolist(), self.swaps.tolist())
+        trajs, finals, swaps = self._lists
+        s = swaps[r]
+        traj = tuple(trajs[r][: s + 1])
+        return RestartRecord(provenance, traj[0], finals[r], s, traj)
 
 
 def run_search_device(hist: torch.Tensor, nmax: int, profile: VariabilityProfile, batch: RunBatch,

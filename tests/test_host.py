@@ -267,3 +267,19 @@ def test_all_layer_jobs_equals_per_layer_jobs():
         assert np.array_equal(got.needs_greedy, want.needs_greedy)
         assert np.array_equal(got.run_layer, want.run_layer)
         assert got.provenance == want.provenance
+
+
+def test_eplb_assignments_equals_per_row():
+    """The batched LPT (all layers at once) makes the per-layer decisions of
+    eplb_assignment (reference baselines.py:24-53), ties included."""
+    from paper_2605_19945_b200.baselines import eplb_assignment, eplb_assignments
+
+    rng = np.random.default_rng(5)
+    mu = rng.random((12, 32))
+    mu[3] = 1.0 / 32                  # all tied
+    mu[5, rng.integers(0, 32, 10)] = 0.0  # ties at zero
+    mu[7] = np.round(mu[7] * 4) / 4   # few distinct values, equal GPU totals
+    for G in (1, 2, 4, 8, 32):
+        got = eplb_assignments(mu, G)
+        want = np.stack([eplb_assignment(mu[l], G) for l in range(mu.shape[0])])
+        assert np.array_equal(got, want)
