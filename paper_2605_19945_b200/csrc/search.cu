@@ -673,8 +673,14 @@ best_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, cons
 // (transposed uint16 histogram, one contiguous 64-byte run per expert), the
 // run's l_a / l_b rows and the fp32 latency rows of every GPU (transposed
 // per-run state kept current across swaps), then derives pother'.
-constexpr int kSwapY = 4;
-constexpr int kSwap3Threads = 256;
+#ifndef GEM_SWAP_Y
+#define GEM_SWAP_Y 4
+#endif
+constexpr int kSwapY = GEM_SWAP_Y;
+#ifndef GEM_SCAN_THREADS
+#define GEM_SCAN_THREADS 256
+#endif
+constexpr int kSwap3Threads = GEM_SCAN_THREADS;
 constexpr int kSwap3TChunk = 32;
 
 struct Swap3Geom {
