@@ -222,6 +222,8 @@ greedy_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, const d
 // decides; otherwise the window's GPUs are scored exactly (v1's serial chain
 // in t order) and the strict-< / lowest-index rule picks among them.
 constexpr int kG2Threads = 512;
+// 32-GPU slots: 256 threads, so the per-thread GPU arrays get 255 registers
+__host__ __device__ constexpr int g2_threads(int GM) { return GM >= 32 ? 256 : kG2Threads; }
 #ifndef GEM_GREEDY_UNROLL
 #define GEM_GREEDY_UNROLL 4
 #endif
@@ -291,18 +293,20 @@ __global__ void hist_t16_kernel(const int32_t* __restrict__ hist, int64_t T, int
 }
 
 // FULL: G == GM (no padded GPU columns: the per-GPU guards vanish at compile time)
-template <int GM, bool FULL>
-__global__ void __launch_bounds__(kG2Threads, 1)
+// SL: the fp32 table window [G][W] sits in shared memory; otherwise (G = 32
+// with a wide window) the gathers read ws.lut32 through L1/L2
+template <int GM, bool FULL, bool SL>
+__global__ void __launch_bounds__(g2_threads(GM), 1)
 greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
                const double* __restrict__ lut, int64_t nmax, int W, const int32_t* __restrict__ run_layer,
                const uint8_t* __restrict__ needs_greedy, const int16_t* __restrict__ order,
                int8_t* __restrict__ assign, uint16_t* __restrict__ loads16, SearchWs ws) {
   const int G = FULL ? GM : G_;
   extern __shared__ __align__(16) unsigned char g2s[];
-  float* s_lut = reinterpret_cast<float*>(g2s);                                        // [G][W]
+  float* s_lut = reinterpret_cast<float*>(g2s);                                        // [G][W] (SL)
   const uint32_t lut_base = (uint32_t)__cvta_generic_to_shared(s_lut);
-  double* red = reinterpret_cast<double*>(g2s + (((size_t)G * W * 4 + 15) & ~size_t(15)));  // [warps][GM]
-  double* buf = red + (kG2Threads / 32) * GM;                                           // [kGreedyTChunk]
+  double* red = reinterpret_cast<double*>(g2s + (SL ? (((size_t)G * W * 4 + 15) & ~size_t(15)) : 0));  // [warps][GM]
+  double* buf = red + (g2_threads(GM) / 32) * GM;                                          // [kGreedyTChunk]
   __shared__ int counts[GM];
   __shared__ int s_best, s_ncand;
   __shared__ int s_cand[GM];
@@ -314,10 +318,16 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
   const int32_t* h = hist + layer * T * E;
   const uint16_t* hl = ws.ht16 + layer * E * ws.Tp;
   uint16_t* ld = loads16 + r * T * GM;  // row stride GM (padded), unused GPUs stay 0
-  for (int i = tid; i < G * W; i += blockDim.x) {
-    const int g = i / W, nn = i - g * W;
-    s_lut[i] = ws.lut32[(int64_t)g * width + nn];
-  }
+  if (SL)
+    for (int i = tid; i < G * W; i += blockDim.x) {
+      const int g = i / W, nn = i - g * W;
+      s_lut[i] = ws.lut32[(int64_t)g * width + nn];
+    }
+  // table value of GPU slot g (rows of padded slots g >= G read row G - 1)
+  auto tab = [&](const uint32_t* row_addr, int g, uint32_t nn) -> float {
+    if (SL) return lds_f32(row_addr[g] + 4u * nn);
+    return __ldg(ws.lut32 + (int64_t)(g < G ? g : G - 1) * width + nn);
+  };
   if (tid < GM) counts[tid] = 0;
   for (int64_t i = tid; i < T * GM; i += blockDim.x) ld[i] = 0;
   const int cap = E / G;
@@ -360,7 +370,7 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
       float cur[GM], pre[GM + 1], suf[GM + 1];
 #pragma unroll
       for (int g = 0; g < GM; ++g) {
-        const float v = lds_f32(row_addr[g] + 4u * lrow[g]);
+        const float v = tab(row_addr, g, lrow[g]);
         cur[g] = g < G ? v : __int_as_float(0xff800000);
       }
       pre[0] = __int_as_float(0xff800000);
@@ -371,7 +381,7 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
       for (int g = GM - 1; g >= 0; --g) suf[g] = fmaxf(suf[g + 1], cur[g]);
 #pragma unroll
       for (int g = 0; g < GM; ++g) {
-        const float cl = lds_f32(row_addr[g] + 4u * (lrow[g] + hv));
+        const float cl = tab(row_addr, g, lrow[g] + hv);
         acc[g] += (double)fmaxf(fmaxf(pre[g], suf[g + 1]), cl);  // g >= G: ignored by the selection
       }
     }
@@ -1659,7 +1669,12 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   int dev = 0, optin = 0;
   GEM_CHECK_CUDA(cudaGetDevice(&dev));
   GEM_CHECK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  if (ws.lut32 == nullptr || ws.ht16 == nullptr || smem3 > (size_t)optin) {
+  // v5 needs only the two tables of its GPU pair in shared memory (v4 stages
+  // every GPU's latencies: too large at G = 32)
+  const int W5 = ws.win > 0 ? ws.win : (int)(nmax + 1);
+  const size_t smem5 = swap5_smem(E, G, W5);
+  const bool v5 = ws.ht16s != nullptr && ws.first != nullptr && smem5 <= (size_t)optin && !std::getenv("GEM_SCAN_V4");
+  if (ws.lut32 == nullptr || ws.ht16 == nullptr || (!v5 && smem3 > (size_t)optin)) {
     return launch_exact_scan(hist, T, E, G, lut, nmax, R, run_layer, assign, ws, nullptr, st);
   }
   GEM_CHECK_CUDA(cudaMemsetAsync(ws.counters + 3, 0, 4, st));
@@ -1668,10 +1683,8 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   GEM_CHECK_CUDA(cudaMemsetAsync(ws.loc_cnt, 0, (size_t)R * NP * 4, st));
   const Swap3Geom g = swap3_geom(E, G);
   dim3 grid((unsigned)NP, (unsigned)((n_active + g.rpc - 1) / g.rpc));
-  const int W5 = ws.win > 0 ? ws.win : (int)(nmax + 1);
-  const size_t smem5 = swap5_smem(E, G, W5);
   double window = kWindow;
-  if (ws.ht16s != nullptr && ws.first != nullptr && smem5 <= (size_t)optin && !std::getenv("GEM_SCAN_V4")) {
+  if (v5) {
     top3_kernel<<<(unsigned)imin64((n_active * ws.Tp + 255) / 256, 16 * num_sms()), 256, 0, st>>>(
         (int32_t)n_active, ws.Tp, G, ws);
     GEM_CHECK_LAUNCH("top3_kernel");
@@ -1733,23 +1746,32 @@ static int launch_greedy(const int32_t* hist, int64_t T, int32_t E, int32_t G, c
   if (ws.ht16 && G <= 32) {
     const int W = (int)imin64(U, nmax) + 1;
     const int GM = G <= 8 ? 8 : (G <= 16 ? 16 : 32);
-    const size_t smem = (((size_t)G * W * 4 + 15) & ~size_t(15)) + (size_t)(kG2Threads / 32) * GM * 8 +
-                        (size_t)GM * kGreedyTChunk * 8;
+    const size_t rest = (size_t)(g2_threads(GM) / 32) * GM * 8 + (size_t)GM * kGreedyTChunk * 8;
+    size_t smem = (((size_t)G * W * 4 + 15) & ~size_t(15)) + rest;
+    const bool sl = smem <= (size_t)optin;  // else the table stays in global memory (L1/L2 gathers)
+    if (!sl) smem = rest;
     if (smem <= (size_t)optin) {
       uint16_t* l16 = nullptr;  // uint16 per-run loads, stream-ordered scratch
       GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&l16), (size_t)R * T * GM * 2, st));
       auto go = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        kern<<<(unsigned)R, kG2Threads, smem, st>>>(hist, T, E, G, lut, nmax, W, run_layer, needs_greedy, order,
+        kern<<<(unsigned)R, g2_threads(GM), smem, st>>>(hist, T, E, G, lut, nmax, W, run_layer, needs_greedy, order,
                                                     assign, l16, ws);
         return cudaGetLastError();
       };
       const cudaError_t ek =
-          GM == G ? (GM == 8 ? go(greedy2_kernel<8, true>) : (GM == 16 ? go(greedy2_kernel<16, true>)
-                                                                        : go(greedy2_kernel<32, true>)))
-                  : (GM == 8 ? go(greedy2_kernel<8, false>) : (GM == 16 ? go(greedy2_kernel<16, false>)
-                                                                        : go(greedy2_kernel<32, false>)));
+          sl ? (GM == G ? (GM == 8 ? go(greedy2_kernel<8, true, true>)
+                                   : (GM == 16 ? go(greedy2_kernel<16, true, true>) : go(greedy2_kernel<32, true, true>)))
+                        : (GM == 8 ? go(greedy2_kernel<8, false, true>)
+                                   : (GM == 16 ? go(greedy2_kernel<16, false, true>)
+                                               : go(greedy2_kernel<32, false, true>))))
+             : (GM == G ? (GM == 8 ? go(greedy2_kernel<8, true, false>)
+                                   : (GM == 16 ? go(greedy2_kernel<16, true, false>)
+                                               : go(greedy2_kernel<32, true, false>)))
+                        : (GM == 8 ? go(greedy2_kernel<8, false, false>)
+                                   : (GM == 16 ? go(greedy2_kernel<16, false, false>)
+                                               : go(greedy2_kernel<32, false, false>))));
       cudaFreeAsync(l16, st);
       if (ek != cudaSuccess) return fail_cuda(ek, "greedy2_kernel");
       return GEM_OK;

@@ -386,6 +386,20 @@ def test_search_router_like_trace_matches_oracle(oracle):
     assert [r.trajectory for r in res.per_restart] == [tuple(r["trajectory"]) for r in want["records"]]
 
 
+def test_search_deepseek_like_trace_matches_oracle(oracle):
+    """The C5 shape (E = 256, G = 32, router-like counts): the load window is wide
+    enough that the greedy's 32 fp32 table rows stay in global memory (L1/L2
+    gathers) and the scan runs v5 with only its GPU pair's two rows in shared memory."""
+    tok = _generated_counts(1, 48, 256, 8, 1024, seed=5)[0]
+    p = gem.generate_profile(gem.VariabilitySetupSpec(num_gpus=32, setup="moderate", tile_size=64,
+                                                      max_tokens=8192, rng_seed=4))
+    res = gem.search(gem.ExpertTrace(tok), p, gem.SearchConfig(restarts=2, rng_seed=3))
+    want = oracle.search(tok, oracle.Curves.from_profile(p), restarts=2, rng_seed=3)
+    assert res.best_score == want["best_score"]
+    assert res.best_mapping.assignment.tolist() == want["best_assignment"].tolist()
+    assert [r.trajectory for r in res.per_restart] == [tuple(r["trajectory"]) for r in want["records"]]
+
+
 def test_search_exact_ties_follow_reference_rules(oracle):
     """Duplicated expert columns and GPUs with identical curves make many greedy placements
     and swap candidates tie exactly: lowest GPU in greedy, first (i, j) in the scan."""
