@@ -70,6 +70,7 @@ struct SearchWs {
   const uint16_t* ht16;  // [L][E][Tp] transposed counts (set by the driver when every count < 65536)
   const uint16_t* ht16s; // [L][E][Tp] the same counts times 4 (byte offsets into fp32 rows; 4U < 65536)
   int32_t lut_monotone;  // every fp32 table row is nondecreasing (set by the driver)
+  int32_t lut_monotone64;  // every fp64 table row is nondecreasing (set by the driver)
   int32_t win;           // loads never exceed win - 1 (= min(U, nmax)): table window of the screened scan
   const uint16_t* first;  // [G][kBuckets + 2] first n whose value bucket is >= b (clamp-point search hints)
   const float* bscale;    // [G] buckets per unit latency: bucket(v) = min(kBuckets, (int)(v * bscale[g]))
@@ -120,6 +121,7 @@ static size_t carve(SearchWs* ws, void* base, int64_t R, int64_t T, int E, int G
   w.ht16 = nullptr;
   w.ht16s = nullptr;
   w.lut_monotone = 0;
+  w.lut_monotone64 = 0;
   w.win = 0;
   w.first = nullptr;
   w.bscale = nullptr;
@@ -310,6 +312,7 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
   __shared__ int counts[GM];
   __shared__ int s_best, s_ncand;
   __shared__ int s_cand[GM];
+  __shared__ unsigned s_exc;  // GPUs whose candidate latency may reach the others' maximum at some step
   const int64_t r = blockIdx.x;
   if (!needs_greedy[r]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -329,6 +332,7 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
     return __ldg(ws.lut32 + (int64_t)(g < G ? g : G - 1) * width + nn);
   };
   if (tid < GM) counts[tid] = 0;
+  if (tid == 0) s_exc = 0u;
   for (int64_t i = tid; i < T * GM; i += blockDim.x) ld[i] = 0;
   const int cap = E / G;
   __syncthreads();
@@ -348,6 +352,7 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
     // experts to the exact re-score).
     double acc[GM];
     uint32_t row_addr[GM];
+    unsigned exc = 0u;
 #pragma unroll
     for (int g = 0; g < GM; ++g) {
       acc[g] = 0.0;
@@ -382,7 +387,9 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
 #pragma unroll
       for (int g = 0; g < GM; ++g) {
         const float cl = tab(row_addr, g, lrow[g] + hv);
-        acc[g] += (double)fmaxf(fmaxf(pre[g], suf[g + 1]), cl);  // g >= G: ignored by the selection
+        const float pm = fmaxf(pre[g], suf[g + 1]);
+        acc[g] += (double)fmaxf(pm, cl);  // g >= G: ignored by the selection
+        if (hv != 0u && cl >= pm) exc |= 1u << g;  // hv == 0: the term is the step maximum exactly
       }
     }
 #pragma unroll
@@ -392,6 +399,8 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0) red[warp * GM + g] = v;
     }
+    exc = __reduce_or_sync(0xffffffffu, exc);
+    if (lane == 0 && exc) atomicOr(&s_exc, exc);
     __syncthreads();
     if (tid == 0) {
       double mn = __longlong_as_double(0x7ff0000000000000LL);
@@ -402,9 +411,21 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
         if (avail >> g & 1u) mn = fmin(mn, v);
       }
       const double lim = mn * kWindow;
+      // Monotone tables: no placement scores below S_M = the serial sum of the
+      // current step maxima. A GPU scores exactly S_M if at every step either
+      // the expert adds nothing (h = 0: the same table entry) or its fp32
+      // candidate latency is strictly below the fp32 maximum of the others
+      // (then so is the exact one -- rounding is monotone -- and the GPU is
+      // not the step's unique maximum, so the others' maximum is the step's).
+      // The lowest such GPU g* wins unless a window GPU of lower index ties
+      // it; only those need the exact chains.
+      const unsigned nx = ws.lut_monotone64 ? (avail & ~s_exc) : 0u;
+      const int gstar = nx ? __ffs(nx) - 1 : G;
+      s_exc = 0u;
       int nc = 0;
-      for (int g = 0; g < G; ++g)
+      for (int g = 0; g < gstar; ++g)
         if ((avail >> g & 1u) && red[g] <= lim) s_cand[nc++] = g;
+      if (gstar < G) s_cand[nc++] = gstar;
       s_ncand = nc;
       s_best = s_cand[0];
       if (nc > 1) atomicAdd(&ws.counters[2], 1);  // statistics: exact re-scores
@@ -1494,11 +1515,14 @@ __global__ void bucket_first_kernel(const float* __restrict__ lut32, int G, int6
 }
 
 // flag[0] = 1 when some fp32 table row decreases somewhere
-__global__ void lut_monotone_kernel(const float* __restrict__ lut32, int G, int64_t width, int32_t* __restrict__ flag) {
+// flag bit 0: some fp32 row decreases; bit 1: some fp64 row decreases
+__global__ void lut_monotone_kernel(const float* __restrict__ lut32, const double* __restrict__ lut, int G,
+                                    int64_t width, int32_t* __restrict__ flag) {
   const int64_t n = (int64_t)G * width;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = i % width;
-    if (k + 1 < width && !(lut32[i] <= lut32[i + 1])) atomicExch(flag, 1);
+    if (k + 1 < width && !(lut32[i] <= lut32[i + 1])) atomicOr(flag, 1);
+    if (k + 1 < width && !(lut[i] <= lut[i + 1])) atomicOr(flag, 2);
   }
 }
 
@@ -1820,7 +1844,8 @@ static int prepare_screen(const int32_t* hist, int64_t L, int64_t T, int32_t E, 
   int32_t* bound = nullptr;
   GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bound), (size_t)(L + 1) * 4, st));
   GEM_CHECK_CUDA(cudaMemsetAsync(bound, 0, (size_t)(L + 1) * 4, st));
-  lut_monotone_kernel<<<(unsigned)imin64((n + 255) / 256, 4096), 256, 0, st>>>(sc.lut32, G, nmax + 1, bound + L);
+  lut_monotone_kernel<<<(unsigned)imin64((n + 255) / 256, 4096), 256, 0, st>>>(sc.lut32, lut, G, nmax + 1,
+                                                                               bound + L);
   GEM_CHECK_LAUNCH("lut_monotone_kernel");
   const int warps = 8;
   topn_bound_kernel<<<(unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms()), warps * 32,
@@ -1834,7 +1859,8 @@ static int prepare_screen(const int32_t* hist, int64_t L, int64_t T, int32_t E, 
   if (e2 != cudaSuccess) return fail_cuda(e2, "topn bound copy");
   if (e3 != cudaSuccess) return fail_cuda(e3, "topn bound sync");
   for (int64_t l = 0; l < L; ++l) sc.U = imax64(sc.U, ub[l]);
-  ws.lut_monotone = ub[L] == 0;
+  ws.lut_monotone = (ub[L] & 1) == 0;
+  ws.lut_monotone64 = (ub[L] & 2) == 0;
   ws.win = (int32_t)imin64(sc.U, nmax) + 1;
   if (ws.win <= 65535) {  // u16 search hints
     GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.bscale), (size_t)G * 4, st));
