@@ -126,15 +126,18 @@ def test_shard_plan_covers_everything():
 
 
 @pytest.mark.timeout(300)
-def test_two_rank_gloo_pipeline_matches_single_process(tmp_path, oracle):
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_gloo_pipeline_matches_single_process(tmp_path, oracle, world):
+    """world 3 and 4 split the 5 layers and 24 steps unevenly (2/2/1, 2/1/1/1)."""
     out = tmp_path / "rank0.npz"
-    mp.spawn(_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(out)), nprocs=world, join=True)
     got = np.load(out)
     ids, cand = _inputs()
     curves = _curves()
     hist, _ = oracle.topk_hist(ids, B, E)
     # statistics: exact integers, bit-exact floats
-    assert np.array_equal(got["owned"], hist[:3])  # rank 0 owns layers [0, 3)
+    l0, l1 = ShardPlan(world, 0, L, T).layer_range()
+    assert np.array_equal(got["owned"], hist[l0:l1])  # the layers rank 0 owns
     assert np.array_equal(got["colsum"], hist.sum(axis=1))
     assert np.array_equal(got["active"], (hist > 0).sum(axis=1))
     for l in range(L):
