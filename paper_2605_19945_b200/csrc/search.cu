@@ -59,7 +59,8 @@ struct SearchWs {
   int32_t* loc_flat;   // [R][NP][kLocK]
   int32_t* cand_flat;  // [R][kCandK] pairs to evaluate exactly
   int32_t* cand_n;     // [R]
-  int32_t* need_exact; // [R] window overflow -> exact full scan of the run
+  int32_t* need_exact; // [R] kNeedExact: window overflow -> exact full scan of the run;
+                       // kPreAccept / kPreReject: the window alone decides (search only)
   double* cand_exact;  // [R][kCandK]
   float* latT;         // [R][G][Tp] fp32 latencies of the current loads (screened scan)
   uint16_t* loadT;     // [R][G][Tp] current loads (screened scan)
@@ -84,6 +85,7 @@ struct SearchWs {
 #endif
 constexpr int kLocK = GEM_LOCK;
 constexpr int kCandK = GEM_CANDK;
+constexpr int32_t kNeedExact = 1, kPreAccept = 2, kPreReject = 3;
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -560,7 +562,7 @@ best_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, cons
                  SearchWs ws, const int32_t* __restrict__ filter, const int32_t* __restrict__ rlist) {
   extern __shared__ unsigned char bsm[];
   const int64_t r = rlist ? rlist[blockIdx.x] : blockIdx.x;  // rlist: the compacted active runs
-  if (!ws.run_active[r] || (filter && !filter[r])) return;
+  if (!ws.run_active[r] || (filter && filter[r] != kNeedExact)) return;
   const int NP = G * (G - 1) / 2;
   // pair index -> (a, b), a < b
   int p = blockIdx.y, a = 0;
@@ -1370,8 +1372,15 @@ __global__ void split_window_kernel(int E, int G, const int8_t* __restrict__ ass
   if (tid == 0) ws.loc_min[tile] = mn;
 }
 
-// per active run: the run's window over all GPU-pair tiles -> exact-candidate list
-__global__ void window_kernel(int32_t n_active, int G, double window, SearchWs ws) {
+// per active run: the run's window over all GPU-pair tiles -> exact-candidate list.
+// thr >= 0 (the search's convergence threshold; the refinement only needs the
+// winner when it is accepted, search.py:222-227): the acceptance test is
+// monotone in the candidate score, so with bounds lo <= exact min <= hi from
+// the approximate minimum (|cand' - cand| < 2^-18.9 cand) a run whose lo is
+// rejected stops without exact scores, and a run with ONE pair in its window
+// (necessarily the exact winner) whose hi is accepted swaps without one (the
+// apply kernel's full re-score is the exact candidate, search.py:236).
+__global__ void window_kernel(int32_t n_active, int G, double window, double thr, SearchWs ws) {
   const int NP = G * (G - 1) / 2;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_active; i += gridDim.x * blockDim.x) {
     const int r = ws.run_list[i];
@@ -1392,7 +1401,14 @@ __global__ void window_kernel(int32_t n_active, int G, double window, SearchWs w
     }
     if (cnt > kCandK) overflow = 1;
     ws.cand_n[r] = overflow ? 0 : cnt;
-    ws.need_exact[r] = overflow;
+    int32_t mode = overflow ? kNeedExact : 0;
+    if (thr >= 0.0) {
+      const double s = ws.run_score[r];
+      const double lo = gmin * (1.0 - 0x1p-17), hi = gmin * (1.0 + 0x1p-17);
+      if (!(lo < s) || __dsub_rn(1.0, __ddiv_rn(lo, s)) < thr) mode = kPreReject;
+      else if (!overflow && cnt == 1 && hi < s && !(__dsub_rn(1.0, __ddiv_rn(hi, s)) < thr)) mode = kPreAccept;
+    }
+    ws.need_exact[r] = mode;
   }
 }
 
@@ -1450,7 +1466,16 @@ __global__ void exact_pairs_kernel(const int32_t* __restrict__ hist, int64_t T, 
 __global__ void select_pairs_kernel(int32_t n_active, int E, SearchWs ws) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_active; s += gridDim.x * blockDim.x) {
     const int r = ws.run_list[s];
-    if (ws.need_exact[r]) continue;
+    const int32_t mode = ws.need_exact[r];
+    if (mode == kNeedExact) continue;
+    if (mode == kPreAccept || mode == kPreReject) {
+      const int f = ws.cand_flat[(int64_t)r * kCandK];
+      ws.run_found[r] = mode == kPreAccept;
+      ws.run_i[r] = mode == kPreAccept ? f / E : -1;
+      ws.run_j[r] = mode == kPreAccept ? f % E : -1;
+      ws.run_cand[r] = __longlong_as_double(0x7ff8000000000000LL);  // exact value: the apply's re-score
+      continue;
+    }
     double bc = __longlong_as_double(0x7ff0000000000000LL);
     int bf = 0x7fffffff;
     for (int k = 0; k < ws.cand_n[r]; ++k) {
@@ -1566,7 +1591,7 @@ __global__ void compact_runs_kernel(int64_t R, SearchWs ws) {
 __global__ void reduce_pairs_kernel(int64_t R, int G, int E, SearchWs ws, const int32_t* __restrict__ filter) {
   const int NP = G * (G - 1) / 2;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
-    if (!ws.run_active[r] || (filter && !filter[r])) continue;
+    if (!ws.run_active[r] || (filter && filter[r] != kNeedExact)) continue;
     double bc = __longlong_as_double(0x7ff0000000000000LL);
     int bf = 0x7fffffff;
     for (int p = 0; p < NP; ++p) {
@@ -1597,6 +1622,7 @@ apply_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, con
     int go = ws.run_found[r] && (cand < score);
     // convergence is judged on the best candidate before applying it (search.py:224-227)
     if (go && __dsub_rn(1.0, __ddiv_rn(cand, score)) < threshold) go = 0;
+    if (ws.need_exact[r] == kPreAccept) go = 1;  // accepted by the window bound (window_kernel)
     s_go = go;
     if (!go) ws.run_active[r] = 0;
   }
@@ -1626,7 +1652,7 @@ apply_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, con
   if (threadIdx.x == 0) {
     assign[r * E + i] = (int8_t)b;
     assign[r * E + j] = (int8_t)a;
-    if (s != ws.run_cand[r]) atomicExch(&ws.counters[1], 1);  // search.py:236 assert
+    if (ws.need_exact[r] != kPreAccept && s != ws.run_cand[r]) atomicExch(&ws.counters[1], 1);  // search.py:236
     ws.run_score[r] = s;
     const int n = swaps[r] + 1;
     swaps[r] = n;
@@ -1684,9 +1710,11 @@ static int launch_exact_scan(const int32_t* hist, int64_t T, int32_t E, int32_t 
 
 // One best-swap scan over the active runs: screened (v3) when the two fp32
 // table rows fit shared memory, else the exact v1 scan for every active run.
+// thr >= 0: the search's convergence threshold (window-bound accept / reject,
+// see window_kernel); < 0: every active run gets its exact best pair
 static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, const double* lut, int64_t nmax,
                        int64_t R, int64_t n_active, const int32_t* run_layer, const int8_t* assign,
-                       const SearchWs& ws, cudaStream_t st) {
+                       const SearchWs& ws, cudaStream_t st, double thr = -1.0) {
   const int NP = G * (G - 1) / 2;
   if (NP == 0 || n_active <= 0) return GEM_OK;
   const size_t smem3 = swap3_smem(E, G, nmax);
@@ -1749,7 +1777,7 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
     approx_scan_kernel<<<grid, kSwap3Threads, smem3, st>>>(T, E, G, nmax, run_layer, assign, (int32_t)n_active, ws);
     GEM_CHECK_LAUNCH("approx_scan_kernel");
   }
-  window_kernel<<<(unsigned)((n_active + 127) / 128), 128, 0, st>>>((int32_t)n_active, G, window, ws);
+  window_kernel<<<(unsigned)((n_active + 127) / 128), 128, 0, st>>>((int32_t)n_active, G, window, thr, ws);
   GEM_CHECK_LAUNCH("window_kernel");
   const int64_t warps = n_active * kCandK;
   exact_pairs_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(hist, T, E, G, lut, nmax, run_layer,
@@ -1903,6 +1931,7 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
   Screen screen;
   if ((rc = prepare_screen(hist, L, T, E, G, lut, nmax, screen, ws, st))) return rc;
   GEM_CHECK_CUDA(cudaMemsetAsync(ws.counters, 0, 16, st));
+  GEM_CHECK_CUDA(cudaMemsetAsync(ws.need_exact, 0, (size_t)R * 4, st));  // the apply reads the window's verdict
   cudaEvent_t g0 = nullptr, g1 = nullptr;
   if (std::getenv("GEM_SEARCH_TRACE")) {
     GEM_CHECK_CUDA(cudaEventCreate(&g0));
@@ -1945,7 +1974,7 @@ extern "C" int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_
   int64_t n_active = R;  // every run is active before its first scan
   for (int64_t it = 0; it < swap_cap; ++it) {
     if (trace) GEM_CHECK_CUDA(cudaEventRecord(ev[0], st));
-    rc = launch_scan(hist, T, E, G, lut, nmax, R, n_active, run_layer, assign, ws, st);
+    rc = launch_scan(hist, T, E, G, lut, nmax, R, n_active, run_layer, assign, ws, st, threshold);
     if (rc) return rc;
     if (trace) GEM_CHECK_CUDA(cudaEventRecord(ev[1], st));
     if (G < 2) break;  // no cross-GPU pair exists: found == false for every run

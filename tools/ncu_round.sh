@@ -1,13 +1,19 @@
 #!/usr/bin/env bash
-# One ncu --set full capture per hot kernel (one launch each) + the bench launch list.
+# One ncu --set full capture per hot kernel (one launch each) + the bench launch list,
+# summarised on the box (tools/ncu_summary.py) so only small files come back.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out/ncu
+R=/tmp/ncu_reps; mkdir -p $R
 N="ncu --set full --clock-control none --import-source on -c 1"
-$N -k regex:topk_hist -o gpurun_out/ncu/k1 python tools/kbench.py hist --reps 1 --warm 0 > /dev/null 2>&1
-$N -k regex:gram_tc -o gpurun_out/ncu/k2 python tools/kbench.py gram --reps 1 --warm 0 > /dev/null 2>&1
-$N -k regex:maxkey -o gpurun_out/ncu/k5 python tools/kbench.py score --cands 10000 --reps 1 --warm 0 > /dev/null 2>&1
-$N -k regex:approx_scan5 -o gpurun_out/ncu/k6 python tools/kbench.py swap --runs 592 --reps 1 --warm 0 > /dev/null 2>&1
-$N -k regex:greedy2 -o gpurun_out/ncu/k7 python bench.py --steps 1 --warmup 3 --no-candidates --no-e2e --no-cpu > /dev/null 2>&1
+$N -k regex:topk_hist -o $R/k1 python tools/kbench.py hist --reps 1 --warm 0 > /dev/null 2>&1
+$N -k regex:gram_tc -o $R/k2 python tools/kbench.py gram --reps 1 --warm 0 > /dev/null 2>&1
+$N -k regex:maxkey -o $R/k5 python tools/kbench.py score --cands 10000 --reps 1 --warm 0 > /dev/null 2>&1
+$N -k regex:approx_scan5 -o $R/k6 python tools/kbench.py swap --runs 592 --reps 1 --warm 0 > /dev/null 2>&1
+$N -k regex:greedy2 -o $R/k7 python bench.py --steps 1 --warmup 3 --no-candidates --no-e2e --no-cpu > /dev/null 2>&1
+for k in k1 k2 k5 k6 k7; do
+  [ -f $R/$k.ncu-rep ] && python tools/ncu_summary.py $R/$k.ncu-rep > gpurun_out/ncu/$k.json
+  [ -f $R/$k.ncu-rep ] && ncu -i $R/$k.ncu-rep --page source --csv > gpurun_out/ncu/${k}_source.csv 2>/dev/null
+done
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 ls -la gpurun_out/ncu
