@@ -516,23 +516,45 @@ __global__ void init_loads_kernel(const int32_t* __restrict__ hist, int64_t T, i
 }
 
 // full score of a run from its loads: serial over t of max_g lat (block-level)
+// Serial score of one run (sum over t in order of max_g lat). Thread 0 extends
+// the chain over chunk c while warps 1.. fill chunk c+1 (double buffer), so
+// the chain -- the latency floor -- is not serialised with the table gathers.
+constexpr int kScoreChunk = 1024;  // steps per block_score buffer (several gathers in flight per producer)
 __device__ double block_score(const int32_t* __restrict__ ld, int64_t T, int G, const double* __restrict__ lut,
-                              int64_t width, double* buf /*[kGreedyTChunk]*/) {
-  double sum = 0.0;
-  for (int64_t t0 = 0; t0 < T; t0 += kGreedyTChunk) {
-    const int tn = (int)imin64(kGreedyTChunk, T - t0);
-    for (int tt = threadIdx.x; tt < tn; tt += blockDim.x) {
+                              int64_t width, double* buf /*[2][kScoreChunk]*/) {
+  const int nw = blockDim.x >> 5;
+  const int ptid = nw > 1 ? (int)threadIdx.x - 32 : (int)threadIdx.x;  // producer index (warps 1..)
+  const int np = nw > 1 ? (int)blockDim.x - 32 : (int)blockDim.x;
+  auto fill = [&](int64_t t0, double* b) {
+    const int tn = (int)imin64(kScoreChunk, T - t0);
+    for (int tt = ptid; tt < tn; tt += np) {
       const int32_t* lrow = ld + (t0 + tt) * G;
       double m = lut_at(lut, width, 0, lrow[0]);
       for (int g = 1; g < G; ++g) {
         const double v = lut_at(lut, width, g, lrow[g]);
         m = v > m ? v : m;
       }
-      buf[tt] = m;
+      b[tt] = m;
     }
-    __syncthreads();
-    if (threadIdx.x == 0)
-      for (int tt = 0; tt < tn; ++tt) sum = dadd(sum, buf[tt]);
+  };
+  double sum = 0.0;
+  if (ptid >= 0) fill(0, buf);
+  __syncthreads();
+  int k = 0;
+  for (int64_t t0 = 0; t0 < T; t0 += kScoreChunk, k ^= 1) {
+    const int tn = (int)imin64(kScoreChunk, T - t0);
+    if (nw == 1) {
+      if (threadIdx.x == 0)
+        for (int tt = 0; tt < tn; ++tt) sum = dadd(sum, buf[k * kScoreChunk + tt]);
+      __syncthreads();
+      if (t0 + kScoreChunk < T) fill(t0 + kScoreChunk, buf + (k ^ 1) * kScoreChunk);
+    } else if (threadIdx.x == 0) {
+      const double* b = buf + k * kScoreChunk;
+#pragma unroll 8
+      for (int tt = 0; tt < tn; ++tt) sum = dadd(sum, b[tt]);
+    } else if (ptid >= 0 && t0 + kScoreChunk < T) {
+      fill(t0 + kScoreChunk, buf + (k ^ 1) * kScoreChunk);
+    }
     __syncthreads();
   }
   return sum;  // valid in thread 0
@@ -541,7 +563,7 @@ __device__ double block_score(const int32_t* __restrict__ ld, int64_t T, int G, 
 __global__ void __launch_bounds__(kSearchThreads)
 init_score_kernel(int64_t T, int G, const double* __restrict__ lut, int64_t nmax, SearchWs ws, int64_t traj_cap,
                   double* __restrict__ trajectory, int32_t* __restrict__ swaps) {
-  __shared__ double buf[kGreedyTChunk];
+  __shared__ double buf[2 * kScoreChunk];
   const int64_t r = blockIdx.x;
   const double s = block_score(ws.loads + r * T * G, T, G, lut, nmax + 1, buf);
   if (threadIdx.x == 0) {
@@ -1613,7 +1635,7 @@ apply_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, con
                   int64_t nmax, const int32_t* __restrict__ run_layer, int8_t* __restrict__ assign, SearchWs ws,
                   double threshold, int64_t swap_cap, int64_t traj_cap, double* __restrict__ trajectory,
                   int32_t* __restrict__ swaps) {
-  __shared__ double buf[kGreedyTChunk];
+  __shared__ double buf[2 * kScoreChunk];
   __shared__ int s_go;
   const int64_t r = blockIdx.x;
   if (!ws.run_active[r]) return;
@@ -1635,6 +1657,7 @@ apply_swap_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, con
   const bool screened = ws.ht16 != nullptr;
   const int64_t width = nmax + 1;
   const int64_t Tp = ws.Tp;
+#pragma unroll 4
   for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
     const int32_t d = h[t * E + j] - h[t * E + i];
     const int32_t na = ld[t * G + a] + d, nb = ld[t * G + b] - d;
