@@ -482,7 +482,24 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
       __syncthreads();
     }
     const int bg = s_best;
-    for (int64_t t = tid; t < T; t += blockDim.x) ld[t * GM + bg] = (uint16_t)(ld[t * GM + bg] + hcol[t]);
+    // add the expert's counts to the chosen GPU's loads: all loads of a batch
+    // first, then the stores (the compiler cannot move a load of hcol above a
+    // store to ld, so the naive loop pays one L2 round trip per step)
+    constexpr int kUpd = 8;
+    for (int64_t t0 = tid; t0 < T; t0 += (int64_t)kUpd * blockDim.x) {
+      uint32_t hv[kUpd], lv[kUpd];
+#pragma unroll
+      for (int u = 0; u < kUpd; ++u) {
+        const int64_t t = t0 + (int64_t)u * blockDim.x;
+        hv[u] = t < T ? hcol[t] : 0u;
+        lv[u] = t < T ? ld[t * GM + bg] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kUpd; ++u) {
+        const int64_t t = t0 + (int64_t)u * blockDim.x;
+        if (t < T) ld[t * GM + bg] = (uint16_t)(lv[u] + hv[u]);
+      }
+    }
     if (tid == 0) {
       assign[r * E + e] = (int8_t)bg;
       counts[bg] += 1;
