@@ -355,6 +355,7 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
     double acc[GM];
     uint32_t row_addr[GM];
     unsigned exc = 0u;
+    const uint32_t wlast = (uint32_t)W - 1u;
 #pragma unroll
     for (int g = 0; g < GM; ++g) {
       acc[g] = 0.0;
@@ -388,7 +389,9 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
       for (int g = GM - 1; g >= 0; --g) suf[g] = fmaxf(suf[g + 1], cur[g]);
 #pragma unroll
       for (int g = 0; g < GM; ++g) {
-        const float cl = tab(row_addr, g, lrow[g] + hv);
+        // a GPU with free capacity never exceeds the window (l + h <= U); a
+        // full one (ignored by the selection) is clamped to stay inside it
+        const float cl = tab(row_addr, g, min(lrow[g] + hv, wlast));
         const float pm = fmaxf(pre[g], suf[g + 1]);
         acc[g] += (double)fmaxf(pm, cl);  // g >= G: ignored by the selection
         if (hv != 0u && cl >= pm) exc |= 1u << g;  // hv == 0: the term is the step maximum exactly
