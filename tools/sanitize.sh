@@ -1,9 +1,9 @@
 #!/usr/bin/env bash
-# compute-sanitizer memcheck + racecheck over the GPU parity tests (small shapes).
+# compute-sanitizer memcheck, racecheck, initcheck and synccheck over the GPU parity tests (small shapes).
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out/sanitize
 CS=/usr/local/cuda/bin/compute-sanitizer
-for tool in memcheck racecheck; do
+for tool in ${TOOLS:-memcheck racecheck initcheck synccheck}; do
   timeout 1500 $CS --tool $tool --print-limit 20 --error-exitcode 9 \
     python -m pytest tests/test_gpu_parity.py tests/test_gpu_api.py -x -q -p no:cacheprovider \
     > gpurun_out/sanitize/$tool.log 2>&1
