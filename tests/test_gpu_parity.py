@@ -465,3 +465,43 @@ def test_best_swap_screen_versions_agree(monkeypatch):
     lat = orc.latency_matrix(cv, loads)
     found, i, j, cand = orc.best_swap(t0, a0, loads, lat, cv)
     assert (bool(v5[0][r]), int(v5[1][r]), int(v5[2][r]), float(v5[3][r])) == (bool(found), i, j, cand)
+
+
+# ------------------------------------------------- full size, against the reference build
+
+def test_fullsize_layer_matches_reference_build(oracle):
+    """One whole C4-shaped layer (2^24 tokens x top-8 -> 16,384 steps, E = 128, G = 8)
+    through the reference itself (oracle/_ref, travels with the repo) and the
+    B200 path: statistics, candidate scores and a 2-restart search with every
+    trajectory, bit for bit (tools/fullsize_parity.py runs three layers with
+    the default 30 restarts)."""
+    import os
+
+    ref = oracle.import_reference()
+    if ref is None:
+        pytest.skip("oracle/_ref (the reference build) is not present")
+    spec = ingest.TopkTraceSpec(num_layers=1, num_tokens=1 << 24, top_k=8, num_experts=128, tokens_per_step=1024,
+                                seed=1)
+    st = ingest.trace_statistics(ingest.generate_topk_ids(spec), 1024, 128)
+    h = st.hist.hist[0].cpu().numpy().astype(np.int64)
+    assert h.shape == (16384, 128)
+    rs = ref.compute_stats(ref.ExpertTrace(h))
+    mine = gem.compute_stats(gem.ExpertTrace(h))
+    assert np.array_equal(rs.mean_utilization, mine.mean_utilization)
+    assert np.array_equal(rs.active_fraction, mine.active_fraction)
+    assert np.max(np.abs(rs.correlation - mine.correlation)) <= 1e-12
+    pspec = dict(num_gpus=8, setup="moderate", tile_size=64, max_tokens=8192, rng_seed=1)
+    prof = gem.generate_profile(gem.VariabilitySetupSpec(**pspec))
+    rprof = ref.generate_profile(ref.VariabilitySetupSpec(**pspec))
+    rng = np.random.default_rng(7)
+    for _ in range(4):
+        a = rng.permutation(np.repeat(np.arange(8), 16))
+        assert gem.score_mapping(gem.ExpertTrace(h), prof, gem.ExpertMapping(a, 8)) == ref.score_mapping(
+            ref.ExpertTrace(h), rprof, ref.ExpertMapping(a, 8))
+    cfg = dict(restarts=2, rng_seed=3)
+    want = ref.search(ref.ExpertTrace(h), rprof, ref.SearchConfig(**cfg), threads=len(os.sched_getaffinity(0)))
+    got = gem.search(gem.ExpertTrace(h), prof, gem.SearchConfig(**cfg))
+    assert got.best_score == want.best_score
+    assert got.best_mapping.assignment.tolist() == want.best_mapping.assignment.tolist()
+    assert [(r.provenance, tuple(r.trajectory)) for r in got.per_restart] == [
+        (r.provenance, tuple(r.trajectory)) for r in want.per_restart]
