@@ -275,7 +275,7 @@ def run_ours(args):
     algo_bytes = L * n_local * k * 2 + L * (t1 - t0) * E * 4
     peak, peak_src = peaks()
     achieved = algo_bytes / (k1_ms / 1e3) / 1e9
-    result["roofline"] = {"kernel": "topk_hist_kernel (K1)", "bound": "hbm", "achieved": achieved, "peak": peak,
+    result["roofline"] = {"kernel": "topk_hist_ring_kernel (K1)", "bound": "hbm", "achieved": achieved, "peak": peak,
                           "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic() if args.config == "qwen3-235b" and world == 1 else None,
                           "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": k1_ms,
                           "kernel_share_of_step": k1_ms / ms, "peak_source": peak_src}

@@ -290,6 +290,143 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1 ring variant (int16 ids, wide counters, whole-unit fast path only): one
+// warp per CTA, the unit's 4 KB batches staged by cp.async into a
+// kRingStages-deep shared-memory ring, so kRingStages-1 batches (12 KB) are in
+// flight per warp while it counts -- the register double buffer of the main
+// kernel holds one, and its stream stalls on the counting. Every lane counts
+// exactly the 16-byte pieces it copied itself, so cp.async.wait_group alone
+// orders the ring (no barrier); counting, reduction and flush are the main
+// kernel's.
+#ifndef GEM_HIST_RING
+#define GEM_HIST_RING 5
+#endif
+#ifndef GEM_RING_UNROLL
+#define GEM_RING_UNROLL 4
+#endif
+constexpr int kRingStages = GEM_HIST_RING;
+constexpr int kRingUnroll = GEM_RING_UNROLL;  // 16-byte pieces per lane per batch
+
+__device__ __forceinline__ void ring_cp16(uint32_t saddr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void ring_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void ring_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int MAXR>
+__global__ void __launch_bounds__(32)
+topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int k, int B, int E, int64_t T,
+                      int64_t HT, int32_t* __restrict__ hist, int64_t* __restrict__ colsum,
+                      int32_t* __restrict__ active, int64_t* __restrict__ dropped_out) {
+  extern __shared__ __align__(16) uint4 rsm[];
+  constexpr int BATCH = kRingUnroll * 32;  // uint4 per warp batch (4 KB)
+  const int lane = threadIdx.x;
+  uint4* ring = rsm;                                                  // [kRingStages][kRingUnroll][32]
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(rsm + kRingStages * BATCH);  // [E + 1][32]
+  uint32_t* cnt_lane = cnt + lane;
+  const int rows = E + 1;
+  for (int w = lane; w < rows * 32; w += 32) cnt[w] = 0;
+  __syncwarp();
+  const uint32_t uE = (uint32_t)E, Epair = uE | (uE << 16);
+  const uint32_t ring_base = (uint32_t)__cvta_generic_to_shared(ring) + 16u * (uint32_t)lane;
+  const int64_t units_per_layer = (T + kHistStepsPerUnit - 1) / kHistStepsPerUnit;
+  const int64_t total_units = L * units_per_layer;
+  const int bps = (int)((int64_t)B * k * 2 / (BATCH * 16));  // batches per step (caller checked divisibility)
+
+  for (int64_t unit = blockIdx.x; unit < total_units; unit += gridDim.x) {
+    const int64_t l = unit / units_per_layer;
+    const int64_t t_begin = (unit % units_per_layer) * kHistStepsPerUnit;
+    const int64_t t_end = imin64(t_begin + kHistStepsPerUnit, T);
+    const int64_t nb = (t_end - t_begin) * bps;
+    const uint4* pv = reinterpret_cast<const uint4*>(ids + (l * N + t_begin * B) * k) + lane;
+    auto issue = [&](int64_t b) {
+      const uint32_t dst = ring_base + (uint32_t)((b % kRingStages) * BATCH * 16);
+#pragma unroll
+      for (int u = 0; u < kRingUnroll; ++u) ring_cp16(dst + u * 32 * 16, pv + b * BATCH + u * 32);
+    };
+#pragma unroll
+    for (int sidx = 0; sidx < kRingStages - 1; ++sidx) {
+      if (sidx < nb) issue(sidx);
+      ring_commit();
+    }
+    uint32_t prev[MAXR], act[MAXR];
+#pragma unroll
+    for (int q = 0; q < MAXR; ++q) { prev[q] = 0; act[q] = 0; }
+    int in_step = 0;
+    int64_t t = t_begin;
+    for (int64_t bt = 0; bt < nb; ++bt) {
+      ring_wait<kRingStages - 2>();  // this lane's copies of batch bt have landed
+      // the slot of batch bt-1 (consumed by this lane) takes batch bt+S-1
+      if (bt + kRingStages - 1 < nb) issue(bt + kRingStages - 1);
+      ring_commit();
+      const uint4* cur = ring + (bt % kRingStages) * BATCH + lane;
+#pragma unroll
+      for (int u = 0; u < kRingUnroll; ++u) count_vec_wide<int16_t>(cnt_lane, cur[u * 32], uE, Epair);
+      if (++in_step == bps) {
+        in_step = 0;
+        __syncwarp();
+        int32_t* hrow = hist + (l * HT + t) * E;
+#pragma unroll
+        for (int q = 0; q < MAXR; ++q) {
+          const int row = lane + q * 32;
+          if (row < E) {
+            const uint4* rp = reinterpret_cast<const uint4*>(cnt + row * 32);
+            uint32_t sum = 0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint4 v = rp[(c + lane) & 7];
+              sum += (v.x + v.y) + (v.z + v.w);
+            }
+            const uint32_t h = sum - prev[q];
+            prev[q] = sum;
+            hrow[row] = (int32_t)h;
+            act[q] += (h > 0);
+          }
+        }
+        __syncwarp();
+        ++t;
+      }
+    }
+    ring_wait<0>();
+    uint32_t dropped = cnt[E * 32 + lane];
+    __syncwarp();
+    for (int w = lane; w < rows * 32; w += 32) cnt[w] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < MAXR; ++q) {
+      const int row = lane + q * 32;
+      if (row >= E) continue;
+      if (prev[q]) atomicAdd((unsigned long long*)&colsum[l * E + row], (unsigned long long)prev[q]);
+      if (act[q]) atomicAdd(&active[l * E + row], (int)act[q]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dropped += __shfl_xor_sync(0xffffffffu, dropped, o);
+    if (lane == 0 && dropped) atomicAdd((unsigned long long*)&dropped_out[l], (unsigned long long)dropped);
+  }
+}
+
+template <int MAXR>
+static int launch_hist_ring(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
+                            int32_t* hist, int64_t* colsum, int32_t* active, int64_t* dropped, cudaStream_t st) {
+  const size_t smem = (size_t)kRingStages * kRingUnroll * 32 * 16 + (size_t)(E + 1) * 32 * 4;
+  auto kern = topk_hist_ring_kernel<MAXR>;
+  GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      cudaSharedmemCarveoutMaxShared));
+  int per_sm = 0;
+  GEM_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t units = L * ((T + kHistStepsPerUnit - 1) / kHistStepsPerUnit);
+  int64_t blocks = (int64_t)num_sms() * per_sm;
+  if (blocks > units) blocks = units;
+  kern<<<(unsigned)blocks, 32, smem, st>>>((const int16_t*)ids, L, N, k, B, E, T, HT, hist, colsum, active,
+                                           dropped);
+  GEM_CHECK_LAUNCH("topk_hist_ring_kernel");
+  return GEM_OK;
+}
+
 template <typename IdT, bool WIDE, int MAXR>
 static int launch_hist_t(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
                          int32_t* hist,
@@ -316,6 +453,14 @@ template <typename IdT>
 static int dispatch_hist(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
                          int32_t* hist,
                          int64_t* colsum, int32_t* active, int64_t* dropped, cudaStream_t st) {
+  // ring variant: int16 ids, wide counters, every unit one whole-batch block
+  // (steps of whole 4 KB batches, N a multiple of B, 16-byte aligned ids)
+  const int64_t step_bytes = (int64_t)B * k * (int64_t)sizeof(IdT);
+  if (sizeof(IdT) == 2 && E <= 128 && N % B == 0 && step_bytes % (kRingUnroll * 32 * 16) == 0 &&
+      (reinterpret_cast<uintptr_t>(ids) & 15) == 0 && !std::getenv("GEM_HIST_NORING")) {
+    if (E <= 64) return launch_hist_ring<2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+    return launch_hist_ring<4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+  }
   if (E <= 64) return launch_hist_t<IdT, true, 2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
   if (E <= 128) return launch_hist_t<IdT, true, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
   if (E <= kWideMaxE) return launch_hist_t<IdT, true, 5>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);

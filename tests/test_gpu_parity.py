@@ -52,6 +52,22 @@ def test_topk_hist_random_ids(oracle, dtype, shape):
     assert np.array_equal(h.active.cpu().numpy(), (want > 0).sum(axis=1))
 
 
+@pytest.mark.parametrize("shape", [(2, 64 * 1024, 8, 1024, 128), (1, 37 * 512, 8, 512, 100), (3, 33 * 256, 4, 256, 64),
+                                   (1, 40 * 1024, 8, 1024, 8)])
+def test_topk_hist_ring_path(oracle, shape):
+    """The cp.async-ring K1 (int16, E <= 128, whole 2 KB batches per step, N a
+    multiple of B): full and partial 32-step units, odd E, out-of-range ids."""
+    L, N, k, B, E = shape
+    rng = np.random.default_rng(sum(shape))
+    ids = rng.integers(-3, E + 3, (L, N, k)).astype(np.int16)
+    h = ingest.ids_to_histograms(torch.from_numpy(ids).cuda(), B, E, check_dropped=False)
+    want, dropped = oracle.topk_hist(ids, B, E)
+    assert np.array_equal(h.hist.cpu().numpy(), want)
+    assert np.array_equal(h.dropped.cpu().numpy(), dropped)
+    assert np.array_equal(h.colsum.cpu().numpy(), want.sum(axis=1))
+    assert np.array_equal(h.active.cpu().numpy(), (want > 0).sum(axis=1))
+
+
 def test_topk_hist_unaligned_view(oracle):
     rng = np.random.default_rng(9)
     base = rng.integers(0, 32, (1, 4097, 3)).astype(np.int16)
