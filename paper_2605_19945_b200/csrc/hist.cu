@@ -239,7 +239,8 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
             act[q] += (s > 0);
           } else {
             const uint32_t lo = s & 0xffffu, hi = s >> 16;
-            *reinterpret_cast<int2*>(hrow + 2 * row) = make_int2((int)lo, (int)hi);
+            hrow[2 * row] = (int32_t)lo;  // two stores: with odd E the pair is not 8-byte aligned
+            hrow[2 * row + 1] = (int32_t)hi;
             csum[2 * q] += lo;
             csum[2 * q + 1] += hi;
             act[2 * q] += (lo > 0);
@@ -315,7 +316,10 @@ __device__ __forceinline__ void ring_commit() { asm volatile("cp.async.commit_gr
 template <int N>
 __device__ __forceinline__ void ring_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int MAXR>
+// WIDE: u32 counters, rows E + 1; packed (even E only): u16x2 counters, pair
+// rows E/2 + 1 (row E/2 low half = overflow), halves summed separately in the
+// cumulative reduction (a lane's half counts at most B*k <= 65535 per unit).
+template <bool WIDE, int MAXR>
 __global__ void __launch_bounds__(32)
 topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int k, int B, int E, int64_t T,
                       int64_t HT, int32_t* __restrict__ hist, int64_t* __restrict__ colsum,
@@ -326,7 +330,9 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
   uint4* ring = rsm;                                                  // [kRingStages][kRingUnroll][32]
   uint32_t* cnt = reinterpret_cast<uint32_t*>(rsm + kRingStages * BATCH);  // [E + 1][32]
   uint32_t* cnt_lane = cnt + lane;
-  const int rows = E + 1;
+  const int rows = WIDE ? E + 1 : E / 2 + 1;
+  const int hrows = WIDE ? E : E / 2;  // reduced rows holding real bins
+  constexpr int BINS = WIDE ? 1 : 2;
   for (int w = lane; w < rows * 32; w += 32) cnt[w] = 0;
   __syncwarp();
   const uint32_t uE = (uint32_t)E, Epair = uE | (uE << 16);
@@ -351,9 +357,9 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
       if (sidx < nb) issue(sidx);
       ring_commit();
     }
-    uint32_t prev[MAXR], act[MAXR];
+    uint32_t prev[MAXR * BINS], act[MAXR * BINS];
 #pragma unroll
-    for (int q = 0; q < MAXR; ++q) { prev[q] = 0; act[q] = 0; }
+    for (int q = 0; q < MAXR * BINS; ++q) { prev[q] = 0; act[q] = 0; }
     int in_step = 0;
     int64_t t = t_begin;
     for (int64_t bt = 0; bt < nb; ++bt) {
@@ -363,7 +369,7 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
       ring_commit();
       const uint4* cur = ring + (bt % kRingStages) * BATCH + lane;
 #pragma unroll
-      for (int u = 0; u < kRingUnroll; ++u) count_vec_wide<int16_t>(cnt_lane, cur[u * 32], uE, Epair);
+      for (int u = 0; u < kRingUnroll; ++u) count_vec<int16_t, WIDE>(cnt_lane, cur[u * 32], uE, Epair);
       if (++in_step == bps) {
         in_step = 0;
         __syncwarp();
@@ -371,18 +377,34 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
 #pragma unroll
         for (int q = 0; q < MAXR; ++q) {
           const int row = lane + q * 32;
-          if (row < E) {
+          if (row < hrows) {
             const uint4* rp = reinterpret_cast<const uint4*>(cnt + row * 32);
-            uint32_t sum = 0;
+            if (WIDE) {
+              uint32_t sum = 0;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const uint4 v = rp[(c + lane) & 7];
-              sum += (v.x + v.y) + (v.z + v.w);
+              for (int c = 0; c < 8; ++c) {
+                const uint4 v = rp[(c + lane) & 7];
+                sum += (v.x + v.y) + (v.z + v.w);
+              }
+              const uint32_t h = sum - prev[q];
+              prev[q] = sum;
+              hrow[row] = (int32_t)h;
+              act[q] += (h > 0);
+            } else {
+              uint32_t lo = 0, hi = 0;
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const uint4 v = rp[(c + lane) & 7];
+                lo += ((v.x & 0xffffu) + (v.y & 0xffffu)) + ((v.z & 0xffffu) + (v.w & 0xffffu));
+                hi += ((v.x >> 16) + (v.y >> 16)) + ((v.z >> 16) + (v.w >> 16));
+              }
+              const uint32_t hl = lo - prev[2 * q], hh = hi - prev[2 * q + 1];
+              prev[2 * q] = lo;
+              prev[2 * q + 1] = hi;
+              *reinterpret_cast<int2*>(hrow + 2 * row) = make_int2((int)hl, (int)hh);
+              act[2 * q] += (hl > 0);
+              act[2 * q + 1] += (hh > 0);
             }
-            const uint32_t h = sum - prev[q];
-            prev[q] = sum;
-            hrow[row] = (int32_t)h;
-            act[q] += (h > 0);
           }
         }
         __syncwarp();
@@ -390,16 +412,22 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
       }
     }
     ring_wait<0>();
-    uint32_t dropped = cnt[E * 32 + lane];
+    // overflow row: WIDE row E; packed (even E) the low half of pair row E/2
+    uint32_t dropped = WIDE ? cnt[E * 32 + lane] : (cnt[(E / 2) * 32 + lane] & 0xffffu);
     __syncwarp();
     for (int w = lane; w < rows * 32; w += 32) cnt[w] = 0;
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < MAXR; ++q) {
       const int row = lane + q * 32;
-      if (row >= E) continue;
-      if (prev[q]) atomicAdd((unsigned long long*)&colsum[l * E + row], (unsigned long long)prev[q]);
-      if (act[q]) atomicAdd(&active[l * E + row], (int)act[q]);
+      if (row >= hrows) continue;
+#pragma unroll
+      for (int bb = 0; bb < BINS; ++bb) {
+        const int bin = row * BINS + bb;
+        const uint32_t cs = prev[q * BINS + bb], ac = act[q * BINS + bb];
+        if (cs) atomicAdd((unsigned long long*)&colsum[l * E + bin], (unsigned long long)cs);
+        if (ac) atomicAdd(&active[l * E + bin], (int)ac);
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dropped += __shfl_xor_sync(0xffffffffu, dropped, o);
@@ -407,11 +435,12 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
   }
 }
 
-template <int MAXR>
+template <bool WIDE, int MAXR>
 static int launch_hist_ring(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
                             int32_t* hist, int64_t* colsum, int32_t* active, int64_t* dropped, cudaStream_t st) {
-  const size_t smem = (size_t)kRingStages * kRingUnroll * 32 * 16 + (size_t)(E + 1) * 32 * 4;
-  auto kern = topk_hist_ring_kernel<MAXR>;
+  const int rows = WIDE ? E + 1 : E / 2 + 1;
+  const size_t smem = (size_t)kRingStages * kRingUnroll * 32 * 16 + (size_t)rows * 32 * 4;
+  auto kern = topk_hist_ring_kernel<WIDE, MAXR>;
   GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                       cudaSharedmemCarveoutMaxShared));
@@ -453,13 +482,18 @@ template <typename IdT>
 static int dispatch_hist(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
                          int32_t* hist,
                          int64_t* colsum, int32_t* active, int64_t* dropped, cudaStream_t st) {
-  // ring variant: int16 ids, wide counters, every unit one whole-batch block
-  // (steps of whole 4 KB batches, N a multiple of B, 16-byte aligned ids)
+  // ring variant: int16 ids, every unit one whole-batch block (steps of whole
+  // 2 KB batches, N a multiple of B, 16-byte aligned ids); wide counters up to
+  // 160 experts, packed ones for even E up to 512
   const int64_t step_bytes = (int64_t)B * k * (int64_t)sizeof(IdT);
-  if (sizeof(IdT) == 2 && E <= 128 && N % B == 0 && step_bytes % (kRingUnroll * 32 * 16) == 0 &&
-      (reinterpret_cast<uintptr_t>(ids) & 15) == 0 && !std::getenv("GEM_HIST_NORING")) {
-    if (E <= 64) return launch_hist_ring<2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
-    return launch_hist_ring<4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+  if (sizeof(IdT) == 2 && N % B == 0 && step_bytes % (kRingUnroll * 32 * 16) == 0 &&
+      (reinterpret_cast<uintptr_t>(ids) & 15) == 0 && (E <= kWideMaxE || E % 2 == 0) &&
+      !std::getenv("GEM_HIST_NORING")) {
+    if (E <= 64) return launch_hist_ring<true, 2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+    if (E <= 128) return launch_hist_ring<true, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+    if (E <= kWideMaxE) return launch_hist_ring<true, 5>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+    if (E <= 256) return launch_hist_ring<false, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+    return launch_hist_ring<false, 8>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
   }
   if (E <= 64) return launch_hist_t<IdT, true, 2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
   if (E <= 128) return launch_hist_t<IdT, true, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);

@@ -53,10 +53,12 @@ def test_topk_hist_random_ids(oracle, dtype, shape):
 
 
 @pytest.mark.parametrize("shape", [(2, 64 * 1024, 8, 1024, 128), (1, 37 * 512, 8, 512, 100), (3, 33 * 256, 4, 256, 64),
-                                   (1, 40 * 1024, 8, 1024, 8)])
+                                   (1, 40 * 1024, 8, 1024, 8), (1, 40 * 512, 8, 512, 160), (2, 33 * 1024, 8, 1024, 256),
+                                   (1, 20 * 1024, 8, 1024, 300), (1, 20 * 1024, 8, 1024, 301)])
 def test_topk_hist_ring_path(oracle, shape):
-    """The cp.async-ring K1 (int16, E <= 128, whole 2 KB batches per step, N a
-    multiple of B): full and partial 32-step units, odd E, out-of-range ids."""
+    """The cp.async-ring K1 (int16, whole 2 KB batches per step, N a multiple of
+    B; wide counters to E = 160, packed for even E): full and partial 32-step
+    units, odd E, out-of-range ids (E = 301 takes the register-buffered kernel)."""
     L, N, k, B, E = shape
     rng = np.random.default_rng(sum(shape))
     ids = rng.integers(-3, E + 3, (L, N, k)).astype(np.int16)
