@@ -214,6 +214,11 @@ int gem_replay(const int32_t* hist, int64_t T, int32_t E, int32_t G, const int8_
  * swaps [R], final_score [R]. The workspace must be at least
  * gem_search_workspace_bytes(...) bytes of device memory. */
 size_t gem_search_workspace_bytes(int64_t R, int64_t T, int32_t E, int32_t G);
+/* Restart orders (search.py:188-193): order[r] = the experts by descending
+ * keys[r][e], ascending index on ties -- the reference's
+ * np.lexsort((arange(E), -keys)). keys f64 [R, E] (the host computes them with
+ * the reference's generator), order int16 [R, E]. */
+int gem_restart_order(const double* keys, int64_t R, int32_t E, int16_t* order, void* stream);
 int gem_search_runs(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G,
                     const double* lut, int64_t nmax, int64_t R, const int32_t* run_layer,
                     const uint8_t* needs_greedy, const int16_t* order, int8_t* assign,

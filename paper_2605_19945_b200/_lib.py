@@ -64,6 +64,7 @@ _SIGNATURES = {
     "gem_topk_hist": [P, I32, I64, I64, I32, I32, I32, P, P, P, P, P],
     "gem_topk_hist_rows": [P, I32, I64, I64, I32, I32, I32, P, I64, P, P, P, P],
     "gem_scale_gaps": [P, I64, I64, P, I32, P, P],
+    "gem_restart_order": [P, I64, I32, P, P],
     "gem_hist_colstats": [P, I64, I64, I32, P, P, P],
     "gem_step_gram": [P, I64, I64, I32, I64, P, P],
     "gem_step_gram_path": [I32, I64],

@@ -1719,6 +1719,32 @@ static size_t swap_smem(int E) {
 
 using namespace gem;
 
+// restart orders: one CTA per run; expert e goes to position
+// #{e' : key[e'] > key[e]} + #{e' < e : key[e'] == key[e]} (a stable sort by
+// descending key; -0.0 == 0.0 as in numpy's comparison)
+__global__ void restart_order_kernel(const double* __restrict__ keys, int E, int16_t* __restrict__ order) {
+  extern __shared__ double s_key[];
+  const int64_t r = blockIdx.x;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) s_key[e] = keys[r * E + e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const double v = s_key[e];
+    int pos = 0;
+    for (int q = 0; q < E; ++q) {
+      const double w = s_key[q];
+      pos += (w > v) || (w == v && q < e);
+    }
+    order[r * E + pos] = (int16_t)e;
+  }
+}
+
+extern "C" int gem_restart_order(const double* keys, int64_t R, int32_t E, int16_t* order, void* stream) {
+  GEM_REQUIRE(keys && order && R >= 1 && E >= 1 && E <= 6144, "gem_restart_order: bad arguments (E <= 6144)");
+  restart_order_kernel<<<(unsigned)R, 128, (size_t)E * sizeof(double), as_stream(stream)>>>(keys, E, order);
+  GEM_CHECK_LAUNCH("restart_order_kernel");
+  return GEM_OK;
+}
+
 extern "C" size_t gem_search_workspace_bytes(int64_t R, int64_t T, int32_t E, int32_t G) {
   return carve(nullptr, nullptr, R, T, E, G);
 }

@@ -131,9 +131,10 @@ class RunBatch:
 
     run_layer: np.ndarray     # [R] int32
     needs_greedy: np.ndarray  # [R] uint8
-    order: np.ndarray         # [R, E] int16 (greedy expert order; ignored for seeded runs)
+    order: np.ndarray | None  # [R, E] int16 (greedy expert order; ignored for seeded runs)
     assign: np.ndarray        # [R, E] int8  (seed mapping; output for greedy runs)
     provenance: list[str]
+    keys: np.ndarray | None = None  # [R, E] f64 order keys, sorted on the device when order is None
 
 
 def layer_jobs(mean_util: np.ndarray, num_gpus: int, config: SearchConfig, layer: int) -> RunBatch:
@@ -159,35 +160,42 @@ def layer_jobs(mean_util: np.ndarray, num_gpus: int, config: SearchConfig, layer
                     np.asarray(orders, dtype=np.int16), np.asarray(assigns, dtype=np.int8), prov)
 
 
-def all_layer_jobs(mean_util: np.ndarray, num_gpus: int, config: SearchConfig) -> RunBatch:
+def all_layer_jobs(mean_util: np.ndarray, num_gpus: int, config: SearchConfig,
+                   device_order: bool = False) -> RunBatch:
     """layer_jobs for every layer of mean_util [L, E] at once, in the same run
     order. The restart noise comes from default_rng(seed ^ i) -- the same draw
     for every layer -- so it is drawn once per restart; the keys are the same
     fp64 products and a stable argsort of -key is the reference's lexsort
-    (descending key, ascending expert index on ties)."""
+    (descending key, ascending expert index on ties). device_order: leave the
+    sort to gem_restart_order (run_search_device) and ship the keys."""
     mu = np.asarray(mean_util, dtype=np.float64)
     L, E = mu.shape
     K = config.restarts
     nb = 2 if config.seed_with_baselines else 0
     per = K + nb
-    order = np.empty((L, per, E), dtype=np.int16)
+    keys_all = np.zeros((L, per, E))  # seeded runs: all-equal keys, identity order (unused)
     assign = np.zeros((L, per, E), dtype=np.int8)
     for i in range(K):
         keys = mu
         if i > 0:
             eta = np.random.default_rng(config.rng_seed ^ i).uniform(-1.0, 1.0, E)
             keys = mu * (1.0 + config.noise_fraction * eta)
-        order[:, i] = np.argsort(-keys, axis=1, kind="stable")
+        keys_all[:, i] = keys
+    order = None
+    if not device_order:
+        order = np.empty((L, per, E), dtype=np.int16)
+        order[:, :K] = np.argsort(-keys_all[:, :K], axis=2, kind="stable")
+        order[:, K:] = np.arange(E, dtype=np.int16)
+        order = order.reshape(L * per, E)
     prov = [f"greedy:{i}" for i in range(K)]
     if nb:
-        order[:, K:] = np.arange(E, dtype=np.int16)
         assign[:, K] = linear_assignment(E, num_gpus)
         assign[:, K + 1] = eplb_assignments(mu, num_gpus)
         prov += ["baseline:linear", "baseline:eplb"]
     greedy = np.zeros(per, dtype=np.uint8)
     greedy[:K] = 1
-    return RunBatch(np.repeat(np.arange(L, dtype=np.int32), per), np.tile(greedy, L),
-                    order.reshape(L * per, E), assign.reshape(L * per, E), prov * L)
+    return RunBatch(np.repeat(np.arange(L, dtype=np.int32), per), np.tile(greedy, L), order,
+                    assign.reshape(L * per, E), prov * L, keys=keys_all.reshape(L * per, E))
 
 
 def concat_batches(batches: list[RunBatch]) -> RunBatch:
@@ -229,7 +237,12 @@ def run_search_device(hist: torch.Tensor, nmax: int, profile: VariabilityProfile
     traj_cap = swap_cap + 1
     run_layer = _device.upload(batch.run_layer, torch.int32)
     needs = _device.upload(batch.needs_greedy, torch.uint8)
-    order = _device.upload(batch.order, torch.int16)
+    if batch.order is None:  # restart orders sorted on the device from the host-drawn keys
+        keys = _device.upload(batch.keys, torch.float64)
+        order = _device.empty((R, E), torch.int16)
+        _lib.call("gem_restart_order", ptr(keys), R, E, ptr(order), stream())
+    else:
+        order = _device.upload(batch.order, torch.int16)
     assign = _device.upload(batch.assign, torch.int8)
     traj = _device.zeros((R, traj_cap), torch.float64)
     swaps = _device.zeros((R,), torch.int32)
@@ -320,7 +333,7 @@ def search_hist(hist: torch.Tensor, nmax: int, profile: VariabilityProfile, conf
         ds = device_stats(hist, with_gram=False)
         mu_dev, _, _ = finalize_stats(ds, with_corr=False)
         mean_util = _device.host(mu_dev)
-    batch = all_layer_jobs(np.asarray(mean_util).reshape(L, E), G, config)
+    batch = all_layer_jobs(np.asarray(mean_util).reshape(L, E), G, config, device_order=True)
     res = run_search_device(hist, nmax, profile, batch, config.convergence_threshold, config.swap_cap(E))
     out = []
     per = len(batch.provenance) // L

@@ -485,6 +485,26 @@ def test_best_swap_screen_versions_agree(monkeypatch):
     assert (bool(v5[0][r]), int(v5[1][r]), int(v5[2][r]), float(v5[3][r])) == (bool(found), i, j, cand)
 
 
+def test_restart_order_kernel_matches_lexsort():
+    """gem_restart_order == np.lexsort((arange(E), -keys)) per row (search.py:188-193),
+    with exact ties, zeros, -0.0 and all-equal rows."""
+    from paper_2605_19945_b200 import _device, _lib
+
+    rng = np.random.default_rng(17)
+    for R, E in ((7, 128), (3, 256), (5, 13), (2, 1)):
+        keys = rng.random((R, E))
+        keys[0, : E // 2] = keys[0, E // 2: 2 * (E // 2)]  # pairs of equal keys
+        keys[1 % R] = 0.0
+        if E > 3:
+            keys[2 % R, :3] = [0.0, -0.0, 0.0]
+        d = _device.upload(keys, torch.float64)
+        out = _device.empty((R, E), torch.int16)
+        _lib.call("gem_restart_order", d.data_ptr(), R, E, out.data_ptr(), _device.stream())
+        got = out.cpu().numpy()
+        want = np.stack([np.lexsort((np.arange(E), -keys[r])) for r in range(R)])
+        assert np.array_equal(got, want)
+
+
 # ------------------------------------------------- full size, against the reference build
 
 def test_fullsize_layer_matches_reference_build(oracle):

@@ -267,6 +267,11 @@ def test_all_layer_jobs_equals_per_layer_jobs():
         assert np.array_equal(got.needs_greedy, want.needs_greedy)
         assert np.array_equal(got.run_layer, want.run_layer)
         assert got.provenance == want.provenance
+        # the keys shipped for the device sort give the same orders
+        dev = S.all_layer_jobs(mu, 4, cfg, device_order=True)
+        assert dev.order is None and np.array_equal(dev.assign, want.assign)
+        greedy_rows = want.needs_greedy.astype(bool)
+        assert np.array_equal(np.argsort(-dev.keys[greedy_rows], axis=1, kind="stable"), want.order[greedy_rows])
 
 
 def test_eplb_assignments_equals_per_row():
