@@ -762,11 +762,11 @@ struct Swap3Geom {
   int n, ng, nb_pad, units_per_run, rpc;
 };
 
-__host__ __device__ inline Swap3Geom swap3_geom(int E, int G) {
+__host__ __device__ inline Swap3Geom swap3_geom(int E, int G, int Y = kSwapY) {
   Swap3Geom g;
   g.n = E / G;
-  g.ng = (g.n + kSwapY - 1) / kSwapY;
-  g.nb_pad = g.ng * kSwapY;
+  g.ng = (g.n + Y - 1) / Y;
+  g.nb_pad = g.ng * Y;
   g.units_per_run = g.n * g.ng;
   g.rpc = kSwap3Threads / g.units_per_run;
   if (g.rpc < 1) g.rpc = 1;
@@ -1041,8 +1041,8 @@ __host__ __device__ inline size_t swap5_buf_bytes(const Swap3Geom& g, int G) {
 }
 
 // W = table window (loads never exceed W - 1)
-__host__ __device__ inline size_t swap5_smem(int E, int G, int64_t W) {
-  const Swap3Geom g = swap3_geom(E, G);
+__host__ __device__ inline size_t swap5_smem(int E, int G, int64_t W, int Y) {
+  const Swap3Geom g = swap3_geom(E, G, Y);
   const size_t lut = ((size_t)2 * (size_t)W * 4 + 15) & ~size_t(15);
   const size_t fixed = (size_t)g.rpc * (8 + 8 + 8 + 8) + ((((size_t)g.rpc * 2 * g.n * 2) + 15) & ~size_t(15)) +
                        2 * (kBuckets + 2) * 2 + 64;
@@ -1050,14 +1050,16 @@ __host__ __device__ inline size_t swap5_smem(int E, int G, int64_t W) {
 }
 
 
-// GT > 0: instantiated for exactly GT GPUs (the pother pass unrolls); 0: any G
-template <int GT>
+// GT > 0: instantiated for exactly GT GPUs (the pother pass unrolls); 0: any G.
+// Y: y experts per thread (4; 2 when a GPU holds <= 8 experts, so a CTA's
+// per-run staging halves and two CTAs fit an SM -- the DeepSeek-V3 shape)
+template <int GT, int Y>
 __global__ void __launch_bounds__(kSwap3Threads, GEM_SCAN_MINB)
 approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int32_t* __restrict__ run_layer,
                     const int8_t* __restrict__ assign, int32_t n_active, SearchWs ws, int64_t tseg) {
   extern __shared__ __align__(16) unsigned char s5[];
   const int G = GT > 0 ? GT : G_;
-  const Swap3Geom geo = swap3_geom(E, G);
+  const Swap3Geom geo = swap3_geom(E, G, Y);
   const int n = geo.n, ng = geo.ng, RPC = geo.rpc, nb_pad = geo.nb_pad;
   const int NP = G * (G - 1) / 2;
   const int slot0 = blockIdx.y * RPC;
@@ -1226,9 +1228,9 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
     const int s = live ? u / geo.units_per_run : 0;
     const int ur = live ? u % geo.units_per_run : 0;
     const int x = ur / ng, yg = ur % ng;  // y experts of this thread: yg + q*ng
-    double acc[kSwapY];
+    double acc[Y];
 #pragma unroll
-    for (int q = 0; q < kSwapY; ++q) acc[q] = 0.0;
+    for (int q = 0; q < Y; ++q) acc[q] = 0.0;
 
     // kSwap5Stages-deep cp.async ring: chunks c+1 .. c+S-1 in flight while c is scanned
 #pragma unroll
@@ -1285,9 +1287,9 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
         const uint16_t* lbs = las + TC;
         const uint16_t* hAs = B.h + ((size_t)s * hrows + x) * RS;
         const uint16_t* hBs = B.h + ((size_t)s * hrows + n + yg) * RS;
-        float c[kSwapY];
+        float c[Y];
 #pragma unroll
-        for (int q = 0; q < kSwapY; ++q) c[q] = 0.0f;
+        for (int q = 0; q < Y; ++q) c[q] = 0.0f;
 #pragma unroll 2
         for (int tt = 0; tt < TC; tt += 4) {
           const uint2 hx2 = *reinterpret_cast<const uint2*>(hAs + tt);
@@ -1297,9 +1299,9 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
           const uint4 ta4 = *reinterpret_cast<const uint4*>(tha + tt);
           const uint4 tb4 = *reinterpret_cast<const uint4*>(thb + tt);
           const uint32_t taj[4] = {ta4.x, ta4.y, ta4.z, ta4.w}, tbj[4] = {tb4.x, tb4.y, tb4.z, tb4.w};
-          uint2 hy2[kSwapY];
+          uint2 hy2[Y];
 #pragma unroll
-          for (int q = 0; q < kSwapY; ++q) hy2[q] = *reinterpret_cast<const uint2*>(hBs + (size_t)q * ng * RS + tt);
+          for (int q = 0; q < Y; ++q) hy2[q] = *reinterpret_cast<const uint2*>(hBs + (size_t)q * ng * RS + tt);
           const float pj[4] = {p4.x, p4.y, p4.z, p4.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -1309,7 +1311,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
             const uint32_t lb = (j & 1) ? (wb >> 16) : (wb & 0xffffu);
             const uint32_t ra = base_a + la * 4u - hx, rb = base_b + lb * 4u + hx;
 #pragma unroll
-            for (int q = 0; q < kSwapY; ++q) {
+            for (int q = 0; q < Y; ++q) {
               const uint32_t wy = (j < 2) ? hy2[q].x : hy2[q].y;
               const uint32_t hy = (j & 1) ? (wy >> 16) : (wy & 0xffffu);
               c[q] += fmaxf(fmaxf(pj[j], lds_f32(max(ra + hy, taj[j]))), lds_f32(max(rb - hy, tbj[j])));
@@ -1317,7 +1319,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
           }
         }
 #pragma unroll
-        for (int q = 0; q < kSwapY; ++q) acc[q] = dadd(acc[q], (double)c[q]);
+        for (int q = 0; q < Y; ++q) acc[q] = dadd(acc[q], (double)c[q]);
       }
     }
     if (split) {  // partial sums of this step range (fp64 adds in any order: within the screen's bound)
@@ -1325,7 +1327,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
         const int r = ws.run_list[slot0 + s];
         double* pa = ws.split_acc + (((int64_t)r * NP + blockIdx.x) * n + x) * n;
 #pragma unroll
-        for (int q = 0; q < kSwapY; ++q)
+        for (int q = 0; q < Y; ++q)
           if (yg + q * ng < n) atomicAdd(pa + yg + q * ng, acc[q]);
       }
       continue;
@@ -1333,7 +1335,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
     if (live) {
       double mn = acc[0];
 #pragma unroll
-      for (int q = 1; q < kSwapY; ++q)
+      for (int q = 1; q < Y; ++q)
         if (yg + q * ng < n) mn = fmin(mn, acc[q]);
       atomicMin(&smin[s], ord_bits(mn));
     }
@@ -1344,7 +1346,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
       const double lim = __longlong_as_double((long long)smin[s]) * kWindow5;
       const int xe = lists[(s * 2 + 0) * n + x];
 #pragma unroll
-      for (int q = 0; q < kSwapY; ++q) {
+      for (int q = 0; q < Y; ++q) {
         const int yi = yg + q * ng;
         if (yi >= n || !(acc[q] <= lim)) continue;
         const int ye = lists[(s * 2 + 1) * n + yi];
@@ -1793,7 +1795,8 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   // v5 needs only the two tables of its GPU pair in shared memory (v4 stages
   // every GPU's latencies: too large at G = 32)
   const int W5 = ws.win > 0 ? ws.win : (int)(nmax + 1);
-  const size_t smem5 = swap5_smem(E, G, W5);
+  const int y5 = E / G <= 8 ? 2 : kSwapY;
+  const size_t smem5 = swap5_smem(E, G, W5, y5);
   const bool v5 = ws.ht16s != nullptr && ws.first != nullptr && smem5 <= (size_t)optin && !std::getenv("GEM_SCAN_V4");
   if (ws.lut32 == nullptr || ws.ht16 == nullptr || (!v5 && smem3 > (size_t)optin)) {
     return launch_exact_scan(hist, T, E, G, lut, nmax, R, run_layer, assign, ws, nullptr, st);
@@ -1802,7 +1805,7 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   compact_runs_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(R, ws);
   GEM_CHECK_LAUNCH("compact_runs_kernel");
   GEM_CHECK_CUDA(cudaMemsetAsync(ws.loc_cnt, 0, (size_t)R * NP * 4, st));
-  const Swap3Geom g = swap3_geom(E, G);
+  const Swap3Geom g = swap3_geom(E, G, v5 ? y5 : kSwapY);
   dim3 grid((unsigned)NP, (unsigned)((n_active + g.rpc - 1) / g.rpc));
   double window = kWindow;
   if (v5) {
@@ -1837,8 +1840,11 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
       }
       return GEM_OK;
     };
-    const int rc5 = G == 8 ? go5(approx_scan5_kernel<8>) : (G == 4 ? go5(approx_scan5_kernel<4>)
-                                                                    : go5(approx_scan5_kernel<0>));
+    const int rc5 =
+        y5 == 2 ? (G == 8 ? go5(approx_scan5_kernel<8, 2>) : (G == 4 ? go5(approx_scan5_kernel<4, 2>)
+                                                                      : go5(approx_scan5_kernel<0, 2>)))
+                : (G == 8 ? go5(approx_scan5_kernel<8, kSwapY>) : (G == 4 ? go5(approx_scan5_kernel<4, kSwapY>)
+                                                                           : go5(approx_scan5_kernel<0, kSwapY>)));
     if (rc5) return rc5;
     window = kWindow5;
   } else {
