@@ -211,7 +211,7 @@ class RunResults:
     assign: np.ndarray        # [R, E] int64
     final_score: np.ndarray   # [R] fp64
     swaps: np.ndarray         # [R] int32
-    trajectory: np.ndarray    # [R, cap+1] fp64
+    trajectory: np.ndarray    # [R, max swaps + 1] fp64 (columns past a run's swaps are unused)
 
     def record(self, r: int, provenance: str) -> RestartRecord:
         if "_lists" not in self.__dict__:  # python floats/ints of every run, converted once
@@ -252,8 +252,10 @@ def run_search_device(hist: torch.Tensor, nmax: int, profile: VariabilityProfile
     _lib.call("gem_search_runs", ptr(hist), L, T, E, G, ptr(lut), dc.lut_nmax, R, ptr(run_layer), ptr(needs),
               ptr(order), ptr(assign), float(threshold), int(swap_cap), int(traj_cap), ptr(traj), ptr(swaps),
               ptr(final), ptr(ws), ws_bytes, stream())
-    return RunResults(_device.host(assign).astype(np.int64), _device.host(final), _device.host(swaps),
-                      _device.host(traj))
+    swaps_h = _device.host(swaps)
+    width = int(swaps_h.max(initial=0)) + 1  # only the used trajectory columns cross PCIe
+    return RunResults(_device.host(assign).astype(np.int64), _device.host(final), swaps_h,
+                      _device.host(traj[:, :width].contiguous()))
 
 
 def _pick_best(final_scores, lo: int, hi: int) -> int:
