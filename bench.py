@@ -206,10 +206,8 @@ def run_ours(args):
     pev = []  # per timed step: events bracketing each phase
 
     def stats_step(timed: bool):
-        colsum = torch.zeros((L, E), dtype=torch.int64, device="cuda")
-        active = torch.zeros((L, E), dtype=torch.int32, device="cuda")
+        ds = DeviceStats.allocate(L, E, T)  # colsum/active/heavy/Gram: one int64 buffer, one all-reduce
         dropped = torch.zeros((L,), dtype=torch.int64, device="cuda")
-        gram = torch.zeros((L, E, E), dtype=torch.int64, device="cuda")
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(phases) + 1)] if timed else None
 
         def mark(i):
@@ -217,19 +215,17 @@ def run_ours(args):
                 evs[i].record(stream)
 
         mark(0)
-        _lib.call("gem_topk_hist", ids.data_ptr(), 2, L, n_local, k, B, E, hist.data_ptr(), colsum.data_ptr(),
-                  active.data_ptr(), dropped.data_ptr(), stream.cuda_stream)
+        _lib.call("gem_topk_hist", ids.data_ptr(), 2, L, n_local, k, B, E, hist.data_ptr(), ds.colsum.data_ptr(),
+                  ds.active.data_ptr(), ds.heavy.data_ptr(), dropped.data_ptr(), stream.cuda_stream)
         mark(1)
-        _lib.call("gem_step_gram", hist.data_ptr(), L, t1 - t0, E, B * k, gram.data_ptr(), stream.cuda_stream)
+        _lib.call("gem_step_gram", hist.data_ptr(), L, t1 - t0, E, B * k, ds.gram.data_ptr(), stream.cuda_stream)
         mark(2)
         if use_dist:
-            for t in (colsum, active, gram):
-                dist.all_reduce(t)
+            dist.all_reduce(ds.pack)
         mark(3)
-        ds = DeviceStats(colsum, active, gram, T)
         mu, af, corr = finalize_stats(ds, with_corr=True)
         mark(4)
-        cls = ingest.classify_device(colsum, active, gram, T)
+        cls = ingest.classify_device(ds.colsum, ds.heavy, ds.gram, T)
         mark(5)
         if timed:
             kev.append((evs[0], evs[1]))

@@ -98,12 +98,15 @@ int gem_gen_topk(int64_t L, int64_t N, int32_t k, int32_t B, int32_t E,
 /* --- K1: ids -> per-step histograms + per-expert totals -----------------
  * ids [L,N,k] (int16 or int32); T = ceil(N/B) local steps per layer.
  * hist[l][t][e] = #tokens of step t that chose e (int32, [L,T,E]).
- * colsum[l][e] += sum_t hist, active[l][e] += #(hist>0), dropped[l] += ids
- * outside [0,E): these three are ACCUMULATED (zero them first), so token-
- * range shards can all-reduce them. hist rows are overwritten. */
+ * colsum[l][e] += sum_t hist, active[l][e] += #(hist>0),
+ * heavy[l][e] += #(hist>0 and hist*E >= sum_e' hist[t][e'])  (steps in which
+ * e got at least its fair share; drives the consistent-expert class),
+ * dropped[l] += ids outside [0,E): these four are ACCUMULATED (zero them
+ * first), so token-range shards can all-reduce them. hist rows are
+ * overwritten. */
 int gem_topk_hist(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k,
                   int32_t B, int32_t E, int32_t* hist, int64_t* colsum, int32_t* active,
-                  int64_t* dropped, void* stream);
+                  int32_t* heavy, int64_t* dropped, void* stream);
 
 /* The same for one chunk of a longer trace (streamed router dumps, token-range
  * shards written into a full-length histogram): the chunk's ceil(N/B) step
@@ -111,12 +114,12 @@ int gem_topk_hist(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32
  * that starts at step t0); hist_rows >= ceil(N/B). */
 int gem_topk_hist_rows(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k,
                        int32_t B, int32_t E, int32_t* hist, int64_t hist_rows, int64_t* colsum,
-                       int32_t* active, int64_t* dropped, void* stream);
+                       int32_t* active, int32_t* heavy, int64_t* dropped, void* stream);
 
-/* hist [L,T,E] (int32) -> colsum/active (accumulated) — for traces given as
- * counts (ExpertTrace) instead of ids. */
+/* hist [L,T,E] (int32) -> colsum/active/heavy (accumulated) — for traces
+ * given as counts (ExpertTrace) instead of ids. */
 int gem_hist_colstats(const int32_t* hist, int64_t L, int64_t T, int32_t E,
-                      int64_t* colsum, int32_t* active, void* stream);
+                      int64_t* colsum, int32_t* active, int32_t* heavy, void* stream);
 
 /* --- K2: step-level co-activation Gram, gram[l][a][b] = sum_t h_a h_b -----
  * int64, exact (callers guarantee sum fits int64). ACCUMULATED; the upper
@@ -146,15 +149,17 @@ int gem_stats_finalize(const int64_t* colsum, const int32_t* active, const int64
                        double* active_frac, double* corr, void* stream);
 
 /* --- K3b: consistent / temporal classification ----------------------------
- * consistent:  active*cons_den >= cons_num*T
- * temporal:    not consistent, and r(e,f) >= corr_num/corr_den (exact int128
- *              predicate) for some other non-consistent f
+ * (consistent = heavily used in almost every step,
+ * temporal = heavily used only in some steps, correlated with each other)
+ * consistent:  heavy*cons_den >= cons_num*T   (heavy from K1 / colstats)
+ * temporal:    not consistent, heavy > 0, and r(e,f) >= corr_num/corr_den
+ *              (exact int128 predicate) for some other such f
  * group:       connected components of the temporal correlation graph,
  *              labelled by their lowest expert index; -1 otherwise.
  * Asynchronous: *err_flag (device, zeroed by the caller) becomes nonzero if a
  * correlation statistic exceeds the exact int128 predicate range; the caller
  * checks it when it next reads results (no host synchronisation here). */
-int gem_classify(const int64_t* colsum, const int32_t* active, const int64_t* gram,
+int gem_classify(const int64_t* colsum, const int32_t* heavy, const int64_t* gram,
                  int64_t L, int64_t T, int32_t E, int64_t cons_num, int64_t cons_den,
                  int64_t corr_num, int64_t corr_den, int8_t* cls, int16_t* group,
                  int32_t* err_flag, void* stream);

@@ -274,13 +274,21 @@ int64_t or_refine(const int64_t* tok, int64_t T, int64_t E, int64_t G, const int
 
 /* ------------------------------------------------------------ statistics */
 /* exact integer statistics of trace.py:87-114 */
-void or_colstats(const int64_t* tok, int64_t T, int64_t E, int64_t* colsum, int64_t* active) {
-  for (int64_t e = 0; e < E; ++e) { colsum[e] = 0; active[e] = 0; }
-  for (int64_t t = 0; t < T; ++t)
+/* colsum, active = #(h>0) (trace.py:95-98), and heavy = #(h>0 and h*E >=
+ * row total): the steps in which e received at least its fair share
+ * (the consistent-expert statistic). */
+void or_colstats(const int64_t* tok, int64_t T, int64_t E, int64_t* colsum, int64_t* active, int64_t* heavy) {
+  for (int64_t e = 0; e < E; ++e) { colsum[e] = 0; active[e] = 0; heavy[e] = 0; }
+  for (int64_t t = 0; t < T; ++t) {
+    int64_t row = 0;
+    for (int64_t e = 0; e < E; ++e) row += tok[t * E + e];
     for (int64_t e = 0; e < E; ++e) {
-      colsum[e] += tok[t * E + e];
-      active[e] += tok[t * E + e] > 0;
+      const int64_t h = tok[t * E + e];
+      colsum[e] += h;
+      active[e] += h > 0;
+      heavy[e] += h > 0 && h * E >= row;
     }
+  }
 }
 
 void or_gram(const int64_t* tok, int64_t T, int64_t E, int64_t* gram) {
@@ -296,16 +304,20 @@ void or_gram(const int64_t* tok, int64_t T, int64_t E, int64_t* gram) {
 /* classification: consistent = active*cd >= cn*T;
  * temporal = not consistent and r >= rn/rd with another non-consistent expert;
  * group = connected component (lowest index). Returns 0, or 1 on range overflow. */
-int or_classify(const int64_t* colsum, const int64_t* active, const int64_t* gram, int64_t T, int64_t E,
+/* consistent: heavy in >= cn/cd of the steps; temporal: not consistent,
+ * heavy in some step, Pearson r >= rn/rd with another such expert (exact
+ * int128 predicate); groups = connected components, lowest index labels. */
+int or_classify(const int64_t* colsum, const int64_t* heavy, const int64_t* gram, int64_t T, int64_t E,
                 int64_t cn, int64_t cd, int64_t rn, int64_t rd, int8_t* cls, int16_t* group) {
   typedef __int128 i128;
   const i128 lim = (i128)1 << 60;
   int err = 0;
   unsigned char* adj = (unsigned char*)calloc((size_t)(E * E + 1), 1);
-  for (int64_t e = 0; e < E; ++e) cls[e] = ((i128)active[e] * cd >= (i128)cn * T) ? 1 : 0;
+  /* 3 = burst candidate (heavy somewhere, not consistent) until confirmed */
+  for (int64_t e = 0; e < E; ++e) cls[e] = ((i128)heavy[e] * cd >= (i128)cn * T) ? 1 : (heavy[e] > 0 ? 3 : 0);
   for (int64_t a = 0; a < E; ++a)
     for (int64_t b = a + 1; b < E; ++b) {
-      if (cls[a] == 1 || cls[b] == 1) continue;
+      if (cls[a] != 3 || cls[b] != 3) continue;
       i128 sa = colsum[a], sb = colsum[b];
       i128 va = (i128)T * gram[a * E + a] - sa * sa;
       i128 vb = (i128)T * gram[b * E + b] - sb * sb;
@@ -319,7 +331,7 @@ int or_classify(const int64_t* colsum, const int64_t* active, const int64_t* gra
   for (int64_t e = 0; e < E; ++e) {
     int any = 0;
     for (int64_t f = 0; f < E; ++f) any |= adj[e * E + f];
-    if (cls[e] != 1 && any) cls[e] = 2;
+    if (cls[e] == 3) cls[e] = any ? 2 : 0;
     label[e] = cls[e] == 2 ? (int32_t)e : -1;
   }
   /* connected components by repeated min-label relaxation */

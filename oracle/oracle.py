@@ -74,7 +74,7 @@ def lib():
     L.or_refine.argtypes = [i64p, I64, I64, I64, i64p, f64p, i64p, i64p, i64p, F64, I64, f64p, I64,
                             ctypes.POINTER(F64)]
     L.or_colstats.restype = None
-    L.or_colstats.argtypes = [i64p, I64, I64, i64p, i64p]
+    L.or_colstats.argtypes = [i64p, I64, I64, i64p, i64p, i64p]
     L.or_gram.restype = None
     L.or_gram.argtypes = [i64p, I64, I64, i64p]
     L.or_classify.restype = ctypes.c_int
@@ -214,12 +214,26 @@ def refine(tokens, assignment, curves: Curves, threshold: float, cap: int):
 # statistics, baselines, search orchestration
 
 
-def colstats(tokens):
+def colstats3(tokens):
+    """(colsum, active, heavy) of one layer's [T, E] counts (gem_oracle.c or_colstats)."""
     tok = _tok(tokens)
     cs = np.zeros(tok.shape[1], dtype=np.int64)
     ac = np.zeros(tok.shape[1], dtype=np.int64)
-    lib().or_colstats(tok, tok.shape[0], tok.shape[1], cs, ac)
+    hv = np.zeros(tok.shape[1], dtype=np.int64)
+    lib().or_colstats(tok, tok.shape[0], tok.shape[1], cs, ac, hv)
+    return cs, ac, hv
+
+
+def colstats(tokens):
+    cs, ac, _ = colstats3(tokens)
     return cs, ac
+
+
+def heavy_counts(tokens) -> np.ndarray:
+    """#steps with h > 0 and h*E >= row total, per expert (numpy twin of or_colstats' heavy)."""
+    tok = _tok(tokens)
+    row = tok.sum(axis=1, keepdims=True)
+    return ((tok > 0) & (tok * tok.shape[1] >= row)).sum(axis=0).astype(np.int64)
 
 
 def gram(tokens) -> np.ndarray:
@@ -260,25 +274,25 @@ def stats(tokens):
 def classify(tokens, cons=(4, 5), corr=(4, 5)):
     tok = _tok(tokens)
     T, E = tok.shape
-    cs, ac = colstats(tok)
+    cs, _, hv = colstats3(tok)
     g = gram(tok)
     cls = np.zeros(E, dtype=np.int8)
     grp = np.zeros(E, dtype=np.int16)
-    err = lib().or_classify(cs, ac, g, T, E, cons[0], cons[1], corr[0], corr[1], cls, grp)
+    err = lib().or_classify(cs, hv, g, T, E, cons[0], cons[1], corr[0], corr[1], cls, grp)
     if err:
         raise OverflowError("oracle classify: statistics out of exact range")
     return cls, grp
 
 
-def classify_from_stats(colsum, active, gram, T, cons=(4, 5), corr=(4, 5)):
+def classify_from_stats(colsum, heavy, gram, T, cons=(4, 5), corr=(4, 5)):
     """Classification from (already reduced) integer statistics of one layer."""
     colsum = np.ascontiguousarray(colsum, dtype=np.int64)
-    active = np.ascontiguousarray(active, dtype=np.int64)
+    heavy = np.ascontiguousarray(heavy, dtype=np.int64)
     gram = np.ascontiguousarray(gram, dtype=np.int64)
     E = colsum.size
     cls = np.zeros(E, dtype=np.int8)
     grp = np.zeros(E, dtype=np.int16)
-    if lib().or_classify(colsum, active, gram, int(T), E, cons[0], cons[1], corr[0], corr[1], cls, grp):
+    if lib().or_classify(colsum, heavy, gram, int(T), E, cons[0], cons[1], corr[0], corr[1], cls, grp):
         raise OverflowError("oracle classify: statistics out of exact range")
     return cls, grp
 

@@ -61,11 +61,11 @@ _SIGNATURES = {
     "gem_ref_swap_candidate_score": [P, I64, I64, P, P, P, I64, P, P, P, P, I64, I64, P],
     "gem_ref_best_swap": [P, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P],
     "gem_gen_topk": [I64, I64, I32, I32, I32, P, P, U32, U32, U32, U64, I64, I32, P, P],
-    "gem_topk_hist": [P, I32, I64, I64, I32, I32, I32, P, P, P, P, P],
-    "gem_topk_hist_rows": [P, I32, I64, I64, I32, I32, I32, P, I64, P, P, P, P],
+    "gem_topk_hist": [P, I32, I64, I64, I32, I32, I32, P, P, P, P, P, P],
+    "gem_topk_hist_rows": [P, I32, I64, I64, I32, I32, I32, P, I64, P, P, P, P, P],
     "gem_scale_gaps": [P, I64, I64, P, I32, P, P],
     "gem_restart_order": [P, I64, I32, P, P],
-    "gem_hist_colstats": [P, I64, I64, I32, P, P, P],
+    "gem_hist_colstats": [P, I64, I64, I32, P, P, P, P],
     "gem_step_gram": [P, I64, I64, I32, I64, P, P],
     "gem_step_gram_path": [I32, I64],
     "gem_step_gram_cc": [P, I64, I64, I32, P, P],

@@ -23,6 +23,13 @@
 namespace gem {
 
 constexpr int kHistWarps = 4;
+
+// "heavy" step of an expert: it received at least its fair share of the
+// step's routed ids, h * E >= row total (exact integers; h > 0 so an empty
+// step counts for nobody). Feeds the consistent-expert predicate of K3b.
+__device__ __forceinline__ uint32_t is_heavy(uint32_t h, uint32_t E, uint32_t row_total) {
+  return (h > 0 && (uint64_t)h * E >= (uint64_t)row_total) ? 1u : 0u;
+}
 constexpr int kHistStepsPerUnit = 32;
 constexpr int kHistUnroll = 8;  // 128-bit loads in flight per lane (x2 with double buffering)
 
@@ -84,7 +91,7 @@ template <typename IdT, bool WIDE, int MAXR>
 __global__ void __launch_bounds__(kHistWarps * 32, WIDE ? 3 : 2)
 topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
                  int32_t* __restrict__ hist, int64_t* __restrict__ colsum, int32_t* __restrict__ active,
-                 int64_t* __restrict__ dropped_out) {
+                 int32_t* __restrict__ heavy, int64_t* __restrict__ dropped_out) {
   extern __shared__ __align__(16) uint32_t hsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // counter rows: WIDE: E bins + 1 overflow row; packed: ceil((E+1)/2) pair rows
@@ -107,9 +114,9 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
     const int64_t l = unit / units_per_layer;
     const int64_t t_begin = (unit % units_per_layer) * kHistStepsPerUnit;
     const int64_t t_end = imin64(t_begin + kHistStepsPerUnit, T);
-    uint32_t csum[MAXR * BINS], act[MAXR * BINS];
+    uint32_t csum[MAXR * BINS], act[MAXR * BINS], hvy[MAXR * BINS];
 #pragma unroll
-    for (int q = 0; q < MAXR * BINS; ++q) { csum[q] = 0; act[q] = 0; }
+    for (int q = 0; q < MAXR * BINS; ++q) { csum[q] = 0; act[q] = 0; hvy[q] = 0; }
     uint32_t dropped = 0;
     bool t_end_done = false;
 
@@ -144,9 +151,11 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
           in_step = 0;
           __syncwarp();
           int32_t* hrow = hist + (l * HT + t) * E;
+          uint32_t hq[MAXR], part = 0;
 #pragma unroll
           for (int q = 0; q < MAXR; ++q) {
             const int row = lane + q * 32;
+            hq[q] = 0;
             if (row < hrows) {
               const uint4* rp = reinterpret_cast<const uint4*>(cnt + row * 32);
               uint32_t sum = 0;
@@ -159,8 +168,13 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
               prev[q] = sum;
               hrow[row] = (int32_t)h;
               act[q] += (h > 0);
+              hq[q] = h;
+              part += h;
             }
           }
+          const uint32_t stot = __reduce_add_sync(0xffffffffu, part);
+#pragma unroll
+          for (int q = 0; q < MAXR; ++q) hvy[q] += is_heavy(hq[q], uE, stot);
           __syncwarp();
           ++t;
         }
@@ -220,6 +234,9 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
       // lane + 32q and reads them as 8 x 128-bit chunks, chunk (c+lane)&7 in
       // iteration c (4 wavefronts per LDS.128: conflict-free), zeroing as it goes.
       int32_t* hrow = hist + (l * HT + t) * E;
+      uint32_t hq[MAXR * BINS], part = 0;
+#pragma unroll
+      for (int q = 0; q < MAXR * BINS; ++q) hq[q] = 0;
 #pragma unroll
       for (int q = 0; q < MAXR; ++q) {
         const int row = lane + q * 32;
@@ -237,6 +254,8 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
             hrow[row] = (int32_t)s;
             csum[q] += s;
             act[q] += (s > 0);
+            hq[q] = s;
+            part += s;
           } else {
             const uint32_t lo = s & 0xffffu, hi = s >> 16;
             hrow[2 * row] = (int32_t)lo;  // two stores: with odd E the pair is not 8-byte aligned
@@ -245,6 +264,9 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
             csum[2 * q + 1] += hi;
             act[2 * q] += (lo > 0);
             act[2 * q + 1] += (hi > 0);
+            hq[2 * q] = lo;
+            hq[2 * q + 1] = hi;
+            part += lo + hi;
           }
         }
       }
@@ -254,19 +276,22 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
         const int orow = WIDE ? E : E / 2;
         const uint32_t ov = cnt[orow * 32 + lane];
         cnt[orow * 32 + lane] = 0;
+        uint32_t odd = 0;  // packed layout, odd E: bin E-1 sits alone in the overflow pair row
         if (WIDE || (E & 1) == 0) {
           dropped += ov;
         } else {
           dropped += ov >> 16;
-          uint32_t lo = ov & 0xffffu;
+          odd = __reduce_add_sync(0xffffffffu, ov & 0xffffu);
+        }
+        const uint32_t stot = __reduce_add_sync(0xffffffffu, part) + odd;
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) lo += __shfl_xor_sync(0xffffffffu, lo, o);
-          if (lane == 0) {
-            hrow[E - 1] = (int32_t)lo;
-            if (lo) {
-              atomicAdd((unsigned long long*)&colsum[l * E + E - 1], (unsigned long long)lo);
-              atomicAdd(&active[l * E + E - 1], 1);
-            }
+        for (int q = 0; q < MAXR * BINS; ++q) hvy[q] += is_heavy(hq[q], uE, stot);
+        if (!WIDE && (E & 1) && lane == 0) {
+          hrow[E - 1] = (int32_t)odd;
+          if (odd) {
+            atomicAdd((unsigned long long*)&colsum[l * E + E - 1], (unsigned long long)odd);
+            atomicAdd(&active[l * E + E - 1], 1);
+            if (is_heavy(odd, uE, stot)) atomicAdd(&heavy[l * E + E - 1], 1);
           }
         }
       }
@@ -280,9 +305,10 @@ topk_hist_kernel(const IdT* __restrict__ ids, int64_t L, int64_t N, int k, int B
 #pragma unroll
       for (int bb = 0; bb < BINS; ++bb) {
         const int bin = row * BINS + bb;
-        const uint32_t cs = csum[q * BINS + bb], ac = act[q * BINS + bb];
+        const uint32_t cs = csum[q * BINS + bb], ac = act[q * BINS + bb], hv = hvy[q * BINS + bb];
         if (cs) atomicAdd((unsigned long long*)&colsum[l * E + bin], (unsigned long long)cs);
         if (ac) atomicAdd(&active[l * E + bin], (int)ac);
+        if (hv) atomicAdd(&heavy[l * E + bin], (int)hv);
       }
     }
 #pragma unroll
@@ -323,7 +349,7 @@ template <bool WIDE, int MAXR>
 __global__ void __launch_bounds__(32)
 topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int k, int B, int E, int64_t T,
                       int64_t HT, int32_t* __restrict__ hist, int64_t* __restrict__ colsum,
-                      int32_t* __restrict__ active, int64_t* __restrict__ dropped_out) {
+                      int32_t* __restrict__ active, int32_t* __restrict__ heavy, int64_t* __restrict__ dropped_out) {
   extern __shared__ __align__(16) uint4 rsm[];
   constexpr int BATCH = kRingUnroll * 32;  // uint4 per warp batch (4 KB)
   const int lane = threadIdx.x;
@@ -357,9 +383,9 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
       if (sidx < nb) issue(sidx);
       ring_commit();
     }
-    uint32_t prev[MAXR * BINS], act[MAXR * BINS];
+    uint32_t prev[MAXR * BINS], act[MAXR * BINS], hvy[MAXR * BINS];
 #pragma unroll
-    for (int q = 0; q < MAXR * BINS; ++q) { prev[q] = 0; act[q] = 0; }
+    for (int q = 0; q < MAXR * BINS; ++q) { prev[q] = 0; act[q] = 0; hvy[q] = 0; }
     int in_step = 0;
     int64_t t = t_begin;
     for (int64_t bt = 0; bt < nb; ++bt) {
@@ -374,6 +400,9 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
         in_step = 0;
         __syncwarp();
         int32_t* hrow = hist + (l * HT + t) * E;
+        uint32_t hq[MAXR * BINS], part = 0;
+#pragma unroll
+        for (int q = 0; q < MAXR * BINS; ++q) hq[q] = 0;
 #pragma unroll
         for (int q = 0; q < MAXR; ++q) {
           const int row = lane + q * 32;
@@ -390,6 +419,8 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
               prev[q] = sum;
               hrow[row] = (int32_t)h;
               act[q] += (h > 0);
+              hq[q] = h;
+              part += h;
             } else {
               uint32_t lo = 0, hi = 0;
 #pragma unroll
@@ -404,9 +435,15 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
               *reinterpret_cast<int2*>(hrow + 2 * row) = make_int2((int)hl, (int)hh);
               act[2 * q] += (hl > 0);
               act[2 * q + 1] += (hh > 0);
+              hq[2 * q] = hl;
+              hq[2 * q + 1] = hh;
+              part += hl + hh;
             }
           }
         }
+        const uint32_t stot = __reduce_add_sync(0xffffffffu, part);
+#pragma unroll
+        for (int q = 0; q < MAXR * BINS; ++q) hvy[q] += is_heavy(hq[q], uE, stot);
         __syncwarp();
         ++t;
       }
@@ -424,9 +461,10 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
 #pragma unroll
       for (int bb = 0; bb < BINS; ++bb) {
         const int bin = row * BINS + bb;
-        const uint32_t cs = prev[q * BINS + bb], ac = act[q * BINS + bb];
+        const uint32_t cs = prev[q * BINS + bb], ac = act[q * BINS + bb], hv = hvy[q * BINS + bb];
         if (cs) atomicAdd((unsigned long long*)&colsum[l * E + bin], (unsigned long long)cs);
         if (ac) atomicAdd(&active[l * E + bin], (int)ac);
+        if (hv) atomicAdd(&heavy[l * E + bin], (int)hv);
       }
     }
 #pragma unroll
@@ -437,7 +475,7 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
 
 template <bool WIDE, int MAXR>
 static int launch_hist_ring(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
-                            int32_t* hist, int64_t* colsum, int32_t* active, int64_t* dropped, cudaStream_t st) {
+                            int32_t* hist, int64_t* colsum, int32_t* active, int32_t* heavy, int64_t* dropped, cudaStream_t st) {
   const int rows = WIDE ? E + 1 : E / 2 + 1;
   const size_t smem = (size_t)kRingStages * kRingUnroll * 32 * 16 + (size_t)rows * 32 * 4;
   auto kern = topk_hist_ring_kernel<WIDE, MAXR>;
@@ -451,7 +489,7 @@ static int launch_hist_ring(const void* ids, int64_t L, int64_t N, int k, int B,
   int64_t blocks = (int64_t)num_sms() * per_sm;
   if (blocks > units) blocks = units;
   kern<<<(unsigned)blocks, 32, smem, st>>>((const int16_t*)ids, L, N, k, B, E, T, HT, hist, colsum, active,
-                                           dropped);
+                                           heavy, dropped);
   GEM_CHECK_LAUNCH("topk_hist_ring_kernel");
   return GEM_OK;
 }
@@ -459,7 +497,7 @@ static int launch_hist_ring(const void* ids, int64_t L, int64_t N, int k, int B,
 template <typename IdT, bool WIDE, int MAXR>
 static int launch_hist_t(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
                          int32_t* hist,
-                         int64_t* colsum, int32_t* active, int64_t* dropped, cudaStream_t st) {
+                         int64_t* colsum, int32_t* active, int32_t* heavy, int64_t* dropped, cudaStream_t st) {
   const int rows = WIDE ? E + 1 : (E + 2) / 2;
   const size_t smem = (size_t)kHistWarps * rows * 32 * sizeof(uint32_t);
   auto kern = topk_hist_kernel<IdT, WIDE, MAXR>;
@@ -473,7 +511,7 @@ static int launch_hist_t(const void* ids, int64_t L, int64_t N, int k, int B, in
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
   kern<<<(unsigned)blocks, kHistWarps * 32, smem, st>>>((const IdT*)ids, L, N, k, B, E, T, HT, hist, colsum, active,
-                                                         dropped);
+                                                         heavy, dropped);
   GEM_CHECK_LAUNCH("topk_hist_kernel");
   return GEM_OK;
 }
@@ -481,7 +519,7 @@ static int launch_hist_t(const void* ids, int64_t L, int64_t N, int k, int B, in
 template <typename IdT>
 static int dispatch_hist(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
                          int32_t* hist,
-                         int64_t* colsum, int32_t* active, int64_t* dropped, cudaStream_t st) {
+                         int64_t* colsum, int32_t* active, int32_t* heavy, int64_t* dropped, cudaStream_t st) {
   // ring variant: int16 ids, every unit one whole-batch block (steps of whole
   // 2 KB batches, N a multiple of B, 16-byte aligned ids); wide counters up to
   // 160 experts, packed ones for even E up to 512
@@ -489,17 +527,17 @@ static int dispatch_hist(const void* ids, int64_t L, int64_t N, int k, int B, in
   if (sizeof(IdT) == 2 && N % B == 0 && step_bytes % (kRingUnroll * 32 * 16) == 0 &&
       (reinterpret_cast<uintptr_t>(ids) & 15) == 0 && (E <= kWideMaxE || E % 2 == 0) &&
       !std::getenv("GEM_HIST_NORING")) {
-    if (E <= 64) return launch_hist_ring<true, 2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
-    if (E <= 128) return launch_hist_ring<true, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
-    if (E <= kWideMaxE) return launch_hist_ring<true, 5>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
-    if (E <= 256) return launch_hist_ring<false, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
-    return launch_hist_ring<false, 8>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+    if (E <= 64) return launch_hist_ring<true, 2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
+    if (E <= 128) return launch_hist_ring<true, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
+    if (E <= kWideMaxE) return launch_hist_ring<true, 5>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
+    if (E <= 256) return launch_hist_ring<false, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
+    return launch_hist_ring<false, 8>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
   }
-  if (E <= 64) return launch_hist_t<IdT, true, 2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
-  if (E <= 128) return launch_hist_t<IdT, true, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
-  if (E <= kWideMaxE) return launch_hist_t<IdT, true, 5>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
-  if (E <= 256) return launch_hist_t<IdT, false, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
-  return launch_hist_t<IdT, false, 8>(ids, L, N, k, B, E, T, HT, hist, colsum, active, dropped, st);
+  if (E <= 64) return launch_hist_t<IdT, true, 2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
+  if (E <= 128) return launch_hist_t<IdT, true, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
+  if (E <= kWideMaxE) return launch_hist_t<IdT, true, 5>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
+  if (E <= 256) return launch_hist_t<IdT, false, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
+  return launch_hist_t<IdT, false, 8>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
 }
 
 }  // namespace gem
@@ -508,11 +546,11 @@ using namespace gem;
 
 static int topk_hist_rows(const char* who, const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k,
                           int32_t B, int32_t E, int32_t* hist, int64_t hist_rows, int64_t* colsum, int32_t* active,
-                          int64_t* dropped, void* stream) {
+                          int32_t* heavy, int64_t* dropped, void* stream) {
   GEM_REQUIRE(id_bytes == 2 || id_bytes == 4, "%s: id_bytes must be 2 or 4", who);
   GEM_REQUIRE(L >= 1 && N >= 1 && k >= 1 && B >= 1 && E >= 1 && E <= 512,
               "%s: bad shape L=%lld N=%lld k=%d B=%d E=%d (E <= 512)", who, (long long)L, (long long)N, k, B, E);
-  GEM_REQUIRE(ids && hist && colsum && active && dropped, "%s: null pointer", who);
+  GEM_REQUIRE(ids && hist && colsum && active && heavy && dropped, "%s: null pointer", who);
   // a lane's u32 (wide) or u16 (packed) counter must not wrap within one step
   GEM_REQUIRE(E <= kWideMaxE || (int64_t)B * k <= 65535, "%s: E > %d needs at most 65535 ids per step", who,
               kWideMaxE);
@@ -520,20 +558,20 @@ static int topk_hist_rows(const char* who, const void* ids, int32_t id_bytes, in
   GEM_REQUIRE(hist_rows >= T, "%s: %lld histogram rows per layer cannot hold %lld steps", who, (long long)hist_rows,
               (long long)T);
   cudaStream_t st = as_stream(stream);
-  if (id_bytes == 2) return dispatch_hist<int16_t>(ids, L, N, k, B, E, T, hist_rows, hist, colsum, active, dropped, st);
-  return dispatch_hist<int32_t>(ids, L, N, k, B, E, T, hist_rows, hist, colsum, active, dropped, st);
+  if (id_bytes == 2) return dispatch_hist<int16_t>(ids, L, N, k, B, E, T, hist_rows, hist, colsum, active, heavy, dropped, st);
+  return dispatch_hist<int32_t>(ids, L, N, k, B, E, T, hist_rows, hist, colsum, active, heavy, dropped, st);
 }
 
 extern "C" int gem_topk_hist(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k, int32_t B,
-                             int32_t E, int32_t* hist, int64_t* colsum, int32_t* active, int64_t* dropped,
-                             void* stream) {
+                             int32_t E, int32_t* hist, int64_t* colsum, int32_t* active, int32_t* heavy,
+                             int64_t* dropped, void* stream) {
   return topk_hist_rows("gem_topk_hist", ids, id_bytes, L, N, k, B, E, hist, (N + B - 1) / B, colsum, active,
-                        dropped, stream);
+                        heavy, dropped, stream);
 }
 
 extern "C" int gem_topk_hist_rows(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k, int32_t B,
                                   int32_t E, int32_t* hist, int64_t hist_rows, int64_t* colsum, int32_t* active,
-                                  int64_t* dropped, void* stream) {
+                                  int32_t* heavy, int64_t* dropped, void* stream) {
   return topk_hist_rows("gem_topk_hist_rows", ids, id_bytes, L, N, k, B, E, hist, hist_rows, colsum, active,
-                        dropped, stream);
+                        heavy, dropped, stream);
 }

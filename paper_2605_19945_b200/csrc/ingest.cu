@@ -107,21 +107,38 @@ __global__ void gen_topk_kernel(int64_t N, int k, int B, int E, const uint32_t* 
   }
 }
 
-// counts -> colsum / active (ExpertTrace path)
-__global__ void hist_colstats_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int64_t tchunk,
-                                     int64_t* __restrict__ colsum, int32_t* __restrict__ active) {
+// counts -> colsum / active / heavy (ExpertTrace path). heavy counts the
+// steps in which the expert got at least its fair share, h*E >= row total
+// (the same predicate K1 applies while it builds the rows).
+constexpr int kColstatsChunk = 256;
+
+__global__ void __launch_bounds__(256)
+hist_colstats_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int64_t* __restrict__ colsum,
+                     int32_t* __restrict__ active, int32_t* __restrict__ heavy) {
+  __shared__ int64_t rtot[kColstatsChunk];
   const int64_t l = blockIdx.y;
-  const int64_t t0 = (int64_t)blockIdx.x * tchunk, t1 = imin64(t0 + tchunk, T);
+  const int64_t t0 = (int64_t)blockIdx.x * kColstatsChunk, t1 = imin64(t0 + kColstatsChunk, T);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t t = t0 + warp; t < t1; t += blockDim.x >> 5) {
+    int64_t s = 0;
+    for (int e = lane; e < E; e += 32) s += hist[(l * T + t) * E + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) rtot[t - t0] = s;
+  }
+  __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int64_t s = 0;
-    int32_t a = 0;
+    int32_t a = 0, hv = 0;
     for (int64_t t = t0; t < t1; ++t) {
       const int32_t h = hist[(l * T + t) * E + e];
       s += h;
       a += (h > 0);
+      hv += (h > 0 && (int64_t)h * E >= rtot[t - t0]);
     }
     if (s) atomicAdd((unsigned long long*)&colsum[l * E + e], (unsigned long long)s);
     if (a) atomicAdd(&active[l * E + e], a);
+    if (hv) atomicAdd(&heavy[l * E + e], hv);
   }
 }
 
@@ -242,7 +259,7 @@ __global__ void stats_finalize_kernel(const int64_t* __restrict__ colsum, const 
   }
 }
 
-__global__ void classify_kernel(const int64_t* __restrict__ colsum, const int32_t* __restrict__ active,
+__global__ void classify_kernel(const int64_t* __restrict__ colsum, const int32_t* __restrict__ heavy,
                                 const int64_t* __restrict__ gram, int64_t T, int E, int64_t cons_num,
                                 int64_t cons_den, int64_t corr_num, int64_t corr_den,
                                 int8_t* __restrict__ cls, int16_t* __restrict__ group,
@@ -256,16 +273,22 @@ __global__ void classify_kernel(const int64_t* __restrict__ colsum, const int32_
   const int64_t l = blockIdx.x;
   const int64_t* cs = colsum + l * E;
   const int64_t* g = gram + l * (int64_t)E * E;
+  // consistent: heavy (>= fair share) in at least cons_num/cons_den of the
+  // steps; candidates for temporal: heavy in some step but not consistent
+  // (kClassBurst marks them until the correlation pass confirms them)
+  constexpr int8_t kClassBurst = 3;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    const int64_t a = active[l * E + e];
-    scls[e] = ((__int128)a * cons_den >= (__int128)cons_num * T) ? GEM_CLASS_CONSISTENT : GEM_CLASS_OTHER;
+    const int64_t hv = heavy[l * E + e];
+    scls[e] = ((__int128)hv * cons_den >= (__int128)cons_num * T) ? GEM_CLASS_CONSISTENT
+              : hv > 0                                           ? kClassBurst
+                                                                 : GEM_CLASS_OTHER;
   }
   for (int i = threadIdx.x; i < E * words; i += blockDim.x) adj[i] = 0;
   __syncthreads();
   const __int128 lim = (__int128)1 << 60;
   for (int64_t p = threadIdx.x; p < (int64_t)E * E; p += blockDim.x) {
     const int a = (int)(p / E), b = (int)(p % E);
-    if (b <= a || scls[a] == GEM_CLASS_CONSISTENT || scls[b] == GEM_CLASS_CONSISTENT) continue;
+    if (b <= a || scls[a] != kClassBurst || scls[b] != kClassBurst) continue;
     const __int128 sa = cs[a], sb = cs[b];
     const __int128 va = (__int128)T * gram_at(g, E, a, a) - sa * sa;
     const __int128 vb = (__int128)T * gram_at(g, E, b, b) - sb * sb;
@@ -285,7 +308,7 @@ __global__ void classify_kernel(const int64_t* __restrict__ colsum, const int32_
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     bool any = false;
     for (int w = 0; w < words; ++w) any |= adj[(size_t)e * words + w] != 0;
-    if (scls[e] != GEM_CLASS_CONSISTENT && any) scls[e] = GEM_CLASS_TEMPORAL;
+    if (scls[e] == kClassBurst) scls[e] = any ? GEM_CLASS_TEMPORAL : GEM_CLASS_OTHER;
     label[e] = scls[e] == GEM_CLASS_TEMPORAL ? e : -1;
   }
   __syncthreads();
@@ -349,11 +372,11 @@ extern "C" int gem_gen_topk(int64_t L, int64_t N, int32_t k, int32_t B, int32_t 
 }
 
 extern "C" int gem_hist_colstats(const int32_t* hist, int64_t L, int64_t T, int32_t E, int64_t* colsum,
-                                 int32_t* active, void* stream) {
-  GEM_REQUIRE(L >= 1 && T >= 1 && E >= 1 && hist && colsum && active, "gem_hist_colstats: bad arguments");
-  const int64_t tchunk = 256;
-  dim3 grid((unsigned)((T + tchunk - 1) / tchunk), (unsigned)L);
-  hist_colstats_kernel<<<grid, 256, 0, as_stream(stream)>>>(hist, T, E, tchunk, colsum, active);
+                                 int32_t* active, int32_t* heavy, void* stream) {
+  GEM_REQUIRE(L >= 1 && T >= 1 && E >= 1 && hist && colsum && active && heavy, "gem_hist_colstats: bad arguments");
+  GEM_REQUIRE(L <= 65535, "gem_hist_colstats: L too large");
+  dim3 grid((unsigned)((T + kColstatsChunk - 1) / kColstatsChunk), (unsigned)L);
+  hist_colstats_kernel<<<grid, 256, 0, as_stream(stream)>>>(hist, T, E, colsum, active, heavy);
   GEM_CHECK_LAUNCH("hist_colstats_kernel");
   return GEM_OK;
 }
@@ -404,10 +427,10 @@ extern "C" int gem_stats_finalize(const int64_t* colsum, const int32_t* active, 
   return GEM_OK;
 }
 
-extern "C" int gem_classify(const int64_t* colsum, const int32_t* active, const int64_t* gram, int64_t L, int64_t T,
+extern "C" int gem_classify(const int64_t* colsum, const int32_t* heavy, const int64_t* gram, int64_t L, int64_t T,
                             int32_t E, int64_t cons_num, int64_t cons_den, int64_t corr_num, int64_t corr_den,
                             int8_t* cls, int16_t* group, int32_t* err_flag, void* stream) {
-  GEM_REQUIRE(L >= 1 && T >= 1 && E >= 1 && E <= 1024 && colsum && active && gram && cls && group && err_flag,
+  GEM_REQUIRE(L >= 1 && T >= 1 && E >= 1 && E <= 1024 && colsum && heavy && gram && cls && group && err_flag,
               "gem_classify: bad arguments");
   GEM_REQUIRE(cons_den > 0 && cons_num >= 0 && corr_den > 0 && corr_num > 0 && corr_num <= corr_den &&
                   corr_den <= (1 << 20),
@@ -415,7 +438,8 @@ extern "C" int gem_classify(const int64_t* colsum, const int32_t* active, const 
   cudaStream_t st = as_stream(stream);
   const int words = (E + 31) / 32;
   const size_t smem = (size_t)E * words * 4 + (size_t)E * 4 + (size_t)E;
-  classify_kernel<<<(unsigned)L, 256, smem, st>>>(colsum, active, gram, T, E, cons_num, cons_den, corr_num, corr_den,
+  GEM_CHECK_CUDA(cudaFuncSetAttribute(classify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  classify_kernel<<<(unsigned)L, 256, smem, st>>>(colsum, heavy, gram, T, E, cons_num, cons_den, corr_num, corr_den,
                                                   cls, group, err_flag);
   GEM_CHECK_LAUNCH("classify_kernel");
   return GEM_OK;

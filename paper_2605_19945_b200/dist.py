@@ -2,22 +2,27 @@
 
 North-star subsystem (4). Each rank holds the router ids of a contiguous,
 step-aligned TOKEN range (what an EP serving rank observes: its own tokens,
-every layer). The only data-path exchanges are:
+every layer). The data-path exchanges are:
 
-  1. one all-reduce (SUM, int64/int32 — exact, order-free) of the per-expert
-     totals, active-step counts and the step co-activation Gram;
-  2. one all-to-all that routes histogram rows to the rank owning each layer
-     (layers are split into contiguous blocks), because a candidate score or a
-     search run is ONE serial fp64 chain over all steps of a layer and must
-     never be split (SURVEY.md §0 fact 4);
-  3. all-gathers of per-layer results (search outcome; per-layer candidate
-     scores), after which the multi-layer fp64 sums are taken serially in
-     ascending layer order on every rank.
+  1. ONE all-reduce (SUM over int64 words — exact, order-free) of the packed
+     statistics buffer (trace.DeviceStats.pack): per-expert totals, active and
+     heavy step counts, the step co-activation Gram and, when requested, the
+     token-level co-selection counts;
+  2. for the search: one all-to-all that routes histogram rows to the rank
+     owning each layer (layers split into contiguous blocks), because a search
+     run is ONE serial fp64 chain over all steps of a layer and must never be
+     split (SURVEY.md §0 fact 4); then an all-gather of the per-layer results;
+  3. for candidate scoring: candidates are split by INDEX (SURVEY.md §8e);
+     every rank needs all layers' full-length rows, so the histogram shards
+     are all-gathered once, each rank scores its candidate range on every
+     layer, and the fp64 scores (per layer and the serial layer sum, computed
+     on the rank that owns the candidate) are all-gathered.
 
 No floating-point arithmetic crosses ranks, so every result is bit-identical
 to the single-GPU one. The math is delegated to an `ops` object (DeviceOps for
 the B200 kernels); the CPU tests drive the same orchestration with the oracle
-over gloo.
+over gloo, and a two-process gloo test drives DeviceOps on one GPU (gloo
+collectives on CUDA tensors stage through host memory, see _collective).
 """
 
 from __future__ import annotations
@@ -47,20 +52,36 @@ class ShardPlan:
         lo = r * base + min(r, extra)
         return lo, lo + base + (1 if r < extra else 0)
 
+    def candidate_range(self, C: int, r: int | None = None) -> tuple[int, int]:
+        r = self.rank if r is None else r
+        base, extra = divmod(C, self.world)
+        lo = r * base + min(r, extra)
+        return lo, lo + base + (1 if r < extra else 0)
+
     @property
     def max_layers(self) -> int:
         return -(-self.num_layers // self.world)
 
 
-def _group_world(group):
-    return dist.get_world_size(group), dist.get_rank(group)
+def _staged(group) -> bool:
+    """gloo has no device path for every collective: stage CUDA tensors through host."""
+    return dist.get_backend(group) == "gloo"
 
 
-def allreduce_stats(colsum: torch.Tensor, active: torch.Tensor, gram: torch.Tensor | None, group=None) -> None:
-    """In-place exact SUM of the additive integer statistics."""
-    for t in (colsum, active, gram):
-        if t is not None:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+def _collective(fn, group, *tensors):
+    """Run fn(*tensors) on host copies when the backend needs them, copying results back."""
+    if not _staged(group) or not any(t.is_cuda for t in tensors):
+        fn(*tensors)
+        return
+    host = [t.cpu() for t in tensors]
+    fn(*host)
+    for t, h in zip(tensors, host):
+        t.copy_(h)
+
+
+def allreduce_stats(stats, group=None) -> None:
+    """In-place exact SUM of the packed additive integer statistics (ONE collective)."""
+    _collective(lambda t: dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group), group, stats.pack)
 
 
 def exchange_hist(hist_local: torch.Tensor, plan: ShardPlan, group=None) -> torch.Tensor:
@@ -73,8 +94,9 @@ def exchange_hist(hist_local: torch.Tensor, plan: ShardPlan, group=None) -> torc
     recv_steps = [plan.step_range(q)[1] - plan.step_range(q)[0] for q in range(world)]
     recv_sizes = [Lm * s * E for s in recv_steps]
     out = torch.empty(sum(recv_sizes), dtype=hist_local.dtype, device=hist_local.device)
-    dist.all_to_all_single(out, hist_local.contiguous().view(-1), output_split_sizes=recv_sizes,
-                           input_split_sizes=send_sizes, group=group)
+    src = hist_local.contiguous().view(-1)
+    _collective(lambda o, i: dist.all_to_all_single(o, i, output_split_sizes=recv_sizes, input_split_sizes=send_sizes,
+                                                    group=group), group, out, src)
     parts, off = [], 0
     for q in range(world):
         parts.append(out[off:off + recv_sizes[q]].view(Lm, recv_steps[q], E))
@@ -82,18 +104,34 @@ def exchange_hist(hist_local: torch.Tensor, plan: ShardPlan, group=None) -> torc
     return torch.cat(parts, dim=1).contiguous()
 
 
+def allgather_hist(hist_local: torch.Tensor, plan: ShardPlan, group=None) -> torch.Tensor:
+    """[L, T_local, E] token-range rows of every rank -> [L, T, E] on every rank."""
+    L, _, E = hist_local.shape
+    per = -(-plan.num_steps // plan.world)
+    pad = torch.zeros((L, per, E), dtype=hist_local.dtype, device=hist_local.device)
+    pad[:, :hist_local.shape[1]] = hist_local
+    bufs = [torch.empty_like(pad) for _ in range(plan.world)]
+    _collective(lambda *b: dist.all_gather(list(b[1:]), b[0], group=group), group, pad, *bufs)
+    parts = []
+    for q in range(plan.world):
+        a, b = plan.step_range(q)
+        parts.append(bufs[q][:, : b - a])
+    return torch.cat(parts, dim=1).contiguous()
+
+
+def _gather_rows(local: torch.Tensor, rows: int, counts: list[int], group=None) -> torch.Tensor:
+    """All-gather variable-length leading-dimension blocks (padded to `rows`) and concatenate in rank order."""
+    pad = torch.zeros((rows,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[:local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in counts]
+    _collective(lambda *b: dist.all_gather(list(b[1:]), b[0], group=group), group, pad, *bufs)
+    return torch.cat([bufs[q][:n] for q, n in enumerate(counts)], dim=0)
+
+
 def gather_layers(local: torch.Tensor, plan: ShardPlan, group=None) -> torch.Tensor:
     """Stack per-layer rows [L_owned, ...] of every rank into [L, ...] (layer order)."""
-    Lm = local.shape[0]
-    pad = torch.zeros((plan.max_layers,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    pad[:Lm] = local
-    bufs = [torch.empty_like(pad) for _ in range(plan.world)]
-    dist.all_gather(bufs, pad, group=group)
-    rows = []
-    for q in range(plan.world):
-        a, b = plan.layer_range(q)
-        rows.append(bufs[q][: b - a])
-    return torch.cat(rows, dim=0)
+    counts = [plan.layer_range(q)[1] - plan.layer_range(q)[0] for q in range(plan.world)]
+    return _gather_rows(local, plan.max_layers, counts, group)
 
 
 def gather_layer_columns(local: torch.Tensor, plan: ShardPlan, group=None) -> torch.Tensor:
@@ -108,19 +146,33 @@ def gather_layer_columns(local: torch.Tensor, plan: ShardPlan, group=None) -> to
 @dataclass
 class ShardedStats:
     hist_local: torch.Tensor   # [L, T_local, E] this rank's steps
-    colsum: torch.Tensor       # [L, E] global (after all-reduce)
-    active: torch.Tensor       # [L, E]
-    gram: torch.Tensor         # [L, E, E]
+    stats: object              # DeviceStats-like: global sums after the all-reduce (views of .pack)
     finalized: tuple           # ops.finalize(...) output (replicated)
+
+    @property
+    def colsum(self):
+        return self.stats.colsum
+
+    @property
+    def active(self):
+        return self.stats.active
+
+    @property
+    def heavy(self):
+        return self.stats.heavy
+
+    @property
+    def gram(self):
+        return self.stats.gram
 
 
 def sharded_statistics(ids_local, plan: ShardPlan, ops, tokens_per_step: int, num_experts: int,
                        group=None) -> ShardedStats:
-    hist, colsum, active = ops.topk_hist(ids_local, tokens_per_step, num_experts)
-    gram = ops.gram(hist, tokens_per_step * ids_local.shape[-1])  # every count <= B*k
-    allreduce_stats(colsum, active, gram, group)
-    fin = ops.finalize(colsum, active, gram, plan.num_steps)
-    return ShardedStats(hist, colsum, active, gram, fin)
+    hist, stats = ops.topk_hist(ids_local, tokens_per_step, num_experts, plan.num_steps)
+    ops.gram(hist, tokens_per_step * ids_local.shape[-1], stats)  # every count <= B*k
+    allreduce_stats(stats, group)
+    fin = ops.finalize(stats)
+    return ShardedStats(hist, stats, fin)
 
 
 @dataclass
@@ -132,7 +184,12 @@ class ShardedMapping:
 
 def sharded_search(hist_owned: torch.Tensor, plan: ShardPlan, ops, profile, config, nmax: int,
                    group=None) -> ShardedMapping:
-    asg, scores = ops.search(hist_owned, nmax, profile, config)  # [Lm, E] int64, [Lm] fp64
+    E = hist_owned.shape[2]
+    if hist_owned.shape[0]:
+        asg, scores = ops.search(hist_owned, nmax, profile, config)  # [Lm, E] int64, [Lm] fp64
+    else:  # more ranks than layers: this rank owns none
+        asg = torch.zeros((0, E), dtype=torch.int64, device=hist_owned.device)
+        scores = torch.zeros((0,), dtype=torch.float64, device=hist_owned.device)
     all_asg = gather_layers(asg, plan, group)
     all_scores = gather_layers(scores, plan, group)
     agg = 0.0
@@ -141,11 +198,34 @@ def sharded_search(hist_owned: torch.Tensor, plan: ShardPlan, ops, profile, conf
     return ShardedMapping(all_asg, all_scores, agg)
 
 
-def sharded_candidate_scores(hist_owned: torch.Tensor, plan: ShardPlan, ops, profile, cand: torch.Tensor,
+def sharded_candidate_scores(hist_full: torch.Tensor, plan: ShardPlan, ops, profile, cand: torch.Tensor,
                              nmax: int, group=None):
-    """cand [C, L, E] (replicated) -> (total [C] serial over layers, per-layer [C, L])."""
+    """Candidates split by index. hist_full [L, T, E] (allgather_hist), cand [C, L, E] (replicated)
+    -> (total [C] serial over layers, per-layer [C, L]), identical on every rank."""
+    C = cand.shape[0]
+    c0, c1 = plan.candidate_range(C)
+    L = hist_full.shape[0]
+    if c1 > c0:
+        per_layer = ops.score(hist_full, nmax, profile, cand[c0:c1].contiguous())  # [Cr, L] fp64
+        total = ops.layer_sum(per_layer)
+    else:
+        per_layer = torch.zeros((0, L), dtype=torch.float64, device=hist_full.device)
+        total = torch.zeros((0,), dtype=torch.float64, device=hist_full.device)
+    counts = [plan.candidate_range(C, q)[1] - plan.candidate_range(C, q)[0] for q in range(plan.world)]
+    rows = max(counts)
+    both = torch.cat([total.view(-1, 1), per_layer], dim=1)  # one all-gather for both
+    g = _gather_rows(both, rows, counts, group)
+    return g[:, 0].contiguous(), g[:, 1:].contiguous()
+
+
+def sharded_candidate_scores_by_layer(hist_owned: torch.Tensor, plan: ShardPlan, ops, profile, cand: torch.Tensor,
+                                      nmax: int, group=None):
+    """Alternative split by LAYER (no histogram all-gather; the max rank carries ceil(L/P) layers)."""
     l0, l1 = plan.layer_range()
-    local = ops.score(hist_owned, nmax, profile, cand[:, l0:l1].contiguous())  # [C, Lm] fp64
+    if l1 > l0:
+        local = ops.score(hist_owned, nmax, profile, cand[:, l0:l1].contiguous())  # [C, Lm] fp64
+    else:
+        local = torch.zeros((cand.shape[0], 0), dtype=torch.float64, device=cand.device)
     per_layer = gather_layer_columns(local, plan, group)
     return ops.layer_sum(per_layer), per_layer
 
@@ -153,23 +233,24 @@ def sharded_candidate_scores(hist_owned: torch.Tensor, plan: ShardPlan, ops, pro
 class DeviceOps:
     """The B200 kernels behind the sharded pipeline."""
 
-    def topk_hist(self, ids_local, B, E):
+    def topk_hist(self, ids_local, B, E, T_global):
         from .ingest import ids_to_histograms
 
         h = ids_to_histograms(ids_local, B, E, check_dropped=False)
-        return h.hist, h.colsum, h.active
+        h.stats.num_steps = T_global  # the statistics are completed by the all-reduce
+        return h.hist, h.stats
 
-    def gram(self, hist, max_count=-1):
+    def gram(self, hist, max_count, stats):
         from .ingest import step_coactivation
 
-        return step_coactivation(hist, max_count=max_count)
+        step_coactivation(hist, stats.gram, max_count=max_count)
 
-    def finalize(self, colsum, active, gram, T):
+    def finalize(self, stats):
         from .ingest import classify_device
-        from .trace import DeviceStats, finalize_stats
+        from .trace import finalize_stats
 
-        mu, af, corr = finalize_stats(DeviceStats(colsum, active, gram, T))
-        cls = classify_device(colsum, active, gram, T).check()
+        mu, af, corr = finalize_stats(stats)
+        cls = classify_device(stats.colsum, stats.heavy, stats.gram, stats.num_steps).check()
         return mu, af, corr, cls.cls, cls.group
 
     def search(self, hist_owned, nmax, profile, config):
@@ -180,10 +261,10 @@ class DeviceOps:
         scores = torch.tensor([r.best_score for r in res], dtype=torch.float64, device=hist_owned.device)
         return asg, scores
 
-    def score(self, hist_owned, nmax, profile, cand):
+    def score(self, hist, nmax, profile, cand):
         from .mapping import score_candidates_device
 
-        _, per_layer = score_candidates_device(hist_owned, nmax, profile, cand.to(torch.int8))
+        _, per_layer = score_candidates_device(hist, nmax, profile, cand.to(torch.int8))
         return per_layer
 
     def layer_sum(self, per_layer):

@@ -123,14 +123,29 @@ def generate_topk_ids(spec: TopkTraceSpec, dtype: torch.dtype = torch.int16, tok
 
 @dataclass
 class Histograms:
-    """Per-step expert histograms of a (shard of a) top-k trace, on the device."""
+    """Per-step expert histograms of a (shard of a) top-k trace, on the device.
+
+    The additive per-expert statistics live in `stats` (one int64 buffer for
+    colsum / active / heavy / Gram / co-selection: one all-reduce combines
+    token-range shards)."""
 
     hist: torch.Tensor      # [L, T, E] int32
-    colsum: torch.Tensor    # [L, E] int64  (accumulated; all-reduce across token shards)
-    active: torch.Tensor    # [L, E] int32
+    stats: DeviceStats      # colsum [L,E] int64, active/heavy [L,E] int32, gram, coselect (accumulated)
     dropped: torch.Tensor   # [L] int64 ids outside [0, E)
     tokens_per_step: int
     top_k: int = -1         # ids per token (bounds every count by tokens_per_step * top_k)
+
+    @property
+    def colsum(self) -> torch.Tensor:
+        return self.stats.colsum
+
+    @property
+    def active(self) -> torch.Tensor:
+        return self.stats.active
+
+    @property
+    def heavy(self) -> torch.Tensor:
+        return self.stats.heavy
 
     @property
     def max_count(self) -> int:
@@ -156,12 +171,15 @@ class Histograms:
 
 
 def ids_to_histograms(ids: torch.Tensor, tokens_per_step: int, num_experts: int,
-                      hist: torch.Tensor | None = None, check_dropped: bool = True) -> Histograms:
+                      hist: torch.Tensor | None = None, check_dropped: bool = True,
+                      with_gram: bool = True, with_coselect: bool = False) -> Histograms:
     """K1: top-k ids [L, N, k] (int16/int32, device) -> per-step histograms.
 
     Steps are consecutive blocks of `tokens_per_step` tokens (the last may be
     short). Ids outside [0, num_experts) are counted in `dropped`; with
-    check_dropped (default) any dropped id raises ValidationError."""
+    check_dropped (default) any dropped id raises ValidationError (this
+    synchronises). with_gram / with_coselect reserve the Gram and the
+    co-selection counts in the same statistics buffer (filled by K2 / K2b)."""
     if ids.dim() != 3:
         raise ValidationError(f"ids must be [layers, tokens, k], got shape {tuple(ids.shape)}")
     if ids.dtype not in (torch.int16, torch.int32):
@@ -173,12 +191,11 @@ def ids_to_histograms(ids: torch.Tensor, tokens_per_step: int, num_experts: int,
     T = -(-N // tokens_per_step)
     if hist is None:
         hist = _device.empty((L, T, num_experts), torch.int32)
-    colsum = _device.zeros((L, num_experts), torch.int64)
-    active = _device.zeros((L, num_experts), torch.int32)
+    ds = DeviceStats.allocate(L, num_experts, T, with_gram=with_gram, with_coselect=with_coselect)
     dropped = _device.zeros((L,), torch.int64)
     _lib.call("gem_topk_hist", ptr(ids), ids.element_size(), L, N, k, tokens_per_step, num_experts, ptr(hist),
-              ptr(colsum), ptr(active), ptr(dropped), stream())
-    h = Histograms(hist, colsum, active, dropped, tokens_per_step, k)
+              ptr(ds.colsum), ptr(ds.active), ptr(ds.heavy), ptr(dropped), stream())
+    h = Histograms(hist, ds, dropped, tokens_per_step, k)
     if check_dropped and int(dropped.sum().item()):
         raise ValidationError(f"{int(dropped.sum().item())} expert ids outside [0, {num_experts})")
     return h
@@ -215,23 +232,32 @@ class ExpertClasses:
 
 @dataclass(frozen=True)
 class ClassifyConfig:
-    """consistent: active in >= consistent_fraction of steps (paper: ~85%, PAPER.md:261-272);
-    temporal: not consistent and Pearson r >= correlation_threshold with another
-    non-consistent expert (correlated temporal experts, r=0.88 in PAPER.md Fig. 8).
-    Thresholds are exact rationals (num, den) so the predicate is integer-exact."""
+    """The paper's split of the heavily used experts:
+
+    * a step is *heavy* for expert e when e receives at least its fair share of
+      the step's routed ids, h_t[e] * E >= sum_e' h_t[e'] (and h_t[e] > 0);
+    * consistent: heavy in >= consistent_fraction of the steps ("used in almost
+      every time step"; planted consistent experts are on in ~85% of steps);
+    * temporal: not consistent, heavy in at least one step, and Pearson
+      r >= correlation_threshold with another such expert (correlated temporal
+      experts, r = 0.88 in PAPER.md Fig. 8); groups are the connected
+      components of that graph, labelled by their lowest expert index;
+    * everything else (light experts) is CLASS_OTHER.
+
+    Thresholds are exact rationals (num, den) so every predicate is integer-exact."""
 
     consistent_fraction: tuple[int, int] = (4, 5)
     correlation_threshold: tuple[int, int] = (4, 5)
 
 
-def classify_device(colsum, active, gram, num_steps: int, config: ClassifyConfig = ClassifyConfig()) -> ExpertClasses:
+def classify_device(colsum, heavy, gram, num_steps: int, config: ClassifyConfig = ClassifyConfig()) -> ExpertClasses:
     L, E = colsum.shape
     cls = _device.empty((L, E), torch.int8)
     grp = _device.empty((L, E), torch.int16)
     cn, cd = config.consistent_fraction
     rn, rd = config.correlation_threshold
     err = _device.zeros((1,), torch.int32)
-    _lib.call("gem_classify", ptr(colsum), ptr(active), ptr(gram), L, num_steps, E, cn, cd, rn, rd, ptr(cls),
+    _lib.call("gem_classify", ptr(colsum), ptr(heavy), ptr(gram), L, num_steps, E, cn, cd, rn, rd, ptr(cls),
               ptr(grp), ptr(err), stream())
     return ExpertClasses(cls, grp, err)
 
@@ -267,10 +293,24 @@ def trace_statistics(ids: torch.Tensor, tokens_per_step: int, num_experts: int, 
     return statistics_from_histograms(h, correlation=correlation, classify=classify, config=config)
 
 
+def finalize_statistics(h: Histograms, correlation: bool = True, classify: bool = True,
+                        config: ClassifyConfig = ClassifyConfig()) -> TraceStatistics:
+    """K3 + K3b over statistics whose sums are complete (e.g. after the all-reduce)."""
+    ds = h.stats
+    mu, af, corr = finalize_stats(ds, with_corr=correlation)
+    classes = classify_device(ds.colsum, ds.heavy, ds.gram, ds.num_steps, config) if classify else None
+    return TraceStatistics(h, ds.gram, mu, af, corr, classes)
+
+
 def statistics_from_histograms(h: Histograms, correlation: bool = True, classify: bool = True,
                                config: ClassifyConfig = ClassifyConfig()) -> TraceStatistics:
-    gram = step_coactivation(h.hist, max_count=h.max_count)
-    ds = DeviceStats(h.colsum, h.active, gram, h.num_steps)
-    mu, af, corr = finalize_stats(ds, with_corr=correlation)
-    classes = classify_device(h.colsum, h.active, gram, h.num_steps, config) if classify else None
-    return TraceStatistics(h, gram, mu, af, corr, classes)
+    compute_gram(h)
+    return finalize_statistics(h, correlation=correlation, classify=classify, config=config)
+
+
+def compute_gram(h: Histograms) -> torch.Tensor:
+    """K2 into the statistics buffer (allocating the Gram there if it has none)."""
+    ds = h.stats
+    if ds.gram is None:
+        ds.gram = _device.zeros((h.num_layers, h.num_experts, h.num_experts), torch.int64)
+    return step_coactivation(h.hist, ds.gram, max_count=h.max_count)

@@ -212,12 +212,13 @@ def stream_histograms(dump: RouterDump | str | os.PathLike, device: int | None =
     Chunks are read by a host thread into `buffers` pinned buffers, copied
     host->device on a copy stream and ingested by gem_topk_hist_rows on the
     compute stream into one [L, T, E] histogram (rows of chunk c at its step
-    offset); colsum/active/dropped accumulate across chunks. Copy of chunk
+    offset); colsum/active/heavy/dropped accumulate across chunks. Copy of chunk
     c+1 overlaps the ingestion of chunk c. Returns ingest.Histograms."""
     import torch
 
     from . import _device, _lib
     from .ingest import Histograms
+    from .trace import DeviceStats
 
     d = dump if isinstance(dump, RouterDump) else RouterDump(dump)
     h = d.header
@@ -229,8 +230,8 @@ def stream_histograms(dump: RouterDump | str | os.PathLike, device: int | None =
     torch_dtype = torch.int16 if h.id_bytes == 2 else torch.int32
     L, T, E, k = h.num_layers, h.num_steps, h.num_experts, h.top_k
     hist = torch.empty((L, T, E), dtype=torch.int32, device=dev)
-    colsum = torch.zeros((L, E), dtype=torch.int64, device=dev)
-    active = torch.zeros((L, E), dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        ds = DeviceStats.allocate(L, E, T)
     dropped = torch.zeros((L,), dtype=torch.int64, device=dev)
     nb = max(2, buffers)
     chunk_ids = L * h.chunk_tokens * k
@@ -281,8 +282,8 @@ def stream_histograms(dump: RouterDump | str | os.PathLike, device: int | None =
         compute.wait_event(done_copy[j])
         s0 = t0 // h.tokens_per_step
         _lib.call("gem_topk_hist_rows", devb[j].data_ptr(), h.id_bytes, L, t1 - t0, k, h.tokens_per_step, E,
-                  hist.data_ptr() + s0 * E * 4, T, colsum.data_ptr(), active.data_ptr(), dropped.data_ptr(),
-                  compute.cuda_stream)
+                  hist.data_ptr() + s0 * E * 4, T, ds.colsum.data_ptr(), ds.active.data_ptr(), ds.heavy.data_ptr(),
+                  dropped.data_ptr(), compute.cuda_stream)
         done_use[j].record(compute)
         # the reader refills pinned buffer i once its copy has finished (chunk
         # c's ingestion and chunk c+1's copy proceed meanwhile)
@@ -291,7 +292,7 @@ def stream_histograms(dump: RouterDump | str | os.PathLike, device: int | None =
     th.join()
     if err:
         raise err[0]
-    out = Histograms(hist, colsum, active, dropped, h.tokens_per_step, k)
+    out = Histograms(hist, ds, dropped, h.tokens_per_step, k)
     if check_dropped and int(dropped.sum().item()):
         raise ValidationError(f"{int(dropped.sum().item())} expert ids outside [0, {E})")
     return out

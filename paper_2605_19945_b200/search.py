@@ -223,13 +223,19 @@ class RunResults:
         return RestartRecord(provenance, traj[0], finals[r], s, traj)
 
 
+TRAJ_INITIAL_WIDTH = 256  # trajectory columns allocated up front (runs measured: <= 16 swaps at C4)
+
+
 def run_search_device(hist: torch.Tensor, nmax: int, profile: VariabilityProfile, batch: RunBatch,
                       threshold: float, swap_cap: int) -> RunResults:
     """Run greedy + refinement for every run of `batch` on the device."""
     L, T, E = hist.shape
     G = profile.num_gpus
     if G > 32:
-        raise ValidationError("the device search supports at most 32 GPUs per mapping")
+        # known gap vs the reference (search.py:98-131 takes any G): the device
+        # search keeps per-run GPU sets in 32-bit masks (DESIGN.md §9)
+        raise ValidationError(f"the device search supports at most 32 GPUs per mapping, got {G} "
+                              "(known gap vs the reference search; scoring and replay accept any G)")
     _check_divisible(E, G)
     R = len(batch.provenance)
     dc = _device.DeviceCurves.from_profile(profile)
@@ -243,17 +249,26 @@ def run_search_device(hist: torch.Tensor, nmax: int, profile: VariabilityProfile
         _lib.call("gem_restart_order", ptr(keys), R, E, ptr(order), stream())
     else:
         order = _device.upload(batch.order, torch.int16)
-    assign = _device.upload(batch.assign, torch.int8)
-    traj = _device.zeros((R, traj_cap), torch.float64)
+    assign0 = _device.upload(batch.assign, torch.int8)
     swaps = _device.zeros((R,), torch.int32)
     final = _device.empty((R,), torch.float64)
     ws_bytes = int(_lib.lib().gem_search_workspace_bytes(R, T, E, G))
     ws = _device.empty((max(ws_bytes, 1),), torch.uint8)
-    _lib.call("gem_search_runs", ptr(hist), L, T, E, G, ptr(lut), dc.lut_nmax, R, ptr(run_layer), ptr(needs),
-              ptr(order), ptr(assign), float(threshold), int(swap_cap), int(traj_cap), ptr(traj), ptr(swaps),
-              ptr(final), ptr(ws), ws_bytes, stream())
-    swaps_h = _device.host(swaps)
-    width = int(swaps_h.max(initial=0)) + 1  # only the used trajectory columns cross PCIe
+    # swap_cap only bounds the loop (search.py:56-59, possibly "unlimited"); the
+    # trajectory buffer starts at a bounded width and, in the rare case a run
+    # outgrows it, the (deterministic) search is repeated at the exact width
+    width_cap = min(traj_cap, TRAJ_INITIAL_WIDTH)
+    while True:
+        assign = assign0.clone()
+        traj = _device.zeros((R, width_cap), torch.float64)
+        _lib.call("gem_search_runs", ptr(hist), L, T, E, G, ptr(lut), dc.lut_nmax, R, ptr(run_layer), ptr(needs),
+                  ptr(order), ptr(assign), float(threshold), int(swap_cap), int(width_cap), ptr(traj), ptr(swaps),
+                  ptr(final), ptr(ws), ws_bytes, stream())
+        swaps_h = _device.host(swaps)
+        width = int(swaps_h.max(initial=0)) + 1  # only the used trajectory columns cross PCIe
+        if width <= width_cap:
+            break
+        width_cap = width
     return RunResults(_device.host(assign).astype(np.int64), _device.host(final), swaps_h,
                       _device.host(traj[:, :width].contiguous()))
 
@@ -315,14 +330,20 @@ def search_layers(traces, profile: VariabilityProfile, config: SearchConfig | No
     traces = list(traces)
     if not traces:
         return []
-    T, E = traces[0].tokens.shape
     for tr in traces:
-        if tr.tokens.shape != (T, E):
-            raise ValidationError("search_layers: all layers must share (num_steps, num_experts)")
-    _check_divisible(E, profile.num_gpus)
-    stacked = np.stack([tr.tokens for tr in traces])
-    hist, nmax = _device.counts_to_device_int32(stacked)
-    return search_hist(hist, nmax, profile, config)
+        _check_divisible(tr.num_experts, profile.num_gpus)
+    # layers of equal (num_steps, num_experts) share one batched device job;
+    # mixed shapes (e.g. CSV layers whose last step is all zeros) form several
+    groups: dict[tuple[int, int], list[int]] = {}
+    for i, tr in enumerate(traces):
+        groups.setdefault(tr.tokens.shape, []).append(i)
+    out: list[SearchResult | None] = [None] * len(traces)
+    for members in groups.values():
+        stacked = np.stack([traces[i].tokens for i in members])
+        hist, nmax = _device.counts_to_device_int32(stacked)
+        for i, res in zip(members, search_hist(hist, nmax, profile, config)):
+            out[i] = res
+    return out
 
 
 def search_hist(hist: torch.Tensor, nmax: int, profile: VariabilityProfile, config: SearchConfig,

@@ -39,6 +39,12 @@ INPUTS = [
                 "--output", "inputs/layers/layer1.json", "--quiet"]),
     ("layer2", ["gen-trace", "--experts", "16", "--steps", "20", "--seed", "23", "--format", "csv",
                 "--output", "inputs/layers/layer2.csv", "--quiet"]),
+    ("mixed0", ["gen-trace", "--experts", "16", "--steps", "20", "--seed", "31",
+                "--output", "inputs/mixed/m0.json", "--quiet"]),
+    ("mixed1", ["gen-trace", "--experts", "16", "--steps", "19", "--temporal", "1,2", "--seed", "32",
+                "--output", "inputs/mixed/m1.json", "--quiet"]),
+    ("mixed2", ["gen-trace", "--experts", "8", "--steps", "20", "--seed", "33", "--format", "csv",
+                "--output", "inputs/mixed/m2.csv", "--quiet"]),
     ("profile4", ["gen-profile", "--gpus", "4", "--setup", "moderate", "--seed", "5", "--max-tokens", "2048",
                   "--output", "inputs/profile4.json", "--quiet"]),
     ("profile2", ["gen-profile", "--gpus", "2", "--setup", "high", "--tile", "32", "--max-tokens", "1024",
@@ -73,6 +79,9 @@ CASES = [
     ("multi_layer", ["multi-layer", "--trace-dir", "inputs/layers", "--profile", "inputs/profile4.json",
                      "--output-dir", "out/ml", "--seed", "13", "--restarts", "5"],
      ["out/ml/layer0.mapping.json", "out/ml/layer1.mapping.json", "out/ml/layer2.mapping.json"]),
+    ("multi_layer_mixed", ["multi-layer", "--trace-dir", "inputs/mixed", "--profile", "inputs/profile4.json",
+                           "--output-dir", "out/mx", "--seed", "17", "--restarts", "4"],
+     ["out/mx/m0.mapping.json", "out/mx/m1.mapping.json", "out/mx/m2.mapping.json"]),
     ("bad_gpus", ["baseline", "linear", "--trace", "inputs/trace_a.json", "--gpus", "3"], []),
     ("missing_trace", ["stats", "--trace", "inputs/nope.json"], []),
 ]
@@ -87,6 +96,7 @@ def main() -> None:
     assert (REF / "gemap").is_dir(), "build the reference first: bash oracle/build_ref.sh"
     shutil.rmtree(CLI, ignore_errors=True)
     (CLI / "inputs" / "layers").mkdir(parents=True)
+    (CLI / "inputs" / "mixed").mkdir(parents=True)
     for name, args in INPUTS:
         p = run_ref(args, CLI)
         assert p.returncode == 0, (name, p.stderr)

@@ -15,11 +15,14 @@ import torch.multiprocessing as mp
 
 from paper_2605_19945_b200.dist import (
     ShardPlan,
+    allgather_hist,
     exchange_hist,
     sharded_candidate_scores,
+    sharded_candidate_scores_by_layer,
     sharded_search,
     sharded_statistics,
 )
+from paper_2605_19945_b200.trace import DeviceStats
 
 L, T, B, K, E, G, C = 5, 24, 32, 4, 16, 4, 12
 WEIGHT_SEED, GEN_SEED = 3, 17
@@ -53,18 +56,22 @@ class OracleOps:
         self.o = oracle
         self.curves = curves
 
-    def topk_hist(self, ids_local, B, E):
+    def topk_hist(self, ids_local, B, E, T_global):
         hist, _ = self.o.topk_hist(ids_local.numpy(), B, E)
-        h = torch.from_numpy(hist.astype(np.int32))
-        return h, torch.from_numpy(hist.sum(axis=1)), torch.from_numpy((hist > 0).sum(axis=1).astype(np.int32))
+        st = DeviceStats.allocate(hist.shape[0], E, T_global, device=torch.device("cpu"))
+        for l in range(hist.shape[0]):
+            cs, ac, hv = self.o.colstats3(hist[l])
+            st.colsum[l], st.active[l], st.heavy[l] = torch.from_numpy(cs), torch.from_numpy(ac), torch.from_numpy(hv)
+        return torch.from_numpy(hist.astype(np.int32)), st
 
-    def gram(self, hist, max_count=-1):
-        return torch.from_numpy(np.stack([self.o.gram(h.numpy()) for h in hist]))
+    def gram(self, hist, max_count, stats):
+        stats.gram.copy_(torch.from_numpy(np.stack([self.o.gram(h.numpy()) for h in hist])))
 
-    def finalize(self, colsum, active, gram, T):
-        cs, ac, gr = colsum.numpy(), active.numpy().astype(np.int64), gram.numpy()
+    def finalize(self, st):
+        cs, ac, hv, gr, T = st.colsum.numpy(), st.active.numpy().astype(np.int64), st.heavy.numpy(), \
+            st.gram.numpy(), st.num_steps
         mu = np.stack([c / int(c.sum()) for c in cs])
-        classes = [self.o.classify_from_stats(cs[l], ac[l], gr[l], T) for l in range(cs.shape[0])]
+        classes = [self.o.classify_from_stats(cs[l], hv[l], gr[l], T) for l in range(cs.shape[0])]
         return mu, ac / T, np.stack([c for c, _ in classes]), np.stack([g for _, g in classes])
 
     def search(self, hist_owned, nmax, profile, config):
@@ -93,15 +100,18 @@ def _worker(rank, world, port, out_path):
         ops = OracleOps(_curves())
         st = sharded_statistics(torch.from_numpy(ids[:, t0 * B:t1 * B].copy()), plan, ops, B, E)
         owned = exchange_hist(st.hist_local, plan)
+        full = allgather_hist(st.hist_local, plan)
         cfg = {"restarts": 3, "seed": 5}
         mp_res = sharded_search(owned, plan, ops, None, cfg, B * K)
-        total, per_layer = sharded_candidate_scores(owned, plan, ops, None, torch.from_numpy(cand), B * K)
+        total, per_layer = sharded_candidate_scores(full, plan, ops, None, torch.from_numpy(cand), B * K)
+        total2, per_layer2 = sharded_candidate_scores_by_layer(owned, plan, ops, None, torch.from_numpy(cand), B * K)
+        assert torch.equal(total, total2) and torch.equal(per_layer, per_layer2)
         if rank == 0:
             mu, af, cls, grp = st.finalized
-            np.savez(out_path, colsum=st.colsum.numpy(), active=st.active.numpy(), gram=st.gram.numpy(),
-                     mu=mu, af=af, cls=cls, grp=grp, owned=owned.numpy(), asg=mp_res.assignments.numpy(),
-                     scores=mp_res.scores.numpy(), agg=np.array([mp_res.aggregate]), total=total.numpy(),
-                     per_layer=per_layer.numpy())
+            np.savez(out_path, colsum=st.colsum.numpy(), active=st.active.numpy(), heavy=st.heavy.numpy(),
+                     gram=st.gram.numpy(), mu=mu, af=af, cls=cls, grp=grp, owned=owned.numpy(), full=full.numpy(),
+                     asg=mp_res.assignments.numpy(), scores=mp_res.scores.numpy(), agg=np.array([mp_res.aggregate]),
+                     total=total.numpy(), per_layer=per_layer.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -126,9 +136,10 @@ def test_shard_plan_covers_everything():
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 6])
 def test_gloo_pipeline_matches_single_process(tmp_path, oracle, world):
-    """world 3 and 4 split the 5 layers and 24 steps unevenly (2/2/1, 2/1/1/1)."""
+    """world 3 and 4 split the 5 layers and 24 steps unevenly (2/2/1, 2/1/1/1);
+    world 6 leaves one rank without a layer and splits 12 candidates 2 each."""
     out = tmp_path / "rank0.npz"
     mp.spawn(_worker, args=(world, _free_port(), str(out)), nprocs=world, join=True)
     got = np.load(out)
@@ -138,8 +149,10 @@ def test_gloo_pipeline_matches_single_process(tmp_path, oracle, world):
     # statistics: exact integers, bit-exact floats
     l0, l1 = ShardPlan(world, 0, L, T).layer_range()
     assert np.array_equal(got["owned"], hist[l0:l1])  # the layers rank 0 owns
+    assert np.array_equal(got["full"], hist)
     assert np.array_equal(got["colsum"], hist.sum(axis=1))
     assert np.array_equal(got["active"], (hist > 0).sum(axis=1))
+    assert np.array_equal(got["heavy"], np.stack([oracle.heavy_counts(h) for h in hist]))
     for l in range(L):
         assert np.array_equal(got["gram"][l], oracle.gram(hist[l]))
         mu, af, _ = oracle.stats(hist[l])

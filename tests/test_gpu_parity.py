@@ -50,6 +50,7 @@ def test_topk_hist_random_ids(oracle, dtype, shape):
     assert np.array_equal(h.dropped.cpu().numpy(), dropped)
     assert np.array_equal(h.colsum.cpu().numpy(), want.sum(axis=1))
     assert np.array_equal(h.active.cpu().numpy(), (want > 0).sum(axis=1))
+    assert np.array_equal(h.heavy.cpu().numpy(), np.stack([oracle.heavy_counts(w) for w in want]))
 
 
 @pytest.mark.parametrize("shape", [(2, 64 * 1024, 8, 1024, 128), (1, 37 * 512, 8, 512, 100), (3, 33 * 256, 4, 256, 64),
@@ -68,6 +69,7 @@ def test_topk_hist_ring_path(oracle, shape):
     assert np.array_equal(h.dropped.cpu().numpy(), dropped)
     assert np.array_equal(h.colsum.cpu().numpy(), want.sum(axis=1))
     assert np.array_equal(h.active.cpu().numpy(), (want > 0).sum(axis=1))
+    assert np.array_equal(h.heavy.cpu().numpy(), np.stack([oracle.heavy_counts(w) for w in want]))
 
 
 def test_topk_hist_unaligned_view(oracle):
@@ -170,19 +172,53 @@ def test_step_gram_accumulates_and_dispatches():
     assert _lib.lib().gem_step_gram_path(256, 8192) == 1
 
 
-def test_planted_groups_recovered():
-    spec = ingest.TopkTraceSpec(num_layers=2, num_tokens=400 * 1024, top_k=8, num_experts=128, seed=3)
-    st = ingest.trace_statistics(ingest.generate_topk_ids(spec), 1024, 128)
+@pytest.mark.parametrize("E,steps", [(128, 400), (256, 300), (64, 400)])
+def test_planted_groups_recovered(oracle, E, steps):
+    """Recall AND precision of the classifier on the benchmark generator:
+    temporal == exactly the planted groups (one group each, lowest-index
+    label); every planted consistent expert is consistent; every expert called
+    consistent is genuinely heavy (>= its fair share 1/E of the routed ids) and
+    heavy in >= 80% of steps; light background experts are CLASS_OTHER."""
+    spec = ingest.TopkTraceSpec(num_layers=2, num_tokens=steps * 1024, top_k=8, num_experts=E, seed=3)
+    st = ingest.trace_statistics(ingest.generate_topk_ids(spec), 1024, E)
     _, role = ingest.planted_layout(spec)
+    hist = st.hist.hist.cpu().numpy().astype(np.int64)
     for l in range(2):
         cls = st.classes.cls[l].cpu().numpy()
         grp = st.classes.group[l].cpu().numpy()
+        want_cls, want_grp = oracle.classify(hist[l])
+        assert np.array_equal(cls, want_cls) and np.array_equal(grp, want_grp)
+        planted_t = set(np.flatnonzero(role[l] >= 2).tolist())
+        assert set(np.flatnonzero(cls == ingest.CLASS_TEMPORAL).tolist()) == planted_t
         for g in range(spec.num_groups):
             members = np.flatnonzero(role[l] == 2 + g)
-            assert all(cls[m] == ingest.CLASS_TEMPORAL for m in members)
             assert len({int(grp[m]) for m in members}) == 1 and grp[members[0]] == members.min()
         for e in np.flatnonzero(role[l] == 1):
             assert cls[e] == ingest.CLASS_CONSISTENT
+        mu = st.mean_utilization[l].cpu().numpy()
+        heavy = st.hist.heavy[l].cpu().numpy()
+        cons = np.flatnonzero(cls == ingest.CLASS_CONSISTENT)
+        assert (mu[cons] * E >= 0.9).all() and (heavy[cons] * 5 >= 4 * steps).all()
+        light = np.flatnonzero((role[l] == 0) & (mu * E < 0.5))
+        assert len(light) > E // 4 and (cls[light] == ingest.CLASS_OTHER).all()
+        assert len(cons) < E // 4  # not the round-1 degenerate "almost everyone is consistent"
+
+
+def test_device_stats_heavy_from_counts(oracle):
+    """gem_hist_colstats (the ExpertTrace path) produces the same active/heavy counts as K1 / the oracle."""
+    from paper_2605_19945_b200.trace import device_stats
+
+    rng = np.random.default_rng(4)
+    h = rng.integers(0, 40, (3, 700, 37)).astype(np.int32)
+    h[:, ::5, :] = 0       # empty steps are heavy for nobody
+    h[1, 3, :] = 0
+    h[1, 3, 7] = 9
+    ds = device_stats(torch.from_numpy(h).cuda(), with_gram=False)
+    for l in range(3):
+        cs, ac, hv = oracle.colstats3(h[l].astype(np.int64))
+        assert np.array_equal(ds.colsum[l].cpu().numpy(), cs)
+        assert np.array_equal(ds.active[l].cpu().numpy(), ac)
+        assert np.array_equal(ds.heavy[l].cpu().numpy(), hv)
 
 
 def test_compute_stats_golden():

@@ -85,7 +85,7 @@ def test_stream_statistics_equals_in_memory(tmp_path, id_bytes, N, S):
     got = rd.stream_statistics(path)
     want = ingest.trace_statistics(torch.from_numpy(ids).cuda(), B, E)
     torch.cuda.synchronize()
-    for name in ("hist", "colsum", "active", "dropped"):
+    for name in ("hist", "colsum", "active", "heavy", "dropped"):
         assert torch.equal(getattr(got.hist, name), getattr(want.hist, name)), name
     assert torch.equal(got.gram, want.gram)
     assert torch.equal(got.mean_utilization, want.mean_utilization)
