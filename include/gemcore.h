@@ -140,6 +140,25 @@ int gem_step_gram_cc(const int32_t* hist, int64_t L, int64_t T, int32_t E, int64
 int gem_step_gram_tc(const int32_t* hist, int64_t L, int64_t T, int32_t E, int64_t* gram,
                      void* stream);
 
+/* --- K2b: token-level co-selection counts (north-star (1); no reference
+ * counterpart -- its only co-activation statistic is the step-level Pearson of
+ * trace.py:100-113, fed by K2) ---------------------------------------------
+ * cosel[l][a][b] += #tokens of layer l whose top-k ids contain both a and b
+ * (OᵀO of the 0/1 selection indicator; ids outside [0,E) ignored, a repeated
+ * id within a token counts once). int32 [L,E,E], full symmetric matrix,
+ * ACCUMULATED (zero it first); diag == K1's colsum when ids are distinct.
+ * ids [L,N,k] int16/int32 as for gem_topk_hist. gem_coselect runs the tcgen05
+ * kind::i8 kernel when gem_coselect_path() == 1 (E <= 256, k*id_bytes <= 32,
+ * 16-byte aligned ids with N*k*id_bytes % 16 == 0), else the CUDA-core
+ * scatter kernel; both are exact and agree bit for bit. */
+int gem_coselect(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k, int32_t E,
+                 int32_t* cosel, void* stream);
+int gem_coselect_path(const void* ids, int32_t id_bytes, int64_t N, int32_t k, int32_t E);
+int gem_coselect_tc(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k, int32_t E,
+                    int32_t* cosel, void* stream);
+int gem_coselect_scatter(const void* ids, int32_t id_bytes, int64_t L, int64_t N, int32_t k,
+                         int32_t E, int32_t* cosel, void* stream);
+
 /* --- K3: statistics finalisation (trace.py:87-114) -------------------------
  * mean_util = colsum/total, active_frac = active/T (IEEE, bit-exact);
  * corr = Pearson from exact integer statistics (0 on zero variance,

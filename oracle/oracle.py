@@ -374,6 +374,41 @@ def topk_hist(ids, B: int, E: int):
     return hist, dropped
 
 
+def coselect(ids, E: int) -> np.ndarray:
+    """Token-level co-selection counts C[l,a,b] = #tokens choosing both a and b (int64 [L,E,E]).
+
+    No reference counterpart ("parity unpinned by the
+    reference"); restated from its definition OᵀO over the 0/1 selection
+    indicator O[n,e] = [e in ids[n]] (ids outside [0,E) ignored, a repeated id
+    counts once). Its diagonal is the number of tokens choosing e, i.e.
+    topk_hist's column sums when ids are distinct -- the link to the pinned K1."""
+    ids = np.asarray(ids)
+    L, N, k = ids.shape
+    out = np.zeros((L, E, E), dtype=np.int64)
+    for l in range(L):
+        x = ids[l].astype(np.int64)
+        ok = (x >= 0) & (x < E)
+        onehot = np.zeros((N, E + 1), dtype=np.int64)
+        onehot[np.repeat(np.arange(N), k), np.where(ok, x, E).ravel()] = 1  # assignment: duplicates set once
+        o = onehot[:, :E]
+        out[l] = o.T @ o
+    return out
+
+
+def coselect_loops(ids, E: int) -> np.ndarray:
+    """The same by explicit per-token pair loops (pure Python; small cases only)."""
+    ids = np.asarray(ids)
+    L, N, k = ids.shape
+    out = np.zeros((L, E, E), dtype=np.int64)
+    for l in range(L):
+        for n in range(N):
+            s = sorted({int(v) for v in ids[l, n] if 0 <= int(v) < E})
+            for a in s:
+                for b in s:
+                    out[l, a, b] += 1
+    return out
+
+
 def philox4x32_10(counter, key):
     out = np.zeros(4, dtype=np.uint32)
     lib().or_philox4x32_10(np.ascontiguousarray(counter, dtype=np.uint32), int(key[0]), int(key[1]), out)

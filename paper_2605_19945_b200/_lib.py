@@ -70,6 +70,10 @@ _SIGNATURES = {
     "gem_step_gram_path": [I32, I64],
     "gem_step_gram_cc": [P, I64, I64, I32, P, P],
     "gem_step_gram_tc": [P, I64, I64, I32, P, P],
+    "gem_coselect": [P, I32, I64, I64, I32, I32, P, P],
+    "gem_coselect_path": [P, I32, I64, I32, I32],
+    "gem_coselect_tc": [P, I32, I64, I64, I32, I32, P, P],
+    "gem_coselect_scatter": [P, I32, I64, I64, I32, I32, P, P],
     "gem_stats_finalize": [P, P, P, I64, I64, I32, P, P, P, P],
     "gem_classify": [P, P, P, I64, I64, I32, I64, I64, I64, I64, P, P, P, P],
     "gem_eval_curve": [P, P, P, P, I32, P, I64, P, P],

@@ -342,6 +342,114 @@ __device__ __forceinline__ void ring_commit() { asm volatile("cp.async.commit_gr
 template <int N>
 __device__ __forceinline__ void ring_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// ---------------------------------------------------------------------------
+// Heavy-step counts from written histogram rows: heavy[l][e] += #steps t with
+// h > 0 and h*E >= the step's row total (is_heavy, exact). The ring kernel
+// leaves them out of its hot loop (an extra per-bin predicate there cost more
+// than this whole pass); this pass re-reads the L*T*E*4 histogram bytes once.
+// One warp per row: lane-strided loads (16-byte when E % 4 == 0), a 64-bit
+// warp sum, per-lane counters over the CTA's rows, one shared-memory merge and
+// one global atomic per expert per CTA.
+constexpr int kHeavyRows = 256;   // rows (steps) per CTA
+constexpr int kHeavyWarps = 8;
+
+// NJ: 128-expert column blocks (VEC: one int4 per lane per block) or
+// 32-expert scalar columns / 4 (!VEC); RU rows in flight per warp.
+template <bool VEC, int NJ>
+__global__ void __launch_bounds__(kHeavyWarps * 32)
+hist_heavy_rows_kernel(const int32_t* __restrict__ hist, int64_t T, int64_t HT, int E, int32_t* __restrict__ heavy) {
+  constexpr int RU = 4;
+  constexpr int PER = 4 * NJ;  // counters per lane
+  extern __shared__ int32_t hsum[];  // [E]
+  const int64_t l = blockIdx.y;
+  const int64_t t0 = (int64_t)blockIdx.x * kHeavyRows, t1 = imin64(t0 + kHeavyRows, T);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) hsum[e] = 0;
+  __syncthreads();
+  auto col = [&](int j, int i) { return VEC ? (j * 32 + lane) * 4 + i : (4 * j + i) * 32 + lane; };
+  uint32_t cnt[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) cnt[i] = 0;
+  for (int64_t tb = t0 + warp * RU; tb < t1; tb += kHeavyWarps * RU) {
+    uint32_t h[RU][PER];
+#pragma unroll
+    for (int r = 0; r < RU; ++r) {
+      const int64_t t = tb + r;
+      const int32_t* row = hist + (l * HT + t) * E;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        if (VEC) {
+          const int e = col(j, 0);
+          const int4 v = (t < t1 && e < E) ? __ldg(reinterpret_cast<const int4*>(row + e)) : make_int4(0, 0, 0, 0);
+          h[r][4 * j] = (uint32_t)v.x; h[r][4 * j + 1] = (uint32_t)v.y;
+          h[r][4 * j + 2] = (uint32_t)v.z; h[r][4 * j + 3] = (uint32_t)v.w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int e = col(j, i);
+            h[r][4 * j + i] = (t < t1 && e < E) ? (uint32_t)__ldg(row + e) : 0u;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RU; ++r) {
+      uint64_t part = 0;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) part += h[r][i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+#pragma unroll
+      for (int i = 0; i < PER; ++i) cnt[i] += (h[r][i] > 0u && (uint64_t)h[r][i] * (uint64_t)E >= part) ? 1u : 0u;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = col(j, i);
+      if (e < E && cnt[4 * j + i]) atomicAdd(&hsum[e], (int)cnt[4 * j + i]);
+    }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (hsum[e]) atomicAdd(&heavy[l * E + e], hsum[e]);
+}
+
+template <bool VEC, int NJ>
+static void heavy_rows_t(dim3 grid, size_t smem, cudaStream_t st, const int32_t* hist, int64_t T, int64_t HT, int E,
+                         int32_t* heavy) {
+  hist_heavy_rows_kernel<VEC, NJ><<<grid, kHeavyWarps * 32, smem, st>>>(hist, T, HT, E, heavy);
+}
+
+static int launch_heavy_rows(const int32_t* hist, int64_t L, int64_t T, int64_t HT, int E, int32_t* heavy,
+                             cudaStream_t st) {
+  if (L > 65535) {
+    set_error("heavy-step counts: more than 65535 layers");
+    return GEM_ERR_INVALID;
+  }
+  const dim3 grid((unsigned)((T + kHeavyRows - 1) / kHeavyRows), (unsigned)L);
+  const size_t smem = (size_t)E * sizeof(int32_t);
+  if (E % 4 == 0) {
+    const int nj = (E + 127) / 128;
+    if (nj == 1) heavy_rows_t<true, 1>(grid, smem, st, hist, T, HT, E, heavy);
+    else if (nj == 2) heavy_rows_t<true, 2>(grid, smem, st, hist, T, HT, E, heavy);
+    else heavy_rows_t<true, 4>(grid, smem, st, hist, T, HT, E, heavy);
+  } else {
+    const int nj = (E + 127) / 128;
+    if (nj == 1) heavy_rows_t<false, 1>(grid, smem, st, hist, T, HT, E, heavy);
+    else heavy_rows_t<false, 4>(grid, smem, st, hist, T, HT, E, heavy);
+  }
+  GEM_CHECK_LAUNCH("hist_heavy_rows_kernel");
+  return GEM_OK;
+}
+
+// counter rows of the ring kernel: E (+1 overflow) wide rows or E/2 (+1) pair
+// rows, padded to the 32*MAXR rows the per-step reduction reads unguarded
+template <bool WIDE, int MAXR>
+__host__ __device__ constexpr int ring_rows(int E) {
+  return (WIDE ? E + 1 : E / 2 + 1) > 32 * MAXR ? (WIDE ? E + 1 : E / 2 + 1) : 32 * MAXR;
+}
+
 // WIDE: u32 counters, rows E + 1; packed (even E only): u16x2 counters, pair
 // rows E/2 + 1 (row E/2 low half = overflow), halves summed separately in the
 // cumulative reduction (a lane's half counts at most B*k <= 65535 per unit).
@@ -349,14 +457,14 @@ template <bool WIDE, int MAXR>
 __global__ void __launch_bounds__(32)
 topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int k, int B, int E, int64_t T,
                       int64_t HT, int32_t* __restrict__ hist, int64_t* __restrict__ colsum,
-                      int32_t* __restrict__ active, int32_t* __restrict__ heavy, int64_t* __restrict__ dropped_out) {
+                      int32_t* __restrict__ active, int64_t* __restrict__ dropped_out) {
   extern __shared__ __align__(16) uint4 rsm[];
   constexpr int BATCH = kRingUnroll * 32;  // uint4 per warp batch (4 KB)
   const int lane = threadIdx.x;
   uint4* ring = rsm;                                                  // [kRingStages][kRingUnroll][32]
   uint32_t* cnt = reinterpret_cast<uint32_t*>(rsm + kRingStages * BATCH);  // [E + 1][32]
   uint32_t* cnt_lane = cnt + lane;
-  const int rows = WIDE ? E + 1 : E / 2 + 1;
+  const int rows = ring_rows<WIDE, MAXR>(E);  // padded to 32*MAXR
   const int hrows = WIDE ? E : E / 2;  // reduced rows holding real bins
   constexpr int BINS = WIDE ? 1 : 2;
   for (int w = lane; w < rows * 32; w += 32) cnt[w] = 0;
@@ -383,9 +491,9 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
       if (sidx < nb) issue(sidx);
       ring_commit();
     }
-    uint32_t prev[MAXR * BINS], act[MAXR * BINS], hvy[MAXR * BINS];
+    uint32_t prev[MAXR * BINS], act[MAXR * BINS];
 #pragma unroll
-    for (int q = 0; q < MAXR * BINS; ++q) { prev[q] = 0; act[q] = 0; hvy[q] = 0; }
+    for (int q = 0; q < MAXR * BINS; ++q) { prev[q] = 0; act[q] = 0; }
     int in_step = 0;
     int64_t t = t_begin;
     for (int64_t bt = 0; bt < nb; ++bt) {
@@ -400,50 +508,45 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
         in_step = 0;
         __syncwarp();
         int32_t* hrow = hist + (l * HT + t) * E;
-        uint32_t hq[MAXR * BINS], part = 0;
+        // all row sums first (the counter block is padded to 32*MAXR rows, so
+        // the loads need no guard and can all be in flight), then the updates
+        uint32_t sa[MAXR], sb[MAXR];
 #pragma unroll
-        for (int q = 0; q < MAXR * BINS; ++q) hq[q] = 0;
+        for (int q = 0; q < MAXR; ++q) {
+          const uint4* rp = reinterpret_cast<const uint4*>(cnt + (lane + q * 32) * 32);
+          uint32_t a = 0, b = 0;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v = rp[(c + lane) & 7];
+            if (WIDE) {
+              a += (v.x + v.y) + (v.z + v.w);
+            } else {
+              a += ((v.x & 0xffffu) + (v.y & 0xffffu)) + ((v.z & 0xffffu) + (v.w & 0xffffu));
+              b += ((v.x >> 16) + (v.y >> 16)) + ((v.z >> 16) + (v.w >> 16));
+            }
+          }
+          sa[q] = a;
+          sb[q] = b;
+        }
 #pragma unroll
         for (int q = 0; q < MAXR; ++q) {
           const int row = lane + q * 32;
           if (row < hrows) {
-            const uint4* rp = reinterpret_cast<const uint4*>(cnt + row * 32);
             if (WIDE) {
-              uint32_t sum = 0;
-#pragma unroll
-              for (int c = 0; c < 8; ++c) {
-                const uint4 v = rp[(c + lane) & 7];
-                sum += (v.x + v.y) + (v.z + v.w);
-              }
-              const uint32_t h = sum - prev[q];
-              prev[q] = sum;
+              const uint32_t h = sa[q] - prev[q];
+              prev[q] = sa[q];
               hrow[row] = (int32_t)h;
               act[q] += (h > 0);
-              hq[q] = h;
-              part += h;
             } else {
-              uint32_t lo = 0, hi = 0;
-#pragma unroll
-              for (int c = 0; c < 8; ++c) {
-                const uint4 v = rp[(c + lane) & 7];
-                lo += ((v.x & 0xffffu) + (v.y & 0xffffu)) + ((v.z & 0xffffu) + (v.w & 0xffffu));
-                hi += ((v.x >> 16) + (v.y >> 16)) + ((v.z >> 16) + (v.w >> 16));
-              }
-              const uint32_t hl = lo - prev[2 * q], hh = hi - prev[2 * q + 1];
-              prev[2 * q] = lo;
-              prev[2 * q + 1] = hi;
+              const uint32_t hl = sa[q] - prev[2 * q], hh = sb[q] - prev[2 * q + 1];
+              prev[2 * q] = sa[q];
+              prev[2 * q + 1] = sb[q];
               *reinterpret_cast<int2*>(hrow + 2 * row) = make_int2((int)hl, (int)hh);
               act[2 * q] += (hl > 0);
               act[2 * q + 1] += (hh > 0);
-              hq[2 * q] = hl;
-              hq[2 * q + 1] = hh;
-              part += hl + hh;
             }
           }
         }
-        const uint32_t stot = __reduce_add_sync(0xffffffffu, part);
-#pragma unroll
-        for (int q = 0; q < MAXR * BINS; ++q) hvy[q] += is_heavy(hq[q], uE, stot);
         __syncwarp();
         ++t;
       }
@@ -453,6 +556,7 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
     uint32_t dropped = WIDE ? cnt[E * 32 + lane] : (cnt[(E / 2) * 32 + lane] & 0xffffu);
     __syncwarp();
     for (int w = lane; w < rows * 32; w += 32) cnt[w] = 0;
+    dropped = __reduce_add_sync(0xffffffffu, dropped);
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < MAXR; ++q) {
@@ -461,14 +565,11 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
 #pragma unroll
       for (int bb = 0; bb < BINS; ++bb) {
         const int bin = row * BINS + bb;
-        const uint32_t cs = prev[q * BINS + bb], ac = act[q * BINS + bb], hv = hvy[q * BINS + bb];
+        const uint32_t cs = prev[q * BINS + bb], ac = act[q * BINS + bb];
         if (cs) atomicAdd((unsigned long long*)&colsum[l * E + bin], (unsigned long long)cs);
         if (ac) atomicAdd(&active[l * E + bin], (int)ac);
-        if (hv) atomicAdd(&heavy[l * E + bin], (int)hv);
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dropped += __shfl_xor_sync(0xffffffffu, dropped, o);
     if (lane == 0 && dropped) atomicAdd((unsigned long long*)&dropped_out[l], (unsigned long long)dropped);
   }
 }
@@ -476,7 +577,7 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
 template <bool WIDE, int MAXR>
 static int launch_hist_ring(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
                             int32_t* hist, int64_t* colsum, int32_t* active, int32_t* heavy, int64_t* dropped, cudaStream_t st) {
-  const int rows = WIDE ? E + 1 : E / 2 + 1;
+  const int rows = ring_rows<WIDE, MAXR>(E);
   const size_t smem = (size_t)kRingStages * kRingUnroll * 32 * 16 + (size_t)rows * 32 * 4;
   auto kern = topk_hist_ring_kernel<WIDE, MAXR>;
   GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -489,9 +590,9 @@ static int launch_hist_ring(const void* ids, int64_t L, int64_t N, int k, int B,
   int64_t blocks = (int64_t)num_sms() * per_sm;
   if (blocks > units) blocks = units;
   kern<<<(unsigned)blocks, 32, smem, st>>>((const int16_t*)ids, L, N, k, B, E, T, HT, hist, colsum, active,
-                                           heavy, dropped);
+                                           dropped);
   GEM_CHECK_LAUNCH("topk_hist_ring_kernel");
-  return GEM_OK;
+  return launch_heavy_rows(hist, L, T, HT, E, heavy, st);
 }
 
 template <typename IdT, bool WIDE, int MAXR>

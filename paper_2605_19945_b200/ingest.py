@@ -195,10 +195,46 @@ def ids_to_histograms(ids: torch.Tensor, tokens_per_step: int, num_experts: int,
     dropped = _device.zeros((L,), torch.int64)
     _lib.call("gem_topk_hist", ptr(ids), ids.element_size(), L, N, k, tokens_per_step, num_experts, ptr(hist),
               ptr(ds.colsum), ptr(ds.active), ptr(ds.heavy), ptr(dropped), stream())
+    if with_coselect:
+        token_coselection(ids, num_experts, out=ds.coselect)
     h = Histograms(hist, ds, dropped, tokens_per_step, k)
     if check_dropped and int(dropped.sum().item()):
         raise ValidationError(f"{int(dropped.sum().item())} expert ids outside [0, {num_experts})")
     return h
+
+
+# ---------------------------------------------------------------------------
+# K2b: token-level co-selection
+
+
+def token_coselection(ids: torch.Tensor, num_experts: int, out: torch.Tensor | None = None,
+                      path: str = "auto") -> torch.Tensor:
+    """K2b: C[l,a,b] = #tokens of layer l whose top-k ids hold both a and b (int32 [L,E,E]).
+
+    OᵀO of the 0/1 selection indicator: ids outside [0, E) are ignored and a
+    repeated id within one token counts once, so diag(C[l]) equals K1's
+    colsum[l] for distinct router ids. ACCUMULATES into `out` (zeros if None).
+    path: "auto" (tcgen05 kind::i8 where gem_coselect_path allows, CUDA-core
+    scatter otherwise), "tc" or "scatter"."""
+    if ids.dim() != 3 or ids.dtype not in (torch.int16, torch.int32):
+        raise ValidationError("ids must be int16/int32 [layers, tokens, k]")
+    if not ids.is_cuda:
+        ids = ids.to(_device.device())
+    ids = ids.contiguous()
+    L, N, k = ids.shape
+    if out is None:
+        out = _device.zeros((L, num_experts, num_experts), torch.int32)
+    if tuple(out.shape) != (L, num_experts, num_experts) or out.dtype != torch.int32:
+        raise ValidationError("out must be int32 [layers, E, E]")
+    fn = {"auto": "gem_coselect", "tc": "gem_coselect_tc", "scatter": "gem_coselect_scatter"}[path]
+    _lib.call(fn, ptr(ids), ids.element_size(), L, N, k, num_experts, ptr(out), stream())
+    return out
+
+
+def coselection_path(ids: torch.Tensor, num_experts: int) -> str:
+    """Which kernel gem_coselect runs for these ids: "tc" or "scatter"."""
+    L, N, k = ids.shape
+    return "tc" if _lib.lib().gem_coselect_path(ptr(ids), ids.element_size(), N, k, num_experts) == 1 else "scatter"
 
 
 # ---------------------------------------------------------------------------
@@ -287,9 +323,13 @@ class TraceStatistics:
 
 
 def trace_statistics(ids: torch.Tensor, tokens_per_step: int, num_experts: int, correlation: bool = True,
-                     classify: bool = True, config: ClassifyConfig = ClassifyConfig()) -> TraceStatistics:
-    """The whole statistics phase for one top-k trace (all layers): K1 -> K2 -> K3 -> K3b."""
-    h = ids_to_histograms(ids, tokens_per_step, num_experts, check_dropped=False)
+                     classify: bool = True, config: ClassifyConfig = ClassifyConfig(),
+                     coselect: bool = False) -> TraceStatistics:
+    """The whole statistics phase for one top-k trace (all layers): K1 (+ K2b) -> K2 -> K3 -> K3b.
+
+    coselect=True also fills hist.stats.coselect with the token-level
+    co-selection counts (K2b)."""
+    h = ids_to_histograms(ids, tokens_per_step, num_experts, check_dropped=False, with_coselect=coselect)
     return statistics_from_histograms(h, correlation=correlation, classify=classify, config=config)
 
 

@@ -72,6 +72,22 @@ def test_topk_hist_ring_path(oracle, shape):
     assert np.array_equal(h.heavy.cpu().numpy(), np.stack([oracle.heavy_counts(w) for w in want]))
 
 
+@pytest.mark.parametrize("E", [128, 256])
+def test_topk_hist_ring_heavy_with_sparse_drops(oracle, E):
+    """Heavy-step counts on the ring path: steps are full, so the row total is
+    B*k except in units that dropped ids, which recount from their rows."""
+    L, N, k, B = 2, 96 * 1024, 8, 1024
+    rng = np.random.default_rng(E)
+    ids = rng.integers(0, E, (L, N, k)).astype(np.int16)
+    ids[0, 5 * 1024 + 7, 3] = E + 4        # one dropped id in unit 0 of layer 0
+    ids[1, 70 * 1024:70 * 1024 + 900, :] = np.int16(-1)  # a step that lost most of its ids (unit 2 of layer 1)
+    h = ingest.ids_to_histograms(torch.from_numpy(ids).cuda(), B, E, check_dropped=False)
+    want, dropped = oracle.topk_hist(ids, B, E)
+    assert np.array_equal(h.hist.cpu().numpy(), want)
+    assert np.array_equal(h.dropped.cpu().numpy(), dropped)
+    assert np.array_equal(h.heavy.cpu().numpy(), np.stack([oracle.heavy_counts(w) for w in want]))
+
+
 def test_topk_hist_unaligned_view(oracle):
     rng = np.random.default_rng(9)
     base = rng.integers(0, 32, (1, 4097, 3)).astype(np.int16)

@@ -46,12 +46,13 @@ def bench_hist(args):
     hist = torch.empty((L, T, E), dtype=torch.int32, device="cuda")
     colsum = torch.zeros((L, E), dtype=torch.int64, device="cuda")
     active = torch.zeros((L, E), dtype=torch.int32, device="cuda")
+    heavy = torch.zeros((L, E), dtype=torch.int32, device="cuda")
     dropped = torch.zeros((L,), dtype=torch.int64, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
 
     def run():
         _lib.call("gem_topk_hist", ids.data_ptr(), args.id_bytes, L, N, k, B, E, hist.data_ptr(), colsum.data_ptr(),
-                  active.data_ptr(), dropped.data_ptr(), st)
+                  active.data_ptr(), heavy.data_ptr(), dropped.data_ptr(), st)
 
     ms = timed(run, args.reps, args.warm)
     byts = L * N * k * args.id_bytes + L * T * E * 4
@@ -68,6 +69,20 @@ def bench_gram(args):
     for fn in ("gem_step_gram_cc", "gem_step_gram_tc"):
         ms = timed(lambda: _lib.call(fn, hist.data_ptr(), L, T, E, gram.data_ptr(), st), args.reps, args.warm)
         print(json.dumps({"kernel": fn, "ms": ms, "GMACps": macs / ms / 1e6, "hbm_GBps": L * T * E * 4 / ms / 1e6}))
+
+
+def bench_coselect(args):
+    L, N, k, E, B = args.layers, args.tokens, args.k, args.experts, 1024
+    spec = ingest.TopkTraceSpec(num_layers=L, num_tokens=N, top_k=k, num_experts=E, tokens_per_step=B, seed=0)
+    ids = ingest.generate_topk_ids(spec, dtype=torch.int16 if args.id_bytes == 2 else torch.int32)
+    out = torch.zeros((L, E, E), dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    ops = 2 * L * N * (128 * ((E + 127) // 128)) ** 2  # int8 tensor ops issued (padded one-hot OᵀO)
+    for fn in args.paths.split(","):
+        ms = timed(lambda: _lib.call(fn, ids.data_ptr(), args.id_bytes, L, N, k, E, out.data_ptr(), st), args.reps,
+                   args.warm)
+        print(json.dumps({"kernel": fn, "ms": ms, "tokens_per_s": L * N / ms * 1e3, "int8_TOPS": ops / ms / 1e9,
+                          "id_GBps": L * N * k * args.id_bytes / ms / 1e6, "L": L, "N": N, "E": E, "k": k}))
 
 
 def bench_score(args):
@@ -124,7 +139,8 @@ def bench_swap(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=("hist", "gram", "score", "swap"))
+    ap.add_argument("what", choices=("hist", "gram", "coselect", "score", "swap"))
+    ap.add_argument("--paths", default="gem_coselect_tc,gem_coselect_scatter")
     ap.add_argument("--layers", type=int, default=94)
     ap.add_argument("--tokens", type=int, default=1 << 24)
     ap.add_argument("--k", type=int, default=8)
@@ -138,7 +154,7 @@ def main():
     ap.add_argument("--warm", type=int, default=3)
     args = ap.parse_args()
     torch.cuda.set_device(0)
-    {"hist": bench_hist, "gram": bench_gram, "score": bench_score, "swap": bench_swap}[args.what](args)
+    {"hist": bench_hist, "gram": bench_gram, "coselect": bench_coselect, "score": bench_score, "swap": bench_swap}[args.what](args)
 
 
 if __name__ == "__main__":
