@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-search", action="store_true", help="skip the time-to-mapping leg")
     ap.add_argument("--no-candidates", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-coselect", action="store_true", help="skip the K2b co-selection leg")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--search-steps", type=int, default=None, help="search window (default: all steps)")
     ap.add_argument("--force-dist", action="store_true",
@@ -149,6 +150,15 @@ def peaks():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def tensor_peaks():
+    """int8 / fp16 / fp64 GEMM peaks measured on a B200 of this pool by tools/peaks.py (cuBLAS)."""
+    p = ROOT / "profiles" / "r02_peaks.json"
+    try:
+        return json.loads(p.read_text())
+    except (OSError, ValueError):
+        return {}
 
 
 def ncu_traffic():
@@ -262,19 +272,61 @@ def run_ours(args):
                    "tokens": N, "top_k": k, "experts": E, "tokens_per_step": B, "steps_per_layer": T,
                    "virtual_gpus": G, "id_dtype": "int16", "l2": "inputs 25 GB >> 126 MB L2 (no flush needed)",
                    "parallelism": f"token-range shards x{world}, NCCL all-reduce of integer stats"},
-        "gpu_launches": 4 * args.steps,
+        "gpu_launches": 5 * args.steps,  # K1 ring + heavy-row pass, K2, K3, K3b
         "step_breakdown_ms": {name: sum(e[i].elapsed_time(e[i + 1]) for e in pev) / len(pev)
                               for i, name in enumerate(phases)},
         "clocks": clk.summary(),
     }
-    # roofline of the dominant kernel (K1)
-    algo_bytes = L * n_local * k * 2 + L * (t1 - t0) * E * 4
+    # roofline of the dominant kernel (K1 = gem_topk_hist: the ring kernel and
+    # its heavy-step row pass): ids read + histogram written + histogram re-read
+    algo_bytes = L * n_local * k * 2 + 2 * L * (t1 - t0) * E * 4
     peak, peak_src = peaks()
     achieved = algo_bytes / (k1_ms / 1e3) / 1e9
-    result["roofline"] = {"kernel": "topk_hist_ring_kernel (K1)", "bound": "hbm", "achieved": achieved, "peak": peak,
+    result["roofline"] = {"kernel": "gem_topk_hist (K1: topk_hist_ring_kernel + hist_heavy_rows_kernel)",
+                          "bound": "hbm", "achieved": achieved, "peak": peak,
                           "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic() if args.config == "qwen3-235b" and world == 1 else None,
                           "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": k1_ms,
                           "kernel_share_of_step": k1_ms / ms, "peak_source": peak_src}
+
+    # ---- K2b token-level co-selection counts of this rank's token shard (an
+    #      optional statistics output, timed on its own): tcgen05 kind::i8 OᵀO
+    if not args.no_coselect:
+        cs = torch.zeros((L, E, E), dtype=torch.int32, device="cuda")
+
+        def cs_step():
+            cs.zero_()
+            ingest.token_coselection(ids, E, out=cs)
+
+        cs_step()
+        torch.cuda.synchronize()
+        if use_dist:
+            dist.barrier()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(1, min(3, args.steps))
+        c0.record(stream)
+        for _ in range(reps):
+            cs_step()
+        c1.record(stream)
+        torch.cuda.synchronize()
+        cs_t = torch.tensor([c0.elapsed_time(c1) / reps], device="cuda")
+        if use_dist:
+            dist.all_reduce(cs_t, op=dist.ReduceOp.MAX)
+        cs_ms = float(cs_t.item())
+        useful = 2 * L * N * E * E  # int8 MACs x2 of the one-hot OᵀO (unpadded E)
+        tp = tensor_peaks()
+        result["coselection"] = {
+            "value": N / (cs_ms / 1e3), "unit": "tokens/s", "ms": cs_ms,
+            "path": ingest.coselection_path(ids, E),
+            "roofline": {"kernel": "coselect_tc_kernel (K2b)", "bound": "tensor", "achieved": useful / cs_ms / 1e9,
+                         "peak": tp.get("int8_tops"), "unit": "TOPS",
+                         "frac": (useful / cs_ms / 1e9 / tp["int8_tops"]) if tp.get("int8_tops") else None,
+                         "peak_source": "profiles/r02_peaks.json (cuBLAS int8 GEMM, 8192^3)" if tp else None,
+                         "note": "shared-memory bound in practice: SS-mode MMA operand reads + one-hot build; "
+                                 "see DESIGN.md K2b"},
+            # built-in check (outside the timed region): diag(OᵀO) == K1's per-expert token totals
+            "diag_equals_colsum": bool(torch.equal(torch.diagonal(cs, dim1=1, dim2=2).long(),
+                                                   hist.sum(dim=1, dtype=torch.int64)))}
+        del cs
 
     plan = dist_mod.ShardPlan(world, rank, L, T)
     ops = dist_mod.DeviceOps()

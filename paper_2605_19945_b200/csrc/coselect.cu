@@ -50,22 +50,28 @@ constexpr int kCsTok = 128;                     // tokens per pipeline stage
 constexpr int kCsProd = 4;                      // producer / epilogue warps (32 tokens each, TMEM lane quarters)
 constexpr int kCsThreads = (kCsProd + 2) * 32;  // + MMA warp + TMA warp
 constexpr int kCsMaxTokBytes = 32;              // k * id_bytes on the tensor-core path
-constexpr int kCsIdStageBytes = kCsTok * kCsMaxTokBytes;
 
 #ifndef GEM_CS_STAGES1
 #define GEM_CS_STAGES1 4  // E <= 128: 4 x 16 KB operand stages -> two CTAs per SM
 #endif
 
-template <int EB>
+// IDB: bytes of one id-ring slot (kCsTok tokens x 16 or 32 bytes); the id ring
+// is 32 KB deep either way (16 or 8 stages of 128 tokens in flight per CTA),
+// enough outstanding TMA bytes to cover HBM latency at the kernel's id rate
+template <int EB, int IDB>
 struct CsGeo {
   static constexpr int EP = 128 * EB;                // padded experts (operand rows)
-  static constexpr int LBO = EP * 16;                // bytes per 16-token K slice
+  static constexpr int SLICE = EP * 16;              // bytes of one 16-token K slice
+  // K-slice stride: +64 bytes of padding shift the second slice of a warp by
+  // 16 banks, so lanes t and t+16 (same byte column, adjacent slices) stop
+  // colliding in the one-hot scatter; the MMA never reads the padding
+  static constexpr int LBO = SLICE + 64;
   static constexpr int STAGE = LBO * (kCsTok / 16);  // one-hot bytes per stage
-  static constexpr int STAGES = EB == 1 ? GEM_CS_STAGES1 : 4;
-  static constexpr int ISTAGES = STAGES + 2;
+  static constexpr int STAGES = EB == 1 ? GEM_CS_STAGES1 : 4;  // powers of two: ring
+  static constexpr int ISTAGES = 32768 / IDB;                  // indices are masks
   static constexpr int CTAS_PER_SM = EB == 1 && STAGES <= 4 ? 2 : 1;
   static constexpr uint32_t TMEM_COLS = EB == 1 ? 128 : 512;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE + (size_t)ISTAGES * kCsIdStageBytes + 512;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + (size_t)ISTAGES * IDB + 512;
 };
 
 struct CsBars {
@@ -83,16 +89,16 @@ __device__ __forceinline__ uint32_t id_as_u32(IdT v) {
 
 // TOKB: bytes of one token's ids when they can be read as 16-byte vectors (16
 // or 32), 0 for the scalar path.
-template <typename IdT, int EB, int TOKB>
-__global__ void __launch_bounds__(kCsThreads, CsGeo<EB>::CTAS_PER_SM)
+template <typename IdT, int EB, int TOKB, int IDB>
+__global__ void __launch_bounds__(kCsThreads, (CsGeo<EB, IDB>::CTAS_PER_SM))
 coselect_tc_kernel(const IdT* __restrict__ ids, int64_t N, int k, int E, int64_t total, int64_t range,
                    int32_t* __restrict__ out) {
-  using G = CsGeo<EB>;
+  using G = CsGeo<EB, IDB>;
   constexpr int kMaxIds = kCsMaxTokBytes / (int)sizeof(IdT);
   extern __shared__ __align__(1024) unsigned char cs_smem[];
   unsigned char* op = cs_smem;
   unsigned char* idr = cs_smem + G::STAGES * G::STAGE;
-  CsBars* sh = reinterpret_cast<CsBars*>(idr + G::ISTAGES * kCsIdStageBytes);
+  CsBars* sh = reinterpret_cast<CsBars*>(idr + G::ISTAGES * IDB);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t s0 = (int64_t)blockIdx.x * range;
@@ -122,15 +128,15 @@ coselect_tc_kernel(const IdT* __restrict__ ids, int64_t N, int k, int E, int64_t
   if (warp == kCsProd + 1) {
     // ---------------- TMA: ids of each stage -> shared ring
     if (lane == 0) {
-      int64_t g = 0;
+      uint32_t g = 0;
       for (int64_t p = s0; p < s1;) {
         const int64_t seg = imin64(s1 - p, N - p % N);
         for (int64_t j = 0; j < seg; j += kCsTok, ++g) {
           const int is = (int)(g % G::ISTAGES);
-          if (g >= G::ISTAGES) tc::mbar_wait(&sh->ids_empty[is], (uint32_t)((g / G::ISTAGES - 1) & 1));
+          if (g >= G::ISTAGES) tc::mbar_wait(&sh->ids_empty[is], (g / G::ISTAGES - 1) & 1);
           const uint32_t bytes = (uint32_t)(imin64(kCsTok, seg - j) * tok_bytes);
           tc::mbar_arrive_expect_tx(&sh->ids_full[is], bytes);
-          tc::bulk_load_1d(idr + is * kCsIdStageBytes, ids + (p + j) * k, bytes, &sh->ids_full[is]);
+          tc::bulk_load_1d(idr + is * IDB, ids + (p + j) * k, bytes, &sh->ids_full[is]);
         }
         p += seg;
       }
@@ -138,7 +144,7 @@ coselect_tc_kernel(const IdT* __restrict__ ids, int64_t N, int k, int E, int64_t
   } else if (warp == kCsProd) {
     // ---------------- MMA issuer
     if (lane == 0) {
-      int64_t g = 0;
+      uint32_t g = 0;
       int segno = 0;
       const uint32_t op_addr = tc::smem_u32(op);
       for (int64_t p = s0; p < s1; ++segno) {
@@ -146,7 +152,7 @@ coselect_tc_kernel(const IdT* __restrict__ ids, int64_t N, int k, int E, int64_t
         const int64_t nst = (seg + kCsTok - 1) / kCsTok;
         for (int64_t st = 0; st < nst; ++st, ++g) {
           const int s = (int)(g % G::STAGES);
-          tc::mbar_wait(&sh->op_full[s], (uint32_t)((g / G::STAGES) & 1));
+          tc::mbar_wait(&sh->op_full[s], (g / G::STAGES) & 1);
           if (st == 0 && segno > 0) tc::mbar_wait(&sh->acc_empty, (uint32_t)((segno - 1) & 1));
           tc::tc_fence_after();
           const uint32_t base = op_addr + (uint32_t)(s * G::STAGE);
@@ -171,7 +177,7 @@ coselect_tc_kernel(const IdT* __restrict__ ids, int64_t N, int k, int E, int64_t
     }
   } else {
     // ---------------- producers (lane = token of the stage) + segment epilogue
-    int64_t g = 0;
+    uint32_t g = 0;
     int segno = 0;
     const int tok = warp * 32 + lane;
     for (int64_t p = s0; p < s1; ++segno) {
@@ -182,9 +188,9 @@ coselect_tc_kernel(const IdT* __restrict__ ids, int64_t N, int k, int E, int64_t
         const int s = (int)(g % G::STAGES), is = (int)(g % G::ISTAGES);
         const bool valid = tok < imin64(kCsTok, seg - st * kCsTok);
         uint32_t idv[kMaxIds];
-        tc::mbar_wait(&sh->ids_full[is], (uint32_t)((g / G::ISTAGES) & 1));
+        tc::mbar_wait(&sh->ids_full[is], (g / G::ISTAGES) & 1);
         if (valid) {
-          const unsigned char* tp = idr + is * kCsIdStageBytes + tok * tok_bytes;
+          const unsigned char* tp = idr + is * IDB + tok * tok_bytes;
           if (TOKB > 0) {
             uint32_t w[TOKB > 0 ? TOKB / 4 : 1];
 #pragma unroll
@@ -205,11 +211,11 @@ coselect_tc_kernel(const IdT* __restrict__ ids, int64_t N, int k, int E, int64_t
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&sh->ids_empty[is]);
-        if (g >= G::STAGES) tc::mbar_wait(&sh->op_empty[s], (uint32_t)((g / G::STAGES - 1) & 1));
+        if (g >= G::STAGES) tc::mbar_wait(&sh->op_empty[s], (g / G::STAGES - 1) & 1);
         unsigned char* slab = op + s * G::STAGE + warp * 2 * G::LBO;  // this warp's two 16-token K slices
-        uint4* z = reinterpret_cast<uint4*>(slab);
 #pragma unroll
-        for (int i = lane; i < 2 * G::LBO / 16; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
+        for (int i = lane; i < 2 * G::EP; i += 32)
+          *reinterpret_cast<uint4*>(slab + (i / G::EP) * G::LBO + (i % G::EP) * 16) = make_uint4(0u, 0u, 0u, 0u);
         __syncwarp();
         if (valid) {
           unsigned char* col = slab + (lane >> 4) * G::LBO + (lane & 15);
@@ -335,10 +341,10 @@ static int64_t cs_range(int64_t total, int64_t ctas, int64_t align) {
   return ((r + align - 1) / align) * align;
 }
 
-template <typename IdT, int EB, int TOKB>
+template <typename IdT, int EB, int TOKB, int IDB>
 static int launch_cs_tc(const void* ids, int64_t L, int64_t N, int k, int E, int32_t* out, cudaStream_t st) {
-  auto kern = coselect_tc_kernel<IdT, EB, TOKB>;
-  const size_t smem = CsGeo<EB>::SMEM;
+  auto kern = coselect_tc_kernel<IdT, EB, TOKB, IDB>;
+  const size_t smem = CsGeo<EB, IDB>::SMEM;
   GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t total = L * N;
   int per_sm = 1;
@@ -355,9 +361,10 @@ static int launch_cs_tc(const void* ids, int64_t L, int64_t N, int k, int E, int
 template <typename IdT, int EB>
 static int dispatch_cs_tc(const void* ids, int64_t L, int64_t N, int k, int E, int32_t* out, cudaStream_t st) {
   const int tb = k * (int)sizeof(IdT);
-  if (tb == 16) return launch_cs_tc<IdT, EB, 16>(ids, L, N, k, E, out, st);
-  if (tb == 32) return launch_cs_tc<IdT, EB, 32>(ids, L, N, k, E, out, st);
-  return launch_cs_tc<IdT, EB, 0>(ids, L, N, k, E, out, st);
+  if (tb == 16) return launch_cs_tc<IdT, EB, 16, 2048>(ids, L, N, k, E, out, st);
+  if (tb == 32) return launch_cs_tc<IdT, EB, 32, 4096>(ids, L, N, k, E, out, st);
+  if (tb < 16) return launch_cs_tc<IdT, EB, 0, 2048>(ids, L, N, k, E, out, st);
+  return launch_cs_tc<IdT, EB, 0, 4096>(ids, L, N, k, E, out, st);
 }
 
 static size_t cs_scatter_smem(int E) { return (size_t)E * (E + 1) / 2 * sizeof(uint32_t); }
