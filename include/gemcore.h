@@ -184,9 +184,19 @@ int gem_classify(const int64_t* colsum, const int32_t* heavy, const int64_t* gra
                  int32_t* err_flag, void* stream);
 
 /* --- K4: curve evaluation ----------------------------------------------- */
+/* out[i] = C_gpu(counts[i]) (profiles.py:157-190, _kernels.pyx:18-55);
+ * asynchronous: the curve bounds offsets[gpu..gpu+1] / dense_limits[gpu] are
+ * device data read by the kernel; an empty curve sets *err_flag (may be NULL)
+ * to GEM_ERR_INVALID. */
 int gem_eval_curve(const int64_t* xs_flat, const double* ys_flat, const int64_t* offsets,
                    const int64_t* dense_limits, int32_t gpu, const int64_t* counts, int64_t n,
-                   double* out, void* stream);
+                   double* out, int32_t* err_flag, void* stream);
+/* equal_latency_load (profiles.py:308-333): *out = the largest n_b with
+ * C_gpu_b(n_b) <= C_gpu_a(n_a), doubling then bisection saturating at
+ * max_search, the reference's probe sequence on one device thread. */
+int gem_equal_latency_load(const int64_t* xs_flat, const double* ys_flat, const int64_t* offsets,
+                           const int64_t* dense_limits, int32_t gpu_a, int32_t gpu_b, int64_t n_a,
+                           int64_t max_search, int64_t* out, void* stream);
 /* lut[g][n] = C_g(n) for n in [0, nmax]  (f64 [G, nmax+1]) */
 int gem_curve_lut(const int64_t* xs_flat, const double* ys_flat, const int64_t* offsets,
                   const int64_t* dense_limits, int32_t G, int64_t nmax, double* lut,
@@ -204,11 +214,14 @@ int gem_score_batch(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_
 /* The two implementations behind gem_score_batch (which tries the first and
  * falls back to the second):
  *  - gem_score_batch_tc: candidate loads as a one-hot fp16 GEMM on tcgen05
- *    (exact: counts <= 2048, loads < 2^24), written as uint16, then one thread
- *    per (candidate, layer) takes the exact per-step maximum (fp32 table
- *    window in shared memory picks the GPU, the fp64 table gives the value)
- *    and sums serially. Needs E in {64, 128}, G | 256. Returns 1 (nothing
- *    done) when a precondition fails; stream-ordered scratch, one host sync.
+ *    (exact: counts <= 2048, loads < 2^24); every load is looked up in a
+ *    u16 order-key table of the load window (keys rank the distinct fp64
+ *    latencies, so the step maximum is an integer max) and each
+ *    (candidate, layer) chain adds the exact fp64 value of its step maxima
+ *    serially in t. Needs E in {64, 128}, G in {4, 8, 16, 32}. Returns 1
+ *    (nothing done) when a precondition fails. Stream-ordered scratch; ONE
+ *    host sync (the launch geometry depends on the load window), two only
+ *    when G x window > 65,536 entries.
  *  - gem_score_batch_v1: CUDA cores, any shape (E <= 256). */
 int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G,
                        const int8_t* cand, int64_t C, const double* lut, int64_t nmax,

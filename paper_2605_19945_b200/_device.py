@@ -112,12 +112,20 @@ class DeviceCurves:
             pass
         return dc
 
-    def eval(self, gpu: int, counts: torch.Tensor) -> torch.Tensor:
+    def eval(self, gpu: int, counts: torch.Tensor, err: torch.Tensor | None = None) -> torch.Tensor:
+        """C_gpu(counts) on the device, asynchronously (err: optional int32 flag, set on an empty curve)."""
         counts = counts.to(device=device(), dtype=torch.int64).contiguous()
         out = torch.empty(counts.shape, dtype=torch.float64, device=counts.device)
         _lib.call("gem_eval_curve", ptr(self.xs), ptr(self.ys), ptr(self.offsets), ptr(self.dense), int(gpu),
-                  ptr(counts), counts.numel(), ptr(out), stream())
+                  ptr(counts), counts.numel(), ptr(out), ptr(err), stream())
         return out
+
+    def equal_latency_load(self, gpu_a: int, gpu_b: int, n_a: int, max_search: int) -> int:
+        """profiles.equal_latency_load on one device thread (one result read back)."""
+        out = torch.empty((1,), dtype=torch.int64, device=device())
+        _lib.call("gem_equal_latency_load", ptr(self.xs), ptr(self.ys), ptr(self.offsets), ptr(self.dense),
+                  int(gpu_a), int(gpu_b), int(n_a), int(max_search), ptr(out), stream())
+        return int(out.item())
 
     def lut(self, nmax: int) -> torch.Tensor:
         """[G, nmax+1] fp64 table (grown on demand; a larger table serves smaller nmax)."""

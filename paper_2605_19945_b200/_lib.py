@@ -76,7 +76,8 @@ _SIGNATURES = {
     "gem_coselect_scatter": [P, I32, I64, I64, I32, I32, P, P],
     "gem_stats_finalize": [P, P, P, I64, I64, I32, P, P, P, P],
     "gem_classify": [P, P, P, I64, I64, I32, I64, I64, I64, I64, P, P, P, P],
-    "gem_eval_curve": [P, P, P, P, I32, P, I64, P, P],
+    "gem_eval_curve": [P, P, P, P, I32, P, I64, P, P, P],
+    "gem_equal_latency_load": [P, P, P, P, I32, I32, I64, I64, P, P],
     "gem_curve_lut": [P, P, P, P, I32, I64, P, P],
     "gem_score_batch": [P, I64, I64, I32, I32, P, I64, P, I64, P, P, P, P],
     "gem_layer_sum": [P, I64, I64, P, P],

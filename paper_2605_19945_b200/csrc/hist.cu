@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "gem_common.cuh"
+#include "tc.cuh"
 
 namespace gem {
 
@@ -41,12 +42,19 @@ constexpr int kWideMaxE = 160;
 template <typename IdT>
 __device__ __forceinline__ void count_vec_wide(uint32_t* cnt_lane, const uint4& v, uint32_t E, uint32_t Epair) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  // int16: shared-window byte address of (bin, lane) = lane base + bin*128.
+  // The high id of a word m = hi<<16 | lo gives hi*128 = m >> 9 directly
+  // (lo <= E < 512 after the clamp, so its bits shift out): 2 instructions
+  // for the pair's addresses besides the clamp, one reduction each.
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(cnt_lane);
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     if (sizeof(IdT) == 2) {
       const uint32_t m = __vminu2(w[c], Epair);  // clamp both halves to the overflow row E
-      atomicAdd(cnt_lane + ((m & 0xffffu) << 5), 1u);
-      atomicAdd(cnt_lane + ((m >> 16) << 5), 1u);
+      const uint32_t a_lo = base + (__byte_perm(m, 0u, 0x4410) << 7);  // PRMT + LEA
+      const uint32_t a_hi = base + (m >> 9);
+      asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(a_lo) : "memory");
+      asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(a_hi) : "memory");
     } else {
       atomicAdd(cnt_lane + (min(w[c], E) << 5), 1u);
     }
@@ -595,6 +603,193 @@ static int launch_hist_ring(const void* ids, int64_t L, int64_t N, int k, int B,
   return launch_heavy_rows(hist, L, T, HT, E, heavy, st);
 }
 
+// ---------------------------------------------------------------------------
+// K1 CTA variant for large E (int16 ids, u32 lane-private counters SHARED by
+// the CTA's W warps). At E = 256 the per-step reduction of E x 32 lane
+// counters costs as much as the counting, and 32 KB of u32 counters per warp
+// (or the u16x2 packing that halves them at ~2x the instructions per id) caps
+// a one-warp-per-CTA design at 8 warps per SM. Here W warps count into ONE
+// set of lane-private counters -- lane L of every warp always hits bank L, so
+// the reductions never conflict, and warps never conflict with each other --
+// each warp takes bps/W of a step's 2 KB batches, a named barrier closes the
+// step, every warp reduces its 32*R rows (cumulative counters: the reduction
+// only reads, hist = row sum - previous row sum) and a second barrier reopens
+// the counters. No shared-memory staging of the ids: each lane loads its
+// 16-byte pieces straight into registers NB steps ahead (buf rotates with a
+// compile-time index: the step loop is unrolled by NB), so W*NB 2 KB batches
+// per CTA are in flight through the barriers. (A TMA-bulk-copy ring in
+// shared memory was tried first: its copies in and reads out are shared
+// wavefronts the counting needs; 4.86 ms vs 3.26 ms at DeepSeek-V3 shape.)
+constexpr int kCtaBatch = 2048;  // bytes of one warp's slice of a step (1024 int16 ids)
+
+template <int W, int R, int G, int NB, int BPW, int MINB>
+__global__ void __launch_bounds__(W * 32, MINB)
+topk_hist_creg_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int k, int B, int E, int64_t T,
+                      int64_t HT, int32_t* __restrict__ hist, int64_t* __restrict__ colsum,
+                      int32_t* __restrict__ active, int64_t* __restrict__ dropped_out) {
+  extern __shared__ __align__(128) uint32_t crs[];
+  constexpr int PER = BPW * (kCtaBatch / 16 / 32);  // uint4 per lane per step
+  constexpr int D = G * NB;                          // step slots in registers
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rows = (E + 1) > 32 * R * W ? E + 1 : 32 * R * W;
+  const int set_words = rows * 32;
+  for (int i = threadIdx.x; i < G * set_words; i += W * 32) crs[i] = 0;
+  __syncthreads();
+  const uint32_t uE = (uint32_t)E, Epair = uE | (uE << 16);
+  const int64_t upl = (T + kHistStepsPerUnit - 1) / kHistStepsPerUnit;
+  const int64_t total_units = L * upl;
+  const int64_t step_vec = (int64_t)B * k / 8;  // uint4 per step
+  const int64_t lane_off = (int64_t)warp * BPW * (kCtaBatch / 16) + lane;
+
+  // producer: slots of (unit, step), G per group; slots past the unit's end are empty
+  int64_t p_unit = blockIdx.x;
+  int p_left = 0, p_j = 0;
+  const uint4* p_ptr = nullptr;
+  auto p_open = [&]() {
+    if (p_unit < total_units) {
+      const int64_t l = p_unit / upl, tb = (p_unit % upl) * kHistStepsPerUnit;
+      p_left = (int)(imin64(tb + kHistStepsPerUnit, T) - tb);
+      p_ptr = reinterpret_cast<const uint4*>(ids + (l * N + tb * B) * k) + lane_off;
+    }
+  };
+  p_open();
+  uint4 buf[D][PER];
+  auto load_next = [&](uint4 (&b)[PER]) {
+    if (p_unit >= total_units) return;
+    if (p_left > 0) {
+#pragma unroll
+      for (int u = 0; u < PER; ++u) b[u] = __ldcs(p_ptr + u * 32);
+      p_ptr += step_vec;
+      --p_left;
+    }
+    if (++p_j == G) {
+      p_j = 0;
+      if (p_left == 0) {
+        p_unit += gridDim.x;
+        p_open();
+      }
+    }
+  };
+#pragma unroll
+  for (int d = 0; d < D; ++d) load_next(buf[d]);
+
+  // consumer
+  int64_t c_unit = blockIdx.x;
+  int64_t c_l = 0, c_t = 0, c_tend = 0;
+  auto c_open = [&]() {
+    if (c_unit < total_units) {
+      c_l = c_unit / upl;
+      c_t = (c_unit % upl) * kHistStepsPerUnit;
+      c_tend = imin64(c_t + kHistStepsPerUnit, T);
+    }
+  };
+  c_open();
+  uint32_t prev[G][R], act[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    act[q] = 0;
+#pragma unroll
+    for (int j = 0; j < G; ++j) prev[j][q] = 0;
+  }
+  while (c_unit < total_units) {
+#pragma unroll
+    for (int g = 0; g < NB; ++g) {
+      if (c_unit < total_units) {
+        const int nvalid = (int)imin64(G, c_tend - c_t);
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          if (j < nvalid) {
+            uint32_t* cnt_lane = crs + j * set_words + lane;
+#pragma unroll
+            for (int u = 0; u < PER; ++u) count_vec_wide<int16_t>(cnt_lane, buf[g * G + j][u], uE, Epair);
+          }
+          load_next(buf[g * G + j]);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(W * 32) : "memory");  // the group's steps counted by every warp
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          if (j < nvalid) {
+            int32_t* hrow = hist + (c_l * HT + c_t + j) * E;
+            uint32_t sa[R];
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+              const uint4* rp =
+                  reinterpret_cast<const uint4*>(crs + j * set_words + ((warp * R + q) * 32 + lane) * 32);
+              uint32_t a = 0;
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const uint4 x = rp[(c + lane) & 7];
+                a += (x.x + x.y) + (x.z + x.w);
+              }
+              sa[q] = a;
+            }
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+              const int row = (warp * R + q) * 32 + lane;
+              const uint32_t h = sa[q] - prev[j][q];
+              prev[j][q] = sa[q];
+              if (row < E) {
+                hrow[row] = (int32_t)h;
+                act[q] += (h > 0);
+              }
+            }
+          }
+        }
+        c_t += nvalid;
+        if (c_t == c_tend) {  // unit end: dropped ids, per-expert totals, counters reset
+          if (warp == 0) {
+            uint32_t dd = 0;
+#pragma unroll
+            for (int j = 0; j < G; ++j) dd += crs[j * set_words + E * 32 + lane];
+            dd = __reduce_add_sync(0xffffffffu, dd);
+            if (lane == 0 && dd) atomicAdd((unsigned long long*)&dropped_out[c_l], (unsigned long long)dd);
+          }
+#pragma unroll
+          for (int q = 0; q < R; ++q) {
+            const int row = (warp * R + q) * 32 + lane;
+            uint32_t cs = 0;
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+              cs += prev[j][q];
+              prev[j][q] = 0;
+            }
+            if (row < E) {
+              if (cs) atomicAdd((unsigned long long*)&colsum[c_l * E + row], (unsigned long long)cs);
+              if (act[q]) atomicAdd(&active[c_l * E + row], (int)act[q]);
+            }
+            act[q] = 0;
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(W * 32) : "memory");
+          for (int i = threadIdx.x; i < G * set_words; i += W * 32) crs[i] = 0;
+          c_unit += gridDim.x;
+          c_open();
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(W * 32) : "memory");  // reads (and resets) done
+      }
+    }
+  }
+}
+
+template <int W, int R, int G, int NB, int BPW, int MINB>
+static int launch_hist_creg(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
+                            int32_t* hist, int64_t* colsum, int32_t* active, int32_t* heavy, int64_t* dropped,
+                            cudaStream_t st) {
+  const int rows = (E + 1) > 32 * R * W ? E + 1 : 32 * R * W;
+  const size_t smem = (size_t)G * rows * 32 * 4;
+  auto kern = topk_hist_creg_kernel<W, R, G, NB, BPW, MINB>;
+  GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  GEM_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t units = L * ((T + kHistStepsPerUnit - 1) / kHistStepsPerUnit);
+  int64_t blocks = (int64_t)num_sms() * per_sm;
+  if (blocks > units) blocks = units;
+  kern<<<(unsigned)blocks, W * 32, smem, st>>>((const int16_t*)ids, L, N, k, B, E, T, HT, hist, colsum, active,
+                                               dropped);
+  GEM_CHECK_LAUNCH("topk_hist_creg_kernel");
+  return launch_heavy_rows(hist, L, T, HT, E, heavy, st);
+}
+
 template <typename IdT, bool WIDE, int MAXR>
 static int launch_hist_t(const void* ids, int64_t L, int64_t N, int k, int B, int E, int64_t T, int64_t HT,
                          int32_t* hist,
@@ -628,6 +823,19 @@ static int dispatch_hist(const void* ids, int64_t L, int64_t N, int k, int B, in
   if (sizeof(IdT) == 2 && N % B == 0 && step_bytes % (kRingUnroll * 32 * 16) == 0 &&
       (reinterpret_cast<uintptr_t>(ids) & 15) == 0 && (E <= kWideMaxE || E % 2 == 0) &&
       !std::getenv("GEM_HIST_NORING")) {
+    // E in (160, 256]: the CTA-shared-counter kernel (GEM_HIST_CTA=0 disables it,
+    // =1 also takes it for smaller E); other shapes: the one-warp ring kernels
+    const char* cta_env = std::getenv("GEM_HIST_CTA");
+    const int cta_mode = cta_env ? std::atoi(cta_env) : -1;
+    const int bps = (int)(step_bytes / kCtaBatch);
+    if (cta_mode != 0 && E <= 256 && (E > kWideMaxE || cta_mode == 1)) {
+      if (bps == 8)
+        return launch_hist_creg<8, 1, 1, 3, 1, 2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
+      if (bps == 4)
+        return launch_hist_creg<4, 2, 1, 3, 1, 2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
+      if (bps == 2 && E <= 128)
+        return launch_hist_creg<2, 2, 1, 3, 1, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
+    }
     if (E <= 64) return launch_hist_ring<true, 2>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
     if (E <= 128) return launch_hist_ring<true, 4>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);
     if (E <= kWideMaxE) return launch_hist_ring<true, 5>(ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy, dropped, st);

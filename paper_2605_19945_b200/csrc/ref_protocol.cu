@@ -173,7 +173,7 @@ extern "C" int gem_ref_eval_curve_packed(const int64_t* xs_flat, const double* y
   GEM_ARENA_CHECK(err, "upload offsets");
   int64_t* ddl = ar.upload(dense_limits + gpu, 1, &err);
   GEM_ARENA_CHECK(err, "upload dense_limit");
-  int rc = gem_eval_curve(dxs, dys, doff, ddl, 0, dcounts, n, dout, (void*)st);
+  int rc = gem_eval_curve(dxs, dys, doff, ddl, 0, dcounts, n, dout, nullptr, (void*)st);
   if (rc) return rc;
   GEM_CHECK_CUDA(cudaMemcpyAsync(out, dout, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, st));
   GEM_CHECK_CUDA(cudaStreamSynchronize(st));

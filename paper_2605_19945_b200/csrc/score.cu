@@ -11,11 +11,50 @@
 
 namespace gem {
 
-__global__ void eval_curve_kernel(const int64_t* __restrict__ xs, const double* __restrict__ ys, int64_t size,
-                                  int64_t dense_limit, const int64_t* __restrict__ counts, int64_t n,
-                                  double* __restrict__ out) {
+// one GPU's curve; its bounds are read on the device (no host round trip).
+// An empty curve sets err_flag (GEM_ERR_INVALID) and leaves out untouched.
+__global__ void eval_curve_kernel(const int64_t* __restrict__ xs_flat, const double* __restrict__ ys_flat,
+                                  const int64_t* __restrict__ offsets, const int64_t* __restrict__ dense_limits,
+                                  int gpu, const int64_t* __restrict__ counts, int64_t n, double* __restrict__ out,
+                                  int32_t* __restrict__ err_flag) {
+  const int64_t o0 = offsets[gpu], o1 = offsets[gpu + 1], dl = dense_limits[gpu];
+  if (o1 <= o0) {
+    if (err_flag && blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(err_flag, 0, (int32_t)GEM_ERR_INVALID);
+    return;
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = eval_one(xs, ys, size, dense_limit, counts[i]);
+    out[i] = eval_one(xs_flat + o0, ys_flat + o0, o1 - o0, dl, counts[i]);
+}
+
+// equal_latency_load (profiles.py:308-333) on one thread: the largest n_b
+// with C_b(n_b) <= C_a(n_a), by doubling then bisection on the monotone
+// curve, saturating at max_search. Same probes in the same order as the
+// reference, each one eval_one, so the answer is the reference's.
+__global__ void equal_latency_kernel(const int64_t* __restrict__ xs_flat, const double* __restrict__ ys_flat,
+                                     const int64_t* __restrict__ offsets, const int64_t* __restrict__ dense_limits,
+                                     int ga, int gb, int64_t n_a, int64_t max_search, int64_t* __restrict__ out) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const int64_t a0 = offsets[ga], a1 = offsets[ga + 1], b0 = offsets[gb], b1 = offsets[gb + 1];
+  auto cb = [&](int64_t n) { return eval_one(xs_flat + b0, ys_flat + b0, b1 - b0, dense_limits[gb], n); };
+  const double target = eval_one(xs_flat + a0, ys_flat + a0, a1 - a0, dense_limits[ga], n_a);
+  if (cb(1) > target) {
+    *out = 0;
+    return;
+  }
+  int64_t lo = 1, hi = 2;
+  while (hi < max_search && cb(hi) <= target) {
+    lo = hi;
+    hi *= 2;
+  }
+  if (hi >= max_search) {
+    *out = lo;
+    return;
+  }
+  while (lo + 1 < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (cb(mid) <= target) lo = mid; else hi = mid;
+  }
+  *out = lo;
 }
 
 __global__ void curve_lut_kernel(const int64_t* __restrict__ xs_flat, const double* __restrict__ ys_flat,
@@ -163,20 +202,26 @@ static unsigned grid_for(int64_t n, int threads, int cap = 65535) {
 
 extern "C" int gem_eval_curve(const int64_t* xs_flat, const double* ys_flat, const int64_t* offsets,
                               const int64_t* dense_limits, int32_t gpu, const int64_t* counts, int64_t n, double* out,
-                              void* stream) {
+                              int32_t* err_flag, void* stream) {
   GEM_REQUIRE(xs_flat && ys_flat && offsets && dense_limits && gpu >= 0, "gem_eval_curve: bad arguments");
   if (n <= 0) return GEM_OK;
   GEM_REQUIRE(counts && out, "gem_eval_curve: null counts/out");
-  // offsets/dense_limits are device arrays: read this GPU's entries
-  int64_t off[2], dl;
-  cudaStream_t st = as_stream(stream);
-  GEM_CHECK_CUDA(cudaMemcpyAsync(off, offsets + gpu, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  GEM_CHECK_CUDA(cudaMemcpyAsync(&dl, dense_limits + gpu, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  GEM_CHECK_CUDA(cudaStreamSynchronize(st));
-  GEM_REQUIRE(off[1] > off[0], "gem_eval_curve: empty curve");
-  eval_curve_kernel<<<grid_for(n, 256), 256, 0, st>>>(xs_flat + off[0], ys_flat + off[0], off[1] - off[0], dl, counts,
-                                                     n, out);
+  // asynchronous: the curve's bounds are device data, read by the kernel
+  eval_curve_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(xs_flat, ys_flat, offsets, dense_limits, gpu,
+                                                                     counts, n, out, err_flag);
   GEM_CHECK_LAUNCH("eval_curve_kernel");
+  return GEM_OK;
+}
+
+extern "C" int gem_equal_latency_load(const int64_t* xs_flat, const double* ys_flat, const int64_t* offsets,
+                                      const int64_t* dense_limits, int32_t gpu_a, int32_t gpu_b, int64_t n_a,
+                                      int64_t max_search, int64_t* out, void* stream) {
+  GEM_REQUIRE(xs_flat && ys_flat && offsets && dense_limits && out && gpu_a >= 0 && gpu_b >= 0 && n_a >= 1 &&
+                  max_search >= 2,
+              "gem_equal_latency_load: bad arguments");
+  equal_latency_kernel<<<1, 32, 0, as_stream(stream)>>>(xs_flat, ys_flat, offsets, dense_limits, gpu_a, gpu_b, n_a,
+                                                        max_search, out);
+  GEM_CHECK_LAUNCH("equal_latency_kernel");
   return GEM_OK;
 }
 

@@ -37,8 +37,8 @@
 namespace gem {
 
 __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, int64_t T, int E, int n,
-                                  int32_t* __restrict__ bound, int32_t* __restrict__ top1,
-                                  int32_t* __restrict__ rowmin);  // search.cu
+                                  const int32_t* __restrict__ n_dev, int32_t* __restrict__ bound,
+                                  int32_t* __restrict__ top1, int32_t* __restrict__ rowmin);  // search.cu
 
 constexpr int kLtThreads = 256;
 constexpr int kLtN = 256;        // MMA N (candidate x GPU columns per CTA)
@@ -89,6 +89,13 @@ __global__ void window_bits_kernel(const double* __restrict__ lut, int G, int64_
     if (b >= 0x7ff0000000000000ull) atomicExch(bad, 1);  // sign bit, inf or NaN
     bits[i] = b;
   }
+}
+
+// bad = 1 if any table entry is negative, NaN or infinite (checked over the
+// whole [G][width] table so the decision is known at the one host sync)
+__global__ void lut_bad_kernel(const double* __restrict__ lut, int64_t count, int32_t* __restrict__ bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    if ((unsigned long long)__double_as_longlong(lut[i]) >= 0x7ff0000000000000ull) atomicExch(bad, 1);
 }
 
 // keys[g*W + n] = rank of lut[g][n] among the sorted distinct values
@@ -423,32 +430,33 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
     scratch.push_back(p);
     return p;
   };
-  // ---- bounds: experts per GPU, load window, largest count (one host sync)
-  // [2] cand stats, [L] top-n, [L] max, [1] smallest step total, [G] gather clamp patterns
-  int32_t* bnd_d = static_cast<int32_t*>(alloc((size_t)(3 + 2 * L + G) * 4));
+  // ---- bounds, all on the device, then ONE host sync for the launch geometry:
+  // [0] experts per GPU (maxcnt), [1] invalid entry, [2, 2+L) top-maxcnt load bound U[l],
+  // [2+L, 2+2L) largest count, [2+2L] smallest step total, [3+2L] bad table entry,
+  // [4+2L, 4+2L+G) gather clamp patterns
+  int32_t* bnd_d = static_cast<int32_t*>(alloc((size_t)(4 + 2 * L + G) * 4));
   if (!bnd_d) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc scratch");
-  GEM_CHECK_CUDA(cudaMemsetAsync(bnd_d, 0, (size_t)(2 + 2 * L) * 4, st));
+  GEM_CHECK_CUDA(cudaMemsetAsync(bnd_d, 0, (size_t)(4 + 2 * L) * 4, st));
   GEM_CHECK_CUDA(cudaMemsetAsync(bnd_d + 2 + 2 * L, 0x7f, 4, st));  // rowmin starts at 0x7f7f7f7f
   cand_stats_kernel<<<(unsigned)imin64((C * L + 7) / 8, 16 * num_sms()), 256, (size_t)8 * G * 4, st>>>(
       cand, C * L, E, G, bnd_d);
   GEM_CHECK_LAUNCH("cand_stats_kernel");
-  int32_t cs[2] = {0, 0};
-  GEM_CHECK_CUDA(cudaMemcpyAsync(cs, bnd_d, 8, cudaMemcpyDeviceToHost, st));
-  GEM_CHECK_CUDA(cudaStreamSynchronize(st));
-  if (cs[1]) return 1;  // invalid entries: the CUDA-core scorer reports them
-  const int maxcnt = cs[0] < 1 ? 1 : cs[0];
   const int warps = 8;
   const unsigned tb_grid = (unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms());
-  topn_bound_kernel<<<tb_grid, warps * 32, (size_t)warps * E * 4, st>>>(hist, L, T, E, maxcnt, bnd_d + 2,
+  topn_bound_kernel<<<tb_grid, warps * 32, (size_t)warps * E * 4, st>>>(hist, L, T, E, 1, bnd_d, bnd_d + 2,
                                                                         bnd_d + 2 + L, bnd_d + 2 + 2 * L);
   GEM_CHECK_LAUNCH("topn_bound_kernel");
-  std::vector<int32_t> bnd((size_t)2 * L);
-  GEM_CHECK_CUDA(cudaMemcpyAsync(bnd.data(), bnd_d + 2, (size_t)2 * L * 4, cudaMemcpyDeviceToHost, st));
-  GEM_CHECK_CUDA(cudaStreamSynchronize(st));
+  lut_bad_kernel<<<(unsigned)imin64(((int64_t)G * (nmax + 1) + 255) / 256, 4096), 256, 0, st>>>(
+      lut, (int64_t)G * (nmax + 1), bnd_d + 3 + 2 * L);
+  GEM_CHECK_LAUNCH("lut_bad_kernel");
+  std::vector<int32_t> bnd((size_t)4 + 2 * L);
+  GEM_CHECK_CUDA(cudaMemcpyAsync(bnd.data(), bnd_d, bnd.size() * 4, cudaMemcpyDeviceToHost, st));
+  GEM_CHECK_CUDA(cudaStreamSynchronize(st));  // the only sync when the window has <= 65,536 entries
+  if (bnd[1] || bnd[3 + 2 * L]) return 1;  // invalid entries / bad table values: the CUDA-core scorer reports them
   int64_t U = 0, hmax = 0;
   for (int64_t l = 0; l < L; ++l) {
-    U = imax64(U, bnd[l]);
-    hmax = imax64(hmax, bnd[L + l]);
+    U = imax64(U, bnd[2 + l]);
+    hmax = imax64(hmax, bnd[2 + L + l]);
   }
   if (hmax > 2048 || U > nmax || U >= 65536) return 1;  // fp16 exactness, table range
   const int W = (int)U + 1;
@@ -475,14 +483,16 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   if (!tmp) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc cub");
   GEM_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t1, bits, sorted, (int)cnt, 0, 64, st));
   GEM_CHECK_CUDA(cub::DeviceSelect::Unique(tmp, t2, sorted, uniq, nu, (int)cnt, st));
-  int32_t nk[2] = {0, 0};
-  GEM_CHECK_CUDA(cudaMemcpyAsync(nk, nu, 8, cudaMemcpyDeviceToHost, st));
-  GEM_CHECK_CUDA(cudaStreamSynchronize(st));
-  if (nk[1] || nk[0] < 1 || nk[0] > kMaxKeys) return 1;
+  if (cnt > kMaxKeys) {  // only then can the distinct count exceed the u16 key range
+    int32_t nk = 0;
+    GEM_CHECK_CUDA(cudaMemcpyAsync(&nk, nu, 4, cudaMemcpyDeviceToHost, st));
+    GEM_CHECK_CUDA(cudaStreamSynchronize(st));
+    if (nk < 1 || nk > kMaxKeys) return 1;
+  }
   key_table_kernel<<<(unsigned)imin64((cnt + 255) / 256, 4096), 256, 0, st>>>(bits, cnt, uniq, nu, keys);
   GEM_CHECK_LAUNCH("key_table_kernel");
   const double* vals = reinterpret_cast<const double*>(uniq);  // the bit patterns are the values
-  uint32_t* nbmin = reinterpret_cast<uint32_t*>(bnd_d + 3 + 2 * L);
+  uint32_t* nbmin = reinterpret_cast<uint32_t*>(bnd_d + 4 + 2 * L);
   if (std::getenv("GEM_SCORE_NOCLAMP")) {
     std::vector<uint32_t> nb0((size_t)G, 0x4B000000u);
     GEM_CHECK_CUDA(cudaMemcpyAsync(nbmin, nb0.data(), (size_t)G * 4, cudaMemcpyHostToDevice, st));

@@ -234,10 +234,12 @@ __host__ __device__ constexpr int g2_threads(int GM) { return GM >= 32 ? 256 : k
 constexpr int kGreedyUnroll = GEM_GREEDY_UNROLL;
 
 // U[l] = max_t (sum of the n largest counts of step t): one warp per step row
+// (n_dev, when given, replaces n with max(*n_dev, 1): the caller's bound stays on the device)
 __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, int64_t T, int E, int n,
-                                  int32_t* __restrict__ bound, int32_t* __restrict__ top1,
-                                  int32_t* __restrict__ rowmin) {
+                                  const int32_t* __restrict__ n_dev, int32_t* __restrict__ bound,
+                                  int32_t* __restrict__ top1, int32_t* __restrict__ rowmin) {
   extern __shared__ int32_t tb_rows[];  // [warps][E]
+  if (n_dev != nullptr) n = min(max(*n_dev, 1), E);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int32_t* row = tb_rows + (size_t)w * E;
   const int64_t rows = L * T;
@@ -1952,7 +1954,7 @@ static int prepare_screen(const int32_t* hist, int64_t L, int64_t T, int32_t E, 
   GEM_CHECK_LAUNCH("lut_monotone_kernel");
   const int warps = 8;
   topn_bound_kernel<<<(unsigned)imin64((L * T + warps - 1) / warps, 16 * num_sms()), warps * 32,
-                      (size_t)warps * E * 4, st>>>(hist, L, T, E, E / G, bound, nullptr, nullptr);
+                      (size_t)warps * E * 4, st>>>(hist, L, T, E, E / G, nullptr, bound, nullptr, nullptr);
   std::vector<int32_t> ub((size_t)L + 1);
   cudaError_t e1 = cudaGetLastError();
   cudaError_t e2 = cudaMemcpyAsync(ub.data(), bound, (size_t)(L + 1) * 4, cudaMemcpyDeviceToHost, st);

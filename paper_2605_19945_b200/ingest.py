@@ -286,13 +286,19 @@ class ClassifyConfig:
     correlation_threshold: tuple[int, int] = (4, 5)
 
 
-def classify_device(colsum, heavy, gram, num_steps: int, config: ClassifyConfig = ClassifyConfig()) -> ExpertClasses:
+def classify_device(colsum, heavy, gram, num_steps: int, config: ClassifyConfig = ClassifyConfig(),
+                    out: ExpertClasses | None = None) -> ExpertClasses:
+    """K3b on the device, asynchronously (out: optional preallocated classes; its err flag is re-zeroed)."""
     L, E = colsum.shape
-    cls = _device.empty((L, E), torch.int8)
-    grp = _device.empty((L, E), torch.int16)
+    if out is not None:
+        cls, grp, err = out.cls, out.group, out.err
+        err.zero_()
+    else:
+        cls = _device.empty((L, E), torch.int8)
+        grp = _device.empty((L, E), torch.int16)
+        err = _device.zeros((1,), torch.int32)
     cn, cd = config.consistent_fraction
     rn, rd = config.correlation_threshold
-    err = _device.zeros((1,), torch.int32)
     _lib.call("gem_classify", ptr(colsum), ptr(heavy), ptr(gram), L, num_steps, E, cn, cd, rn, rd, ptr(cls),
               ptr(grp), ptr(err), stream())
     return ExpertClasses(cls, grp, err)

@@ -72,6 +72,30 @@ def test_topk_hist_ring_path(oracle, shape):
     assert np.array_equal(h.heavy.cpu().numpy(), np.stack([oracle.heavy_counts(w) for w in want]))
 
 
+@pytest.mark.parametrize("mode", ["1", "0"])
+@pytest.mark.parametrize("shape", [(2, 64 * 1024, 8, 1024, 128), (1, 37 * 512, 8, 512, 100), (3, 33 * 1024, 8, 1024, 256),
+                                   (1, 45 * 512, 8, 512, 200), (2, 40 * 256, 8, 256, 64), (1, 35 * 1024, 8, 1024, 250),
+                                   (3, 9 * 1024, 8, 1024, 256)])
+def test_topk_hist_cta_path(oracle, monkeypatch, shape, mode):
+    """The CTA-shared-counter K1 (W warps share lane-private u32 counters, ids
+    loaded straight into registers 3 steps ahead, two named barriers per
+    step): forced on (mode 1, also E <= 128) and off (mode 0: the ring
+    kernels) give the oracle's counts -- W = 8 (8 batches per step), W = 4 and
+    W = 2 with 2 rows per lane (4 / 2 batches per step), partial 32-step
+    units, units spanning layers, out-of-range ids."""
+    monkeypatch.setenv("GEM_HIST_CTA", mode)
+    L, N, k, B, E = shape
+    rng = np.random.default_rng(sum(shape) + 1)
+    ids = rng.integers(-3, E + 3, (L, N, k)).astype(np.int16)
+    h = ingest.ids_to_histograms(torch.from_numpy(ids).cuda(), B, E, check_dropped=False)
+    want, dropped = oracle.topk_hist(ids, B, E)
+    assert np.array_equal(h.hist.cpu().numpy(), want)
+    assert np.array_equal(h.dropped.cpu().numpy(), dropped)
+    assert np.array_equal(h.colsum.cpu().numpy(), want.sum(axis=1))
+    assert np.array_equal(h.active.cpu().numpy(), (want > 0).sum(axis=1))
+    assert np.array_equal(h.heavy.cpu().numpy(), np.stack([oracle.heavy_counts(w) for w in want]))
+
+
 @pytest.mark.parametrize("E", [128, 256])
 def test_topk_hist_ring_heavy_with_sparse_drops(oracle, E):
     """Heavy-step counts on the ring path: steps are full, so the row total is

@@ -1,7 +1,7 @@
-# scratch experiment driver for gpurun (edited per call)
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out/ncu
-R=/tmp/ncu_reps; mkdir -p $R
-GEM_LIB_VARIANT=x12 ncu --set full --clock-control none --import-source on -c 1 -k regex:coselect_tc -o $R/x12 python tools/kbench.py coselect --layers 8 --reps 1 --warm 0 --paths gem_coselect_tc > /dev/null 2>&1
-ncu -i $R/x12.ncu-rep --page source --csv > gpurun_out/ncu/x12_source.csv 2>/dev/null
-python tools/ncu_summary.py $R/x12.ncu-rep > gpurun_out/ncu/x12.json
+mkdir -p gpurun_out
+timeout 600 python tools/k1_modes.py --layers 58 --experts 256 --modes 0,6,8,10,1 > gpurun_out/k1m.txt 2>&1
+timeout 600 python tools/k1_modes.py --modes 0,6,8,1 >> gpurun_out/k1m.txt 2>&1
+timeout 600 python tools/k1_modes.py --layers 16 --experts 64 --modes 0,6,1 >> gpurun_out/k1m.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q -k "topk_hist" > gpurun_out/pytest_k1.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_k1.log
+cat gpurun_out/k1m.txt; tail -2 gpurun_out/pytest_k1.log
