@@ -91,20 +91,79 @@ __global__ void window_bits_kernel(const double* __restrict__ lut, int G, int64_
   }
 }
 
-// bad = 1 if any table entry is negative, NaN or infinite (checked over the
+// bad: bit 0 if any table entry is negative, NaN or infinite (checked over the
 // whole [G][width] table so the decision is known at the one host sync)
-__global__ void lut_bad_kernel(const double* __restrict__ lut, int64_t count, int32_t* __restrict__ bad) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
-    if ((unsigned long long)__double_as_longlong(lut[i]) >= 0x7ff0000000000000ull) atomicExch(bad, 1);
+// (bit 0), and bit 1 if a row decreases anywhere (the gather clamp needs
+// nondecreasing rows; CostCurve guarantees them, the flag only guards)
+__global__ void lut_bad_kernel(const double* __restrict__ lut, int G, int64_t width, int32_t* __restrict__ bad) {
+  const int64_t count = (int64_t)G * width;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = lut[i];
+    if ((unsigned long long)__double_as_longlong(v) >= 0x7ff0000000000000ull) atomicOr(bad, 1);
+    if (i % width != 0 && v < lut[i - 1]) atomicOr(bad, 2);
+  }
 }
 
-// keys[g*W + n] = rank of lut[g][n] among the sorted distinct values
-__global__ void key_table_kernel(const unsigned long long* __restrict__ bits, int64_t count,
-                                 const unsigned long long* __restrict__ uniq, const int32_t* __restrict__ nuniq,
-                                 uint16_t* __restrict__ keys) {
+// Gather clamp, on the values (before any sort): v* = the smallest table value
+// such that sum_g cap_g(v*) >= bmin, cap_g(v) = #{n : lut[g][n] <= v}. No
+// step with >= bmin ids can have every GPU strictly below v* (its loads would
+// sum to < bmin), so every step maximum is >= v*, and a load n <= thr_g =
+// cap_g(v*) - 1 may read the latency at thr_g (<= v* <= the maximum) instead:
+// thr[g] = that index (0: no clamp for rows that are bad or decreasing).
+// One warp, lane = GPU (G <= 32); bisection on the fp64 bit patterns, which
+// order like the values for finite v >= 0.
+__global__ void value_clamp_kernel(const double* __restrict__ lut, int G, int64_t width,
+                                   const int32_t* __restrict__ bmin, const int32_t* __restrict__ bad,
+                                   int32_t* __restrict__ thr) {
+  const int g = threadIdx.x;
+  if (*bad) {
+    if (g < G) thr[g] = 0;
+    return;
+  }
+  const double* row = lut + (int64_t)(g < G ? g : 0) * width;
+  auto cap = [&](unsigned long long vb) -> int64_t {  // #{n : lut[g][n] <= v}, 0 for lanes >= G
+    if (g >= G) return 0;
+    const double v = __longlong_as_double((long long)vb);
+    int64_t lo = 0, hi = width;  // first n with row[n] > v
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (row[mid] <= v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  auto total = [&](unsigned long long vb) {
+    int64_t c = cap(vb);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    return c;
+  };
+  const int64_t need = *bmin > 0 ? *bmin : 0;
+  unsigned long long hi = 0;
+  for (int gg = 0; gg < G; ++gg) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(lut[(int64_t)gg * width + width - 1]);
+    hi = b > hi ? b : hi;
+  }
+  unsigned long long lo = 0;  // smallest bit pattern with total >= need (hi always qualifies)
+  while (lo < hi) {
+    const unsigned long long mid = lo + ((hi - lo) >> 1);
+    if (total(mid) >= need) hi = mid; else lo = mid + 1;
+  }
+  const int64_t c = cap(lo);
+  if (g < G) thr[g] = (int32_t)(c > 0 ? c - 1 : 0);
+}
+
+// packed key rows of K5 v4: keys[rb_g + n - s_g] = rank of lut[g][n] for n in
+// [s_g, U] (rowinfo: [g] = s_g, [G+g] = rb_g, [2G] = total entries)
+__global__ void key_rows_kernel(const unsigned long long* __restrict__ bits, int G, int W,
+                                const int32_t* __restrict__ rowinfo, const unsigned long long* __restrict__ uniq,
+                                const int32_t* __restrict__ nuniq, uint16_t* __restrict__ keys) {
   const int K = *nuniq;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long b = bits[i];
+  const int total = rowinfo[2 * G];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    int g = 0;
+    while (g + 1 < G && rowinfo[G + g + 1] <= i) ++g;
+    const int n = rowinfo[g] + (i - rowinfo[G + g]);
+    const unsigned long long b = bits[(int64_t)g * W + n];
     int lo = 0, hi = K - 1;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
@@ -114,66 +173,45 @@ __global__ void key_table_kernel(const unsigned long long* __restrict__ bits, in
   }
 }
 
-// Gather clamp (as in K6 v5). thr_g(K) = the largest load whose key on GPU g
-// is <= K. If every GPU's key were <= K, the step could hold at most
-// sum_g thr_g(K) ids; so with LB = the smallest K whose sum reaches the
-// smallest step total bmin (the water-filling level), every step's maximum
-// key is >= LB. A load n <= thr_g(LB) may then read key[g][thr_g(LB)]
-// instead without changing the maximum, and all such lanes share one address.
-// out[g] = 0x4B000000 + thr_g(LB) (the fp32 bit pattern of 2^23 + thr: the
-// epilogue clamps the pattern directly).
-__global__ void key_clamp_kernel(const uint16_t* __restrict__ keys, int G, int W, const int32_t* __restrict__ bmin,
-                                 uint32_t* __restrict__ out) {
-  if (threadIdx.x != 0) return;
-  auto thr = [&](int g, int K) {  // largest n with key[g][n] <= K, -1 if none (rows are nondecreasing)
-    const uint16_t* row = keys + (int64_t)g * W;
-    if (row[0] > K) return -1;
-    int lo = 0, hi = W - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (row[mid] <= K) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-  };
-  const int64_t need = max(*bmin, 0);
-  int klo = 0, khi = 0;
-  for (int g = 0; g < G; ++g) khi = max(khi, (int)keys[(int64_t)g * W + W - 1]);
-  while (klo < khi) {  // smallest K with sum_g (thr_g(K) + 1) >= need (K = khi always qualifies)
-    const int mid = (klo + khi) >> 1;
-    int64_t cap = 0;
-    for (int g = 0; g < G; ++g) cap += thr(g, mid) + 1;
-    if (cap >= need) khi = mid; else klo = mid + 1;
-  }
-  for (int g = 0; g < G; ++g) out[g] = 0x4B000000u + (uint32_t)max(thr(g, klo), 0);
-}
-
 // ---------------------------------------------------------------------------
-// pass 1: CTA = (candidate tile of CT = N/G candidates, layer of the batch);
-// loops over every 128-step tile of the layer in order: produce the fp16 H
-// tile, one thread issues the E/16 MMAs, all warps drain TMEM into keys.
+// pass 1 (v4): CTA = (candidate tile of CT = N/G candidates, layer of the
+// batch); walks every 128-step tile of the layer in order.
+//
+// Loads on tcgen05 kind::i8 with exact integer accumulators: a count h < 4096
+// is split into u8 limbs lo = h & 255 and hi16 = 16*(h >> 8) (<= 240); the A
+// tile holds [lo | hi16] along K (K = 2E bytes per step row) and the one-hot
+// B holds [O | 16*O], so D = sum lo*O + sum 16hi*16O is the load n itself in
+// s32 (v3 used fp16 values and fp32 sums: one FADD per load to recover n).
+// The epilogue maps n straight to the shared-memory address of its order key:
+// GPU g's key row only covers [s_g, U] (s_g = the gather clamp: a load below
+// it reads the key at s_g, which never exceeds the step maximum), so
+// addr = max(2n + koff_g, base_g) -- LEA + max, one LDS.U16, one max per GPU
+// -- and the compressed rows free shared memory for longer load windows.
 template <int E, int G>
 __global__ void __launch_bounds__(kLtThreads, 1)
 maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __restrict__ cand, int64_t C,
-                 int64_t L, int64_t layer0, int64_t Cp, const uint16_t* __restrict__ gkeys, int W,
-                 const uint32_t* __restrict__ nbmin_g, uint16_t* __restrict__ out_keys) {
-  constexpr int KCH = E / 8;                 // 16-byte K chunks (8 fp16 experts)
+                 int64_t L, int64_t layer0, int64_t Cp, const uint16_t* __restrict__ gkeys, int keys_total,
+                 const int32_t* __restrict__ rowinfo, uint16_t* __restrict__ out_keys) {
+  constexpr int KB = 2 * E;                  // K bytes per step row: [lo | hi16]
+  constexpr int KCH = KB / 16;               // 16-byte K chunks
   constexpr uint32_t LBO_A = 128 * 16 + 16;  // A: [KCH][128 rows][16 B], K slices padded by 16 B (bank spread)
   constexpr uint32_t LBO_B = kLtN * 16;      // B: [KCH][N rows][16 B]
   constexpr int A_BYTES = (int)LBO_A * KCH;
-  constexpr int B_BYTES = kLtN * E * 2;
+  constexpr int B_BYTES = kLtN * KB;
   constexpr int CT = kLtN / G;               // candidates per CTA
   constexpr int KPT = CT / 2;                // keys per thread per tile (one column half)
   constexpr int CPL = 32 / G;                // candidates per 32-column TMEM load
   constexpr int STG_ROW = KPT * 2 + 16;      // staging row: the thread's keys + 16 B pad
   constexpr int STG_BYTES = 8 * 32 * STG_ROW;
-  static_assert(STG_BYTES <= A_BYTES, "key staging must fit the H tile");
+  static_assert(STG_BYTES <= A_BYTES, "key staging must fit the A tile");
   static_assert(G >= 4 && G <= 32 && (kLtN % G) == 0, "G in {4, 8, 16, 32}");
   extern __shared__ __align__(1024) unsigned char lt_smem[];
   unsigned char* sa = lt_smem;
   unsigned char* sb = lt_smem + A_BYTES;
   LoadsTcShared* sh = reinterpret_cast<LoadsTcShared*>(sb + B_BYTES);
-  uint16_t* skeys = reinterpret_cast<uint16_t*>(sb + B_BYTES + 64);  // [G][W]
-  unsigned char* stg = sa;  // the H tile's space, free once the tile's MMAs completed
+  int32_t* sinfo = reinterpret_cast<int32_t*>(sb + B_BYTES + 64);        // [2G]: koff, base
+  uint16_t* skeys = reinterpret_cast<uint16_t*>(sb + B_BYTES + 64 + 256);  // packed key rows
+  unsigned char* stg = sa;  // the A tile's space, free once the tile's MMAs completed
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * CT;
@@ -187,21 +225,32 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
     tc::fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc<kLtN>(&sh->tmem_base);
-  {  // key table -> shared memory (16-byte pieces)
-    const int pieces = (W * G * 2 + 15) / 16;
-    for (int i = tid; i < pieces; i += blockDim.x)
+  {  // key rows -> shared memory (16-byte pieces; the global copy is padded to 16 bytes)
+    const int pieces = (keys_total * 2 + 15) / 16;
+    for (int i = tid; i < pieces; i += kLtThreads)
       reinterpret_cast<uint4*>(skeys)[i] = __ldg(reinterpret_cast<const uint4*>(gkeys) + i);
   }
-  // one-hot B: row r = j*G + g (candidate j of the tile, GPU g), 1.0 where cand == g
-  for (int i = tid; i < kLtN * KCH; i += blockDim.x) {
+  if (tid < G) {
+    // rowinfo: [g] = s_g (first load of the row), [G+g] = row offset (entries)
+    const int32_t sk = (int32_t)tc::smem_u32(skeys);
+    const int32_t s0 = rowinfo[tid], rb = rowinfo[G + tid];
+    sinfo[tid] = sk + 2 * (rb - s0);  // koff: 2n + koff = address of key[g][n]
+    sinfo[G + tid] = sk + 2 * rb;     // base: address of key[g][s_g]
+  }
+  // one-hot B: row r = j*G + g (candidate j of the tile, GPU g); K chunk q < E/16
+  // holds experts 16q.. as 1, chunk q >= E/16 the same experts as 16
+  for (int i = tid; i < kLtN * KCH; i += kLtThreads) {
     const int r = i / KCH, q = i % KCH;
     uint32_t w[4] = {0u, 0u, 0u, 0u};
     const int j = r / G, g = r % G;
+    const bool hiq = q >= E / 16;
+    const int e0 = (hiq ? q - E / 16 : q) * 16;
+    const uint32_t one = hiq ? 16u : 1u;
     if (c0 + j < C) {
-      const int8_t* m = cand + ((c0 + j) * L + l) * E + q * 8;
+      const int8_t* m = cand + ((c0 + j) * L + l) * E + e0;
 #pragma unroll
-      for (int x = 0; x < 8; ++x)
-        if (m[x] == g) w[x >> 1] |= 0x3C00u << ((x & 1) * 16);
+      for (int x = 0; x < 16; ++x)
+        if (m[x] == g) w[x >> 2] |= one << ((x & 3) * 8);
     }
     *reinterpret_cast<uint4*>(sb + (size_t)q * LBO_B + (size_t)r * 16) = make_uint4(w[0], w[1], w[2], w[3]);
   }
@@ -211,10 +260,15 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
   tc::tc_fence_after();
   const uint32_t tmem = sh->tmem_base;
   const uint32_t sa_addr = tc::smem_u32(sa), sb_addr = tc::smem_u32(sb);
-  const uint32_t sk_addr = tc::smem_u32(skeys);
-  const uint32_t idesc = tc::instr_desc(/*F32*/ 1, /*F16*/ 0, /*F16*/ 0, 128, kLtN);
+  const uint32_t idesc = tc::instr_desc(/*S32*/ 2, /*u8*/ 0, /*u8*/ 0, 128, kLtN);
   const int ntiles = (int)((T + 127) / 128);
   const int lg = warp & 3, half = warp >> 2;
+  int32_t koff[G], kbase[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    koff[g] = sinfo[g];
+    kbase[g] = sinfo[G + g];
+  }
 
   // H rows: each warp reads whole rows (coalesced), the next tile's rows are in
   // flight during the current tile's MMA and epilogue
@@ -231,36 +285,30 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
       x[v] = t < T ? __ldg(reinterpret_cast<const int4*>(hl + t * E) + (lane % LPR)) : make_int4(0, 0, 0, 0);
     }
   };
-  // per-GPU row offsets into the key table (bytes), biased by the fp32 exponent
-  // pattern so that (bits of n + 2^23) * 2 + off[g] addresses key[g][n]
-  uint32_t koff[G], nbmin[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    koff[g] = sk_addr + 2u * (uint32_t)g * (uint32_t)W - 2u * 0x4B000000u;
-    nbmin[g] = nbmin_g[g];
-  }
   load_rows(0);
   for (int i = 0; i < ntiles; ++i) {
-    // ---- H tile i: exact int -> fp32 (2^23 trick) -> packed fp16 pairs, 8-byte K-major stores
+    // ---- A tile i: u8 limbs, lo bytes at K = e, 16*hi at K = E + e (h < 4096)
 #pragma unroll
     for (int v = 0; v < NX; ++v) {
       const int row = warp * RPW + v * RPI + lane / LPR;
       const int e4 = lane % LPR;  // experts 4*e4 .. 4*e4+3
-      auto f = [](int a) { return __uint_as_float(0x4B000000u | (uint32_t)a) - 8388608.0f; };
-      const __half2 p0 = __floats2half2_rn(f(x[v].x), f(x[v].y));
-      const __half2 p1 = __floats2half2_rn(f(x[v].z), f(x[v].w));
-      *reinterpret_cast<uint2*>(sa + (size_t)(e4 >> 1) * LBO_A + (size_t)row * 16 + (e4 & 1) * 8) =
-          make_uint2(*reinterpret_cast<const uint32_t*>(&p0), *reinterpret_cast<const uint32_t*>(&p1));
+      const uint32_t lo = __byte_perm(__byte_perm((uint32_t)x[v].x, (uint32_t)x[v].y, 0x0040),
+                                      __byte_perm((uint32_t)x[v].z, (uint32_t)x[v].w, 0x0040), 0x5410);
+      const uint32_t hi = __byte_perm(__byte_perm((uint32_t)x[v].x, (uint32_t)x[v].y, 0x0051),
+                                      __byte_perm((uint32_t)x[v].z, (uint32_t)x[v].w, 0x0051), 0x5410) << 4;
+      unsigned char* rowp = sa + (size_t)row * 16 + (e4 & 3) * 4;
+      *reinterpret_cast<uint32_t*>(rowp + (size_t)(e4 >> 2) * LBO_A) = lo;
+      *reinterpret_cast<uint32_t*>(rowp + (size_t)(E / 16 + (e4 >> 2)) * LBO_A) = hi;
     }
     tc::fence_async_smem();
     __syncthreads();
     if (tid == 0) {
       tc::tc_fence_after();
 #pragma unroll
-      for (int k = 0; k < E / 16; ++k) {
+      for (int k = 0; k < KB / 32; ++k) {
         const uint64_t ad = tc::smem_desc(sa_addr + k * 2 * LBO_A, LBO_A, 128);
         const uint64_t bd = tc::smem_desc(sb_addr + k * 2 * LBO_B, LBO_B, 128);
-        tc::mma_f16(tmem, ad, bd, idesc, k > 0 ? 1u : 0u);
+        tc::mma_i8(tmem, ad, bd, idesc, k > 0 ? 1u : 0u);
       }
       tc::mma_commit(&sh->mma_bar);
     }
@@ -268,8 +316,8 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
     tc::mbar_wait(&sh->mma_bar, (uint32_t)(i & 1));
     tc::tc_fence_after();
     // ---- epilogue: warp w drains TMEM lanes 32(w%4).. (one step per lane) and
-    // column half w/4 in 32-column chunks; load n of GPU g -> key[g][n]; the
-    // maximum over a candidate's G columns is its step key
+    // column half w/4 in 32-column chunks; load n of GPU g -> key; the maximum
+    // over a candidate's G columns is its step key
     {
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16);
       uint32_t kk[KPT];
@@ -283,9 +331,7 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
           uint32_t m = 0;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
-            // exact integer n < 2^16 in fp32: + 2^23 puts it in the low mantissa bits
-            const uint32_t nb = __float_as_uint(__uint_as_float(v[j * G + g]) + 8388608.0f);
-            const uint32_t addr = max(nb, nbmin[g]) * 2u + koff[g];
+            const int32_t addr = max((int32_t)v[j * G + g] * 2 + koff[g], kbase[g]);
             uint16_t key;
             asm("ld.shared.u16 %0, [%1];" : "=h"(key) : "r"(addr));
             m = max(m, (uint32_t)key);
@@ -293,14 +339,14 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
           kk[ch * CPL + j] = m;
         }
       }
-      // the H tile is free (its MMAs completed): stage the keys, then store rows
+      // the A tile is free (its MMAs completed): stage the keys, then store rows
       // of KPT keys (2*KPT bytes) per step, 16-byte pieces
       unsigned char* wst = stg + warp * 32 * STG_ROW;
 #pragma unroll
-      for (int x = 0; x < KPT / 8; ++x)
-        *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x * 16) =
-            make_uint4(kk[8 * x] | (kk[8 * x + 1] << 16), kk[8 * x + 2] | (kk[8 * x + 3] << 16),
-                       kk[8 * x + 4] | (kk[8 * x + 5] << 16), kk[8 * x + 6] | (kk[8 * x + 7] << 16));
+      for (int x8 = 0; x8 < KPT / 8; ++x8)
+        *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x8 * 16) =
+            make_uint4(kk[8 * x8] | (kk[8 * x8 + 1] << 16), kk[8 * x8 + 2] | (kk[8 * x8 + 3] << 16),
+                       kk[8 * x8 + 4] | (kk[8 * x8 + 5] << 16), kk[8 * x8 + 6] | (kk[8 * x8 + 7] << 16));
       if (KPT % 8 == 4)
         *reinterpret_cast<uint2*>(wst + lane * STG_ROW + (KPT / 8) * 16) =
             make_uint2(kk[KPT - 4] | (kk[KPT - 3] << 16), kk[KPT - 2] | (kk[KPT - 1] << 16));
@@ -323,7 +369,7 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
       }
     }
     tc::tc_fence_before();
-    __syncthreads();  // TMEM and the H tile are free for tile i+1
+    __syncthreads();  // TMEM and the A tile are free for tile i+1
   }
   if (warp == 0) tc::tmem_dealloc<kLtN>(tmem);
 }
@@ -381,10 +427,10 @@ keysum_kernel(const uint16_t* __restrict__ keys, int64_t T, int64_t C, int64_t C
 template <int E>
 static int launch_maxkey(int G, dim3 grid, size_t smem, cudaStream_t st, const int32_t* hist, int64_t T,
                          const int8_t* cand, int64_t C, int64_t L, int64_t l0, int64_t Cp, const uint16_t* keys,
-                         int W, const uint32_t* nbmin, uint16_t* out) {
+                         int keys_total, const int32_t* rowinfo, uint16_t* out) {
   auto pick = [&](auto kern) -> int {
     GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, kLtThreads, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, W, nbmin, out);
+    kern<<<grid, kLtThreads, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, keys_total, rowinfo, out);
     GEM_CHECK_LAUNCH("maxkey_tc_kernel");
     return GEM_OK;
   };
@@ -409,7 +455,7 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
                                   int32_t* err_flag, void* stream) {
   (void)err_flag;
   if (!(E == 64 || E == 128) || !(G == 4 || G == 8 || G == 16 || G == 32) || (E == 64 && G == 4)) return 1;
-  if (T < 1 || C < 1 || nmax < 0) return 1;
+  if (T < 1 || C < 1 || nmax < 0 || L > 65535) return 1;
   cudaStream_t st = as_stream(stream);
   keep_pool();
   int dev = 0, optin = 0;
@@ -432,11 +478,12 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   };
   // ---- bounds, all on the device, then ONE host sync for the launch geometry:
   // [0] experts per GPU (maxcnt), [1] invalid entry, [2, 2+L) top-maxcnt load bound U[l],
-  // [2+L, 2+2L) largest count, [2+2L] smallest step total, [3+2L] bad table entry,
-  // [4+2L, 4+2L+G) gather clamp patterns
-  int32_t* bnd_d = static_cast<int32_t*>(alloc((size_t)(4 + 2 * L + G) * 4));
+  // [2+L, 2+2L) largest count, [2+2L] smallest step total, [3+2L] bad table flags,
+  // [4+2L, 4+2L+G) gather clamp thr_g (value level)
+  const int64_t NB = 4 + 2 * L + G;
+  int32_t* bnd_d = static_cast<int32_t*>(alloc((size_t)NB * 4));
   if (!bnd_d) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc scratch");
-  GEM_CHECK_CUDA(cudaMemsetAsync(bnd_d, 0, (size_t)(4 + 2 * L) * 4, st));
+  GEM_CHECK_CUDA(cudaMemsetAsync(bnd_d, 0, (size_t)NB * 4, st));
   GEM_CHECK_CUDA(cudaMemsetAsync(bnd_d + 2 + 2 * L, 0x7f, 4, st));  // rowmin starts at 0x7f7f7f7f
   cand_stats_kernel<<<(unsigned)imin64((C * L + 7) / 8, 16 * num_sms()), 256, (size_t)8 * G * 4, st>>>(
       cand, C * L, E, G, bnd_d);
@@ -447,23 +494,35 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
                                                                         bnd_d + 2 + L, bnd_d + 2 + 2 * L);
   GEM_CHECK_LAUNCH("topn_bound_kernel");
   lut_bad_kernel<<<(unsigned)imin64(((int64_t)G * (nmax + 1) + 255) / 256, 4096), 256, 0, st>>>(
-      lut, (int64_t)G * (nmax + 1), bnd_d + 3 + 2 * L);
+      lut, G, nmax + 1, bnd_d + 3 + 2 * L);
   GEM_CHECK_LAUNCH("lut_bad_kernel");
-  std::vector<int32_t> bnd((size_t)4 + 2 * L);
-  GEM_CHECK_CUDA(cudaMemcpyAsync(bnd.data(), bnd_d, bnd.size() * 4, cudaMemcpyDeviceToHost, st));
+  value_clamp_kernel<<<1, 32, 0, st>>>(lut, G, nmax + 1, bnd_d + 2 + 2 * L, bnd_d + 3 + 2 * L, bnd_d + 4 + 2 * L);
+  GEM_CHECK_LAUNCH("value_clamp_kernel");
+  std::vector<int32_t> bnd((size_t)NB);
+  GEM_CHECK_CUDA(cudaMemcpyAsync(bnd.data(), bnd_d, (size_t)NB * 4, cudaMemcpyDeviceToHost, st));
   GEM_CHECK_CUDA(cudaStreamSynchronize(st));  // the only sync when the window has <= 65,536 entries
-  if (bnd[1] || bnd[3 + 2 * L]) return 1;  // invalid entries / bad table values: the CUDA-core scorer reports them
+  if (bnd[1] || (bnd[3 + 2 * L] & 1)) return 1;  // invalid entries / bad table values: the CUDA-core scorer reports them
   int64_t U = 0, hmax = 0;
   for (int64_t l = 0; l < L; ++l) {
     U = imax64(U, bnd[2 + l]);
     hmax = imax64(hmax, bnd[2 + L + l]);
   }
-  if (hmax > 2048 || U > nmax || U >= 65536) return 1;  // fp16 exactness, table range
+  if (U > nmax || U >= 65536) return 1;  // table range
   const int W = (int)U + 1;
-  const size_t key_bytes = (((size_t)W * G * 2) + 15) & ~size_t(15);
-  const size_t a_bytes = (size_t)(128 * 16 + 16) * (E / 8);
-  const size_t lt_smem = a_bytes + (size_t)kLtN * E * 2 + 64 + key_bytes;
-  if (lt_smem > (size_t)optin) return 1;
+  // key rows [s_g, U], s_g = min(thr_g, U): rowinfo [g] = s_g, [G+g] = row offset, [2G] = total
+  std::vector<int32_t> rowinfo((size_t)2 * G + 1);
+  int keys_total = 0;
+  const bool noclamp = std::getenv("GEM_SCORE_NOCLAMP") != nullptr;
+  for (int g = 0; g < G; ++g) {
+    const int sg = noclamp ? 0 : (int)imin64(imax64(bnd[4 + 2 * L + g], 0), U);
+    rowinfo[g] = sg;
+    rowinfo[G + g] = keys_total;
+    keys_total += W - sg;
+  }
+  rowinfo[2 * G] = keys_total;
+  const size_t key_bytes = (((size_t)keys_total * 2) + 15) & ~size_t(15);
+  const size_t lt_smem = (size_t)(128 * 16 + 16) * (2 * E / 16) + (size_t)kLtN * 2 * E + 64 + 256 + key_bytes;
+  if (hmax > 4095 || lt_smem > (size_t)optin) return 1;  // u8 limbs (h < 4096), shared memory
 
   // ---- order keys of the load window: sort the distinct fp64 values
   const int64_t cnt = (int64_t)G * W;
@@ -472,8 +531,11 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   auto* uniq = static_cast<unsigned long long*>(alloc((size_t)cnt * 8));
   auto* nu = static_cast<int32_t*>(alloc(8));  // [0] distinct count, [1] bad entry flag
   auto* keys = static_cast<uint16_t*>(alloc(key_bytes));
-  if (!bits || !sorted || !uniq || !nu || !keys) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc keys");
+  int32_t* rowinfo_d = static_cast<int32_t*>(alloc(rowinfo.size() * 4));
+  if (!bits || !sorted || !uniq || !nu || !keys || !rowinfo_d)
+    return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc keys");
   GEM_CHECK_CUDA(cudaMemsetAsync(nu, 0, 8, st));
+  GEM_CHECK_CUDA(cudaMemcpyAsync(rowinfo_d, rowinfo.data(), rowinfo.size() * 4, cudaMemcpyHostToDevice, st));
   window_bits_kernel<<<(unsigned)imin64((cnt + 255) / 256, 4096), 256, 0, st>>>(lut, G, nmax + 1, W, bits, nu + 1);
   GEM_CHECK_LAUNCH("window_bits_kernel");
   size_t t1 = 0, t2 = 0;
@@ -489,17 +551,10 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
     GEM_CHECK_CUDA(cudaStreamSynchronize(st));
     if (nk < 1 || nk > kMaxKeys) return 1;
   }
-  key_table_kernel<<<(unsigned)imin64((cnt + 255) / 256, 4096), 256, 0, st>>>(bits, cnt, uniq, nu, keys);
-  GEM_CHECK_LAUNCH("key_table_kernel");
+  key_rows_kernel<<<(unsigned)imin64((keys_total + 255) / 256, 4096), 256, 0, st>>>(bits, G, W, rowinfo_d, uniq, nu,
+                                                                                    keys);
+  GEM_CHECK_LAUNCH("key_rows_kernel");
   const double* vals = reinterpret_cast<const double*>(uniq);  // the bit patterns are the values
-  uint32_t* nbmin = reinterpret_cast<uint32_t*>(bnd_d + 4 + 2 * L);
-  if (std::getenv("GEM_SCORE_NOCLAMP")) {
-    std::vector<uint32_t> nb0((size_t)G, 0x4B000000u);
-    GEM_CHECK_CUDA(cudaMemcpyAsync(nbmin, nb0.data(), (size_t)G * 4, cudaMemcpyHostToDevice, st));
-  } else {
-    key_clamp_kernel<<<1, 32, 0, st>>>(keys, G, W, bnd_d + 2 + 2 * L, nbmin);
-    GEM_CHECK_LAUNCH("key_clamp_kernel");
-  }
 
   // ---- layer batches: P layers of u16 step keys [P][T][Cp] in flight (<= ~32 GB)
   const int CT = kLtN / G;
@@ -517,8 +572,10 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   for (int64_t l0 = 0; l0 < L; l0 += P) {
     const int64_t nb = imin64(P, L - l0);
     const dim3 g1((unsigned)ntile, (unsigned)nb);
-    const int rc = E == 128 ? launch_maxkey<128>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, W, nbmin, kbuf)
-                            : launch_maxkey<64>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, W, nbmin, kbuf);
+    const int rc = E == 128 ? launch_maxkey<128>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, keys_total,
+                                                 rowinfo_d, kbuf)
+                            : launch_maxkey<64>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, keys_total,
+                                                rowinfo_d, kbuf);
     if (rc) return rc;
     keysum_kernel<<<dim3((unsigned)((C + 4 * kSumThreads - 1) / (4 * kSumThreads)), (unsigned)nb), kSumThreads,
                     (size_t)kSumSmemVals * 8, st>>>(
