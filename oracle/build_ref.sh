@@ -8,6 +8,12 @@ set -euo pipefail
 HERE="$(cd "$(dirname "$0")" && pwd)"
 SRC=/root/reference/pkg
 [ -d "$SRC" ] || { echo "no /root/reference: keeping existing oracle/_ref" >&2; exit 0; }
+# the reference's own test suite + fixtures, run against this package by
+# tests/test_reference_suite.py (git-ignored like the rest of oracle/_ref)
+if [ ! -f "$HERE/_ref/ref_tests/conftest.py" ]; then
+  mkdir -p "$HERE/_ref/ref_tests"
+  cp -r "$SRC/tests/." "$HERE/_ref/ref_tests/"
+fi
 if [ -f "$HERE/_ref/gemap/__init__.py" ] && ls "$HERE"/_ref/gemap/_kernels*.so >/dev/null 2>&1; then exit 0; fi
 TMP="$(mktemp -d /tmp/gemref.XXXXXX)"
 cp -r "$SRC" "$TMP/pkg"          # the build writes into its source tree; /root/reference is read-only

@@ -97,6 +97,48 @@ class SearchResult:
 # host-side job preparation
 
 
+class _Instance:
+    """Packed profile arrays and per-step loads of one (trace, profile) pair, in
+    the layout of the kernel-backend protocol (/root/reference/pkg/src/gemap/search.py:98-131).
+
+    The protocol's callers (the reference's own tests, third-party drivers of
+    `kernels.get_backend(...)`) build their arguments with this; the device
+    search does not use it. Loads come from the device replay (gem_replay),
+    latencies from the backend the caller passes."""
+
+    def __init__(self, trace: ExpertTrace, profile: VariabilityProfile):
+        self.tokens = np.ascontiguousarray(trace.tokens, dtype=np.int64)
+        self.num_steps, self.num_experts = self.tokens.shape
+        self.num_gpus = profile.num_gpus
+        _check_divisible(self.num_experts, self.num_gpus)
+        self.capacity = self.num_experts // self.num_gpus
+        self._trace, self._profile = trace, profile
+        sizes = [c.num_samples for c in profile.curves]
+        self.offsets = np.concatenate(([0], np.cumsum(sizes))).astype(np.int64)
+        self.xs_flat = np.concatenate([c.token_counts for c in profile.curves]).astype(np.int64)
+        self.ys_flat = np.concatenate([c.latencies for c in profile.curves]).astype(np.float64)
+        self.dense_limits = np.asarray([c.dense_limit for c in profile.curves], dtype=np.int64)
+        for a in (self.tokens, self.offsets, self.xs_flat, self.ys_flat, self.dense_limits):
+            a.setflags(write=False)
+
+    def curve_args(self) -> tuple:
+        return (self.xs_flat, self.ys_flat, self.offsets, self.dense_limits)
+
+    def eval_gpu(self, backend, gpu: int, counts) -> np.ndarray:
+        return backend.eval_curve_packed(*self.curve_args(), gpu, counts)
+
+    def load_matrix(self, assignment: np.ndarray) -> np.ndarray:
+        """[T, G] int64 tokens per GPU per step (device replay)."""
+        from .mapping import replay_loads
+        return replay_loads(self._trace, ExpertMapping(np.asarray(assignment, dtype=np.int64), self.num_gpus))
+
+    def latency_matrix(self, backend, loads: np.ndarray) -> np.ndarray:
+        lat = np.empty(loads.shape, dtype=np.float64)
+        for g in range(self.num_gpus):
+            lat[:, g] = self.eval_gpu(backend, g, loads[:, g])
+        return lat
+
+
 def _restart_order(mean_util: np.ndarray, restart_index: int, rng: np.random.Generator,
                    noise_fraction: float) -> np.ndarray:
     keys = np.asarray(mean_util, dtype=np.float64)
