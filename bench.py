@@ -235,6 +235,7 @@ def run_ours(args):
             if timed:
                 evs[i].record(stream)
 
+        torch.cuda.nvtx.range_push("bench.stats_step")
         mark(0)
         _lib.call("gem_topk_hist", ids.data_ptr(), 2, L, n_local, k, B, E, hist.data_ptr(), ds.colsum.data_ptr(),
                   ds.active.data_ptr(), ds.heavy.data_ptr(), dropped.data_ptr(), stream.cuda_stream)
@@ -248,6 +249,7 @@ def run_ours(args):
         mark(4)
         cls = ingest.classify_device(ds.colsum, ds.heavy, ds.gram, T, out=cls_out)
         mark(5)
+        torch.cuda.nvtx.range_pop()
         if timed:
             kev.append((evs[0], evs[1]))
             pev.append(evs)
@@ -351,6 +353,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
         def e2e_step():
+            torch.cuda.nvtx.range_push("bench.e2e_step")
             dev_ids.copy_(host_ids, non_blocking=True)
             if use_dist:
                 ss = dist_mod.sharded_statistics(dev_ids, plan, ops, B, E)
@@ -361,6 +364,7 @@ def run_ours(args):
                 st.check()
             res = (mu.to("cpu", non_blocking=True), cls.to("cpu", non_blocking=True))
             torch.cuda.current_stream().synchronize()
+            torch.cuda.nvtx.range_pop()
             return res
 
         e2e_step()
@@ -425,7 +429,9 @@ def run_ours(args):
             return gm.score_candidates_device(hist_own, nmax, profile, cand_d)
 
         score_all()  # warm-up (LUT build, module load)
+        torch.cuda.nvtx.range_push("bench.candidates")
         (total, _), cms = dev_time(score_all)
+        torch.cuda.nvtx.range_pop()
         best = int(torch.argmin(total).item())
         result["candidates"] = {"value": C / (cms / 1e3), "unit": "candidate mappings/s", "ms": cms,
                                 "candidates": C, "layers": L, "steps": T, "best_index": best,
@@ -449,7 +455,9 @@ def run_ours(args):
 
         def ttm_info(Tw):
             ttm(Tw)  # warm-up: module load, stream-ordered pool growth (~1.5 GB of search scratch), LUT build
+            torch.cuda.nvtx.range_push(f"bench.time_to_mapping[{Tw}]")
             (shm, results), tms = dev_time(lambda: ttm(Tw))
+            torch.cuda.nvtx.range_pop()
             info = {"value": tms / 1e3, "unit": "s", "steps_searched": Tw, "layers": L,
                     "runs_per_layer": cfg.restarts + 2, "timing": "CUDA events on the launching stream, max over ranks",
                     "includes": "K1..K3b statistics, all-to-all to layer owners (N>1), greedy + refinement of every run"}

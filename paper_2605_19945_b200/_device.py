@@ -26,6 +26,22 @@ def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def nvtx(name: str):
+    """Decorator: an NVTX range around the call (visible in Nsight Systems / ncu --nvtx)."""
+    def wrap(fn):
+        import functools
+
+        @functools.wraps(fn)
+        def inner(*a, **kw):
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*a, **kw)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        return inner
+    return wrap
+
+
 def stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 

@@ -170,6 +170,7 @@ class Histograms:
         return [ExpertTrace(h[l]) for l in range(h.shape[0])]
 
 
+@_device.nvtx("gem.K1 ids_to_histograms")
 def ids_to_histograms(ids: torch.Tensor, tokens_per_step: int, num_experts: int,
                       hist: torch.Tensor | None = None, check_dropped: bool = True,
                       with_gram: bool = True, with_coselect: bool = False) -> Histograms:
@@ -328,6 +329,7 @@ class TraceStatistics:
                           _device.host(self.correlation[l]))
 
 
+@_device.nvtx("gem.trace_statistics")
 def trace_statistics(ids: torch.Tensor, tokens_per_step: int, num_experts: int, correlation: bool = True,
                      classify: bool = True, config: ClassifyConfig = ClassifyConfig(),
                      coselect: bool = False) -> TraceStatistics:
@@ -348,6 +350,7 @@ def finalize_statistics(h: Histograms, correlation: bool = True, classify: bool 
     return TraceStatistics(h, ds.gram, mu, af, corr, classes)
 
 
+@_device.nvtx("gem.K2-K3b statistics")
 def statistics_from_histograms(h: Histograms, correlation: bool = True, classify: bool = True,
                                config: ClassifyConfig = ClassifyConfig()) -> TraceStatistics:
     compute_gram(h)

@@ -268,6 +268,7 @@ class RunResults:
 TRAJ_INITIAL_WIDTH = 256  # trajectory columns allocated up front (runs measured: <= 16 swaps at C4)
 
 
+@_device.nvtx("gem.K6-K8 search runs")
 def run_search_device(hist: torch.Tensor, nmax: int, profile: VariabilityProfile, batch: RunBatch,
                       threshold: float, swap_cap: int) -> RunResults:
     """Run greedy + refinement for every run of `batch` on the device."""
@@ -388,6 +389,7 @@ def search_layers(traces, profile: VariabilityProfile, config: SearchConfig | No
     return out
 
 
+@_device.nvtx("gem.search_hist")
 def search_hist(hist: torch.Tensor, nmax: int, profile: VariabilityProfile, config: SearchConfig,
                 mean_util: np.ndarray | None = None) -> list[SearchResult]:
     """Search every layer of a device histogram [L,T,E] int32."""
