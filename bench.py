@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-coselect", action="store_true", help="skip the K2b co-selection leg")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--search-steps", type=int, default=None, help="search window (default: all steps)")
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
+                    help="gloo: functional check of the N>1 code path with several ranks on one GPU "
+                         "(collectives staged through host memory; not a performance number)")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the sharded (torch.distributed) code path even on one GPU")
     return ap.parse_args()
@@ -187,12 +190,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    dev = local % max(torch.cuda.device_count(), 1)  # gloo check: several ranks may share a GPU
+    torch.cuda.set_device(dev)
     use_dist = world > 1 or args.force_dist
     if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29511")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev), rank=rank, world_size=world)
+        else:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
     L, N, k, E, B, G, C = CONFIGS[args.config]
     if args.candidates:
         C = args.candidates
@@ -261,7 +268,7 @@ def run_ours(args):
     if use_dist:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    with Clocks(dev) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
@@ -419,14 +426,16 @@ def run_ours(args):
         base = np.repeat(np.arange(G, dtype=np.int8), E // G)
         cand = rng.permuted(np.broadcast_to(base, (C * L, E)), axis=1).reshape(C, L, E)
         cand_d = torch.from_numpy(np.ascontiguousarray(cand)).cuda()
-        hist_own = owned_hist()
         nmax = B * k
-        l0, l1 = plan.layer_range()
+        c0, c1 = plan.candidate_range(C)
 
         def score_all():
+            # N>1: candidates split by index; every rank needs every layer's
+            # full-length rows (one all-gather of the token-range shards, timed)
             if use_dist:
-                return dist_mod.sharded_candidate_scores(hist_own, plan, ops, profile, cand_d, nmax)
-            return gm.score_candidates_device(hist_own, nmax, profile, cand_d)
+                hist_full = dist_mod.allgather_hist(hist, plan)
+                return dist_mod.sharded_candidate_scores(hist_full, plan, ops, profile, cand_d, nmax)
+            return gm.score_candidates_device(hist, nmax, profile, cand_d)
 
         score_all()  # warm-up (LUT build, module load)
         torch.cuda.nvtx.range_push("bench.candidates")
@@ -436,8 +445,9 @@ def run_ours(args):
         result["candidates"] = {"value": C / (cms / 1e3), "unit": "candidate mappings/s", "ms": cms,
                                 "candidates": C, "layers": L, "steps": T, "best_index": best,
                                 "best_score": float(total[best].item()),
-                                "sharding": f"layers {l0}..{l1 - 1} on this rank of {world}" if use_dist
-                                else "single GPU"}
+                                "sharding": f"candidates {c0}..{c1 - 1} on this rank of {world} (all-gather of "
+                                            f"the histogram shards + one all-gather of the scores, timed)"
+                                if use_dist else "single GPU"}
         del cand_d
 
     if not args.no_search:

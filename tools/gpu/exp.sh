@@ -1,6 +1,5 @@
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out/ncu
-bash tools/config_sweep.sh > gpurun_out/sweep.txt 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu/launches_c5.csv python bench.py --config deepseek-v3 --steps 1 --warmup 3 --no-e2e --no-cpu --no-coselect --no-candidates > /dev/null 2>&1
-python tools/launches.py gpurun_out/ncu/launches_c5.csv > gpurun_out/launches_c5.txt 2>&1
-cat gpurun_out/sweep.txt; head -30 gpurun_out/launches_c5.txt
+mkdir -p gpurun_out
+timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --dist-backend gloo --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_gloo2.json 2> gpurun_out/bench_gloo2.err; echo "rc=$?" >> gpurun_out/bench_gloo2.err
+timeout 900 python bench.py --force-dist --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_fd.json 2> gpurun_out/bench_fd.err; echo "rc=$?" >> gpurun_out/bench_fd.err
+tail -5 gpurun_out/bench_gloo2.err; cut -c1-1500 gpurun_out/bench_gloo2.json; tail -2 gpurun_out/bench_fd.err; cut -c1-600 gpurun_out/bench_fd.json
