@@ -17,6 +17,7 @@
 //    then the full rescore must equal cand bit for bit (search.py:236).
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "gem_common.cuh"
@@ -301,12 +302,19 @@ __global__ void hist_t16_kernel(const int32_t* __restrict__ hist, int64_t T, int
 // FULL: G == GM (no padded GPU columns: the per-GPU guards vanish at compile time)
 // SL: the fp32 table window [G][W] sits in shared memory; otherwise (G = 32
 // with a wide window) the gathers read ws.lut32 through L1/L2
-template <int GM, bool FULL, bool SL>
+// TOP2 (monotone fp64 table rows): every step's exact top-2 of the current
+// latencies is kept in global memory and updated after each placement (only
+// the chosen GPU's latency changes, and it can only grow), so the max over
+// the OTHER GPUs of GPU g is (g == arg ? D2 : D1) -- no per-placement
+// re-gather of all G current latencies in the approximate pass (fp32: the
+// rounding of D1/D2, rounding being monotone) nor in the exact re-scores.
+template <int GM, bool FULL, bool SL, bool TOP2>
 __global__ void __launch_bounds__(g2_threads(GM), 1)
 greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
                const double* __restrict__ lut, int64_t nmax, int W, const int32_t* __restrict__ run_layer,
                const uint8_t* __restrict__ needs_greedy, const int16_t* __restrict__ order,
-               int8_t* __restrict__ assign, uint16_t* __restrict__ loads16, SearchWs ws) {
+               int8_t* __restrict__ assign, uint16_t* __restrict__ loads16, SearchWs ws,
+               float2* __restrict__ top_p, double2* __restrict__ top_d, uint8_t* __restrict__ top_a) {
   const int G = FULL ? GM : G_;
   extern __shared__ __align__(16) unsigned char g2s[];
   float* s_lut = reinterpret_cast<float*>(g2s);                                        // [G][W] (SL)
@@ -325,6 +333,7 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
   const int32_t* h = hist + layer * T * E;
   const uint16_t* hl = ws.ht16 + layer * E * ws.Tp;
   uint16_t* ld = loads16 + r * T * GM;  // row stride GM (padded), unused GPUs stay 0
+  auto LDI = [&](int64_t t, int g) -> int64_t { return t * GM + g; };
   if (SL)
     for (int i = tid; i < G * W; i += blockDim.x) {
       const int g = i / W, nn = i - g * W;
@@ -338,6 +347,20 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
   if (tid < GM) counts[tid] = 0;
   if (tid == 0) s_exc = 0u;
   for (int64_t i = tid; i < T * GM; i += blockDim.x) ld[i] = 0;
+  float2* tp = nullptr;
+  double2* td = nullptr;
+  uint8_t* ta = nullptr;
+  if (TOP2) {  // no load yet: every latency is C_g(0) = 0; one GPU has no "others" (-inf)
+    tp = top_p + r * T;
+    td = top_d + r * T;
+    ta = top_a + r * T;
+    const float ninf = __int_as_float(0xff800000);
+    for (int64_t t = tid; t < T; t += blockDim.x) {
+      tp[t] = make_float2(0.0f, G > 1 ? 0.0f : ninf);
+      td[t] = make_double2(0.0, G > 1 ? 0.0 : (double)ninf);
+      ta[t] = 0;
+    }
+  }
   const int cap = E / G;
   __syncthreads();
   for (int idx = 0; idx < E; ++idx) {
@@ -363,9 +386,16 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
       acc[g] = 0.0;
       row_addr[g] = lut_base + 4u * (uint32_t)(g < G ? g : G - 1) * (uint32_t)W;
     }
+    {
 #pragma unroll kGreedyUnroll
     for (int64_t t = tid; t < T; t += blockDim.x) {
       const uint32_t hv = (uint32_t)hcol[t];
+      float2 p12;
+      int parg = 0;
+      if (TOP2) {
+        p12 = tp[t];
+        parg = ta[t];
+      }
       uint32_t lrow[GM];
       if (GM == 8) {
         const uint4 v = *reinterpret_cast<const uint4*>(ld + t * GM);
@@ -377,27 +407,31 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
         for (int g = 0; g < GM; ++g) lrow[g] = ld[t * GM + g];
       }
       // rows of GPUs g >= G (GM padding) read row G-1 and are masked by select: no branches
-      float cur[GM], pre[GM + 1], suf[GM + 1];
+      float pre[GM + 1], suf[GM + 1];
+      if (!TOP2) {
+        float cur[GM];
 #pragma unroll
-      for (int g = 0; g < GM; ++g) {
-        const float v = tab(row_addr, g, lrow[g]);
-        cur[g] = g < G ? v : __int_as_float(0xff800000);
+        for (int g = 0; g < GM; ++g) {
+          const float v = tab(row_addr, g, lrow[g]);
+          cur[g] = g < G ? v : __int_as_float(0xff800000);
+        }
+        pre[0] = __int_as_float(0xff800000);
+        suf[GM] = __int_as_float(0xff800000);
+#pragma unroll
+        for (int g = 0; g < GM; ++g) pre[g + 1] = fmaxf(pre[g], cur[g]);
+#pragma unroll
+        for (int g = GM - 1; g >= 0; --g) suf[g] = fmaxf(suf[g + 1], cur[g]);
       }
-      pre[0] = __int_as_float(0xff800000);
-      suf[GM] = __int_as_float(0xff800000);
-#pragma unroll
-      for (int g = 0; g < GM; ++g) pre[g + 1] = fmaxf(pre[g], cur[g]);
-#pragma unroll
-      for (int g = GM - 1; g >= 0; --g) suf[g] = fmaxf(suf[g + 1], cur[g]);
 #pragma unroll
       for (int g = 0; g < GM; ++g) {
         // a GPU with free capacity never exceeds the window (l + h <= U); a
         // full one (ignored by the selection) is clamped to stay inside it
         const float cl = tab(row_addr, g, min(lrow[g] + hv, wlast));
-        const float pm = fmaxf(pre[g], suf[g + 1]);
+        const float pm = TOP2 ? (g == parg ? p12.y : p12.x) : fmaxf(pre[g], suf[g + 1]);
         acc[g] += (double)fmaxf(pm, cl);  // g >= G: ignored by the selection
         if (hv != 0u && cl >= pm) exc |= 1u << g;  // hv == 0: the term is the step maximum exactly
       }
+    }
     }
 #pragma unroll
     for (int g = 0; g < GM; ++g) {
@@ -448,18 +482,24 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
         const int tn = (int)imin64(kGreedyTChunk, T - t0);
         for (int tt = tid; tt < tn; tt += blockDim.x) {
           const int64_t t = t0 + tt;
-          const uint16_t* lrow = ld + t * GM;
           double m1 = -1.0, m2 = -1.0;
           int i1 = -1;
-          for (int q = 0; q < G; ++q) {
-            const double v = __ldg(lut + q * width + lrow[q]);
-            if (v > m1) { m2 = m1; m1 = v; i1 = q; }
-            else if (v > m2) { m2 = v; }
+          if (TOP2) {
+            const double2 d = td[t];
+            m1 = d.x;
+            m2 = d.y;
+            i1 = ta[t];
+          } else {
+            for (int q = 0; q < G; ++q) {
+              const double v = __ldg(lut + q * width + ld[LDI(t, q)]);
+              if (v > m1) { m2 = m1; m1 = v; i1 = q; }
+              else if (v > m2) { m2 = v; }
+            }
           }
           const int hv = h[t * E + e];
           for (int c = 0; c < nc; ++c) {
             const int g = s_cand[c];
-            const double cl = __ldg(lut + g * width + (int64_t)lrow[g] + hv);
+            const double cl = __ldg(lut + g * width + (int64_t)ld[LDI(t, g)] + hv);
             double scv = cl;
             if (G > 1) {
               const double others = (i1 == g) ? m2 : m1;
@@ -497,12 +537,44 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
       for (int u = 0; u < kUpd; ++u) {
         const int64_t t = t0 + (int64_t)u * blockDim.x;
         hv[u] = t < T ? hcol[t] : 0u;
-        lv[u] = t < T ? ld[t * GM + bg] : 0u;
+        lv[u] = t < T ? ld[LDI(t, bg)] : 0u;
       }
 #pragma unroll
       for (int u = 0; u < kUpd; ++u) {
         const int64_t t = t0 + (int64_t)u * blockDim.x;
-        if (t < T) ld[t * GM + bg] = (uint16_t)(lv[u] + hv[u]);
+        if (t < T) ld[LDI(t, bg)] = (uint16_t)(lv[u] + hv[u]);
+      }
+      if (TOP2) {  // the chosen GPU's latency grew where the expert has tokens
+        double nl[kUpd];
+        double2 d[kUpd];
+        int a[kUpd];
+#pragma unroll
+        for (int u = 0; u < kUpd; ++u) {
+          const int64_t t = t0 + (int64_t)u * blockDim.x;
+          const bool on = t < T && hv[u] != 0u;
+          nl[u] = on ? __ldg(lut + (int64_t)bg * width + lv[u] + hv[u]) : 0.0;
+          d[u] = on ? td[t] : make_double2(0.0, 0.0);
+          a[u] = on ? ta[t] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kUpd; ++u) {
+          const int64_t t = t0 + (int64_t)u * blockDim.x;
+          if (!(t < T && hv[u] != 0u)) continue;
+          double d1 = d[u].x, d2 = d[u].y;
+          int ar = a[u];
+          if (ar == bg) {
+            d1 = nl[u];  // the maximum grew (it was bg's); the runner-up is unchanged
+          } else if (nl[u] > d1) {
+            d2 = d1;
+            d1 = nl[u];
+            ar = bg;
+          } else if (nl[u] > d2) {
+            d2 = nl[u];
+          }
+          td[t] = make_double2(d1, d2);
+          tp[t] = make_float2((float)d1, (float)d2);
+          ta[t] = (uint8_t)ar;
+        }
       }
     }
     if (tid == 0) {
@@ -513,7 +585,7 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
   }
   // hand the loads to the refinement in the int32 [T][G] layout
   int32_t* out = ws.loads + r * T * G;
-  for (int64_t i = tid; i < T * G; i += blockDim.x) out[i] = ld[(i / G) * GM + (i % G)];
+  for (int64_t i = tid; i < T * G; i += blockDim.x) out[i] = ld[LDI(i / G, (int)(i % G))];
 }
 
 // loads for seeded runs (or all runs when all_runs)
@@ -1882,26 +1954,47 @@ static int launch_greedy(const int32_t* hist, int64_t T, int32_t E, int32_t G, c
     if (smem <= (size_t)optin) {
       uint16_t* l16 = nullptr;  // uint16 per-run loads, stream-ordered scratch
       GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&l16), (size_t)R * T * GM * 2, st));
+      // per-step exact top-2 state (monotone fp64 rows only; GEM_GREEDY_NOTOP2=1 disables it)
+      // (only for the off-chip table: with the table in shared memory the 8
+      // re-gathers per step are cheaper than the state traffic, 74 vs 102 ms at C4)
+      const bool top2 = ws.lut_monotone64 && !sl && G <= 255 && !std::getenv("GEM_GREEDY_NOTOP2");
+      float2* tp = nullptr;
+      double2* td = nullptr;
+      uint8_t* ta = nullptr;
+      if (top2) {
+        GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tp), (size_t)R * T * sizeof(float2), st));
+        GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&td), (size_t)R * T * sizeof(double2), st));
+        GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ta), (size_t)R * T, st));
+      }
       auto go = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         kern<<<(unsigned)R, g2_threads(GM), smem, st>>>(hist, T, E, G, lut, nmax, W, run_layer, needs_greedy, order,
-                                                    assign, l16, ws);
+                                                    assign, l16, ws, tp, td, ta);
         return cudaGetLastError();
       };
-      const cudaError_t ek =
-          sl ? (GM == G ? (GM == 8 ? go(greedy2_kernel<8, true, true>)
-                                   : (GM == 16 ? go(greedy2_kernel<16, true, true>) : go(greedy2_kernel<32, true, true>)))
-                        : (GM == 8 ? go(greedy2_kernel<8, false, true>)
-                                   : (GM == 16 ? go(greedy2_kernel<16, false, true>)
-                                               : go(greedy2_kernel<32, false, true>))))
-             : (GM == G ? (GM == 8 ? go(greedy2_kernel<8, true, false>)
-                                   : (GM == 16 ? go(greedy2_kernel<16, true, false>)
-                                               : go(greedy2_kernel<32, true, false>)))
-                        : (GM == 8 ? go(greedy2_kernel<8, false, false>)
-                                   : (GM == 16 ? go(greedy2_kernel<16, false, false>)
-                                               : go(greedy2_kernel<32, false, false>))));
+      auto pick = [&](auto tag) -> cudaError_t {
+        constexpr bool T2 = decltype(tag)::value;
+        return sl ? (GM == G ? (GM == 8 ? go(greedy2_kernel<8, true, true, T2>)
+                                        : (GM == 16 ? go(greedy2_kernel<16, true, true, T2>)
+                                                    : go(greedy2_kernel<32, true, true, T2>)))
+                             : (GM == 8 ? go(greedy2_kernel<8, false, true, T2>)
+                                        : (GM == 16 ? go(greedy2_kernel<16, false, true, T2>)
+                                                    : go(greedy2_kernel<32, false, true, T2>))))
+                  : (GM == G ? (GM == 8 ? go(greedy2_kernel<8, true, false, T2>)
+                                        : (GM == 16 ? go(greedy2_kernel<16, true, false, T2>)
+                                                    : go(greedy2_kernel<32, true, false, T2>)))
+                             : (GM == 8 ? go(greedy2_kernel<8, false, false, T2>)
+                                        : (GM == 16 ? go(greedy2_kernel<16, false, false, T2>)
+                                                    : go(greedy2_kernel<32, false, false, T2>))));
+      };
+      const cudaError_t ek = top2 ? pick(std::true_type{}) : pick(std::false_type{});
       cudaFreeAsync(l16, st);
+      if (top2) {
+        cudaFreeAsync(tp, st);
+        cudaFreeAsync(td, st);
+        cudaFreeAsync(ta, st);
+      }
       if (ek != cudaSuccess) return fail_cuda(ek, "greedy2_kernel");
       return GEM_OK;
     }

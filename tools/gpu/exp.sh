@@ -1,5 +1,11 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --dist-backend gloo --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_gloo2.json 2> gpurun_out/bench_gloo2.err; echo "rc=$?" >> gpurun_out/bench_gloo2.err
-timeout 900 python bench.py --force-dist --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_fd.json 2> gpurun_out/bench_fd.err; echo "rc=$?" >> gpurun_out/bench_fd.err
-tail -5 gpurun_out/bench_gloo2.err; cut -c1-1500 gpurun_out/bench_gloo2.json; tail -2 gpurun_out/bench_fd.err; cut -c1-600 gpurun_out/bench_fd.json
+timeout 1500 python -m pytest tests -m gpu -x -q -k "search or greedy or refine or initial or config_slice or fullsize" > gpurun_out/pytest_k7.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_k7.log
+tail -2 gpurun_out/pytest_k7.log
+for c in deepseek-v3 qwen3-235b; do
+GEM_SEARCH_TRACE=1 timeout 900 python bench.py --config $c --steps 1 --warmup 3 --no-cpu --no-e2e --no-coselect --no-candidates > gpurun_out/tr_$c.json 2> gpurun_out/tr_$c.err
+echo "$c $(grep greedy gpurun_out/tr_$c.err | sed -n 2p) $(python -c "
+import json
+d=json.loads(open('gpurun_out/tr_$c.json').read().strip().splitlines()[-1]); print(d['time_to_mapping']['value'], d['time_to_mapping']['aggregate_score'], d['time_to_mapping_w16']['value'], d['time_to_mapping_w16']['aggregate_score'])")"
+done
+grep -i misaligned gpurun_out/tr_*.err | head -3
