@@ -77,19 +77,6 @@ __global__ void cand_stats_kernel(const int8_t* __restrict__ cand, int64_t rows,
   }
 }
 
-// bits[g*W + n] = the fp64 pattern of lut[g][n] for n < W (monotone in the
-// value for finite v >= 0); bad = 1 on a negative, NaN or infinite entry
-__global__ void window_bits_kernel(const double* __restrict__ lut, int G, int64_t width, int W,
-                                   unsigned long long* __restrict__ bits, int32_t* __restrict__ bad) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)G * W;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int g = (int)(i / W);
-    const int64_t n = i - (int64_t)g * W;
-    const unsigned long long b = (unsigned long long)__double_as_longlong(lut[g * width + n]);
-    if (b >= 0x7ff0000000000000ull) atomicExch(bad, 1);  // sign bit, inf or NaN
-    bits[i] = b;
-  }
-}
 
 // bad: bit 0 if any table entry is negative, NaN or infinite (checked over the
 // whole [G][width] table so the decision is known at the one host sync)
@@ -154,22 +141,37 @@ __global__ void value_clamp_kernel(const double* __restrict__ lut, int G, int64_
 
 // packed key rows of K5 v4: keys[rb_g + n - s_g] = rank of lut[g][n] for n in
 // [s_g, U] (rowinfo: [g] = s_g, [G+g] = rb_g, [2G] = total entries)
-__global__ void key_rows_kernel(const unsigned long long* __restrict__ bits, int G, int W,
+template <typename KT>
+__global__ void key_rows_kernel(const double* __restrict__ lut, int64_t width, int G, int W,
                                 const int32_t* __restrict__ rowinfo, const unsigned long long* __restrict__ uniq,
-                                const int32_t* __restrict__ nuniq, uint16_t* __restrict__ keys) {
+                                const int32_t* __restrict__ nuniq, KT* __restrict__ keys) {
   const int K = *nuniq;
   const int total = rowinfo[2 * G];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     int g = 0;
     while (g + 1 < G && rowinfo[G + g + 1] <= i) ++g;
     const int n = rowinfo[g] + (i - rowinfo[G + g]);
-    const unsigned long long b = bits[(int64_t)g * W + n];
+    if (n >= W) continue;  // row padding of the [G][WG] layout (never read: loads <= U = W - 1)
+    const unsigned long long b = (unsigned long long)__double_as_longlong(lut[(int64_t)g * width + n]);
     int lo = 0, hi = K - 1;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if (uniq[mid] < b) lo = mid + 1; else hi = mid;
     }
-    keys[i] = (uint16_t)lo;
+    keys[i] = (KT)lo;
+  }
+}
+
+// bits[i] = the fp64 pattern of lut[g][n] over the packed rows n in [s_g, U]
+// (rowinfo as in key_rows_kernel): only these values can be gathered
+__global__ void row_bits_kernel(const double* __restrict__ lut, int64_t width, int G,
+                                const int32_t* __restrict__ rowinfo, unsigned long long* __restrict__ bits) {
+  const int total = rowinfo[2 * G];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    int g = 0;
+    while (g + 1 < G && rowinfo[G + g + 1] <= i) ++g;
+    const int n = rowinfo[g] + (i - rowinfo[G + g]);
+    bits[i] = (unsigned long long)__double_as_longlong(lut[(int64_t)g * width + n]);
   }
 }
 
@@ -187,30 +189,43 @@ __global__ void key_rows_kernel(const unsigned long long* __restrict__ bits, int
 // it reads the key at s_g, which never exceeds the step maximum), so
 // addr = max(2n + koff_g, base_g) -- LEA + max, one LDS.U16, one max per GPU
 // -- and the compressed rows free shared memory for longer load windows.
-template <int E, int G>
+// KH: the A tile holds E/KH experts (one K part: [lo | hi16] of those
+// experts); KH = 2 for E = 256 stages the two halves through the same A
+// buffer (two MMA batches into one accumulator), so the B one-hot (K = 2E
+// bytes per column) and the key rows fit beside it.
+// SPLIT: the key rows do not fit shared memory (G = 32 with wide load
+// windows): shared memory holds the first WS keys of every row (uniform
+// stride, loads [s_g, s_g + WS)), the full rows [s_g, U] stay in a global
+// [G][WG] table (L2) for the rest; each gather is one predicated LDS or LDG.
+// KT: u16 keys, or u32 when the window holds more than 65,536 distinct latencies.
+template <int E, int G, int KH, bool SPLIT, typename KT>
 __global__ void __launch_bounds__(kLtThreads, 1)
 maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __restrict__ cand, int64_t C,
-                 int64_t L, int64_t layer0, int64_t Cp, const uint16_t* __restrict__ gkeys, int keys_total,
-                 const int32_t* __restrict__ rowinfo, uint16_t* __restrict__ out_keys) {
-  constexpr int KB = 2 * E;                  // K bytes per step row: [lo | hi16]
-  constexpr int KCH = KB / 16;               // 16-byte K chunks
+                 int64_t L, int64_t layer0, int64_t Cp, const KT* __restrict__ gkeys, int keys_total,
+                 const int32_t* __restrict__ rowinfo, int WS, int WG, KT* __restrict__ out_keys) {
+  constexpr int KBY = (int)sizeof(KT);       // bytes per key
+  constexpr int EH = E / KH;                 // experts per K part
+  constexpr int KBH = 2 * EH;                // K bytes per step row per part: [lo | hi16]
+  constexpr int KCH = KBH / 16;              // 16-byte K chunks per part
   constexpr uint32_t LBO_A = 128 * 16 + 16;  // A: [KCH][128 rows][16 B], K slices padded by 16 B (bank spread)
-  constexpr uint32_t LBO_B = kLtN * 16;      // B: [KCH][N rows][16 B]
+  constexpr uint32_t LBO_B = kLtN * 16;      // B: [KH][KCH][N rows][16 B]
   constexpr int A_BYTES = (int)LBO_A * KCH;
-  constexpr int B_BYTES = kLtN * KB;
+  constexpr int B_BYTES = kLtN * KBH * KH;
   constexpr int CT = kLtN / G;               // candidates per CTA
   constexpr int KPT = CT / 2;                // keys per thread per tile (one column half)
   constexpr int CPL = 32 / G;                // candidates per 32-column TMEM load
-  constexpr int STG_ROW = KPT * 2 + 16;      // staging row: the thread's keys + 16 B pad
+  constexpr int STG_ROW = KPT * KBY + 16;    // staging row: the thread's keys + 16 B pad
   constexpr int STG_BYTES = 8 * 32 * STG_ROW;
   static_assert(STG_BYTES <= A_BYTES, "key staging must fit the A tile");
   static_assert(G >= 4 && G <= 32 && (kLtN % G) == 0, "G in {4, 8, 16, 32}");
+  static_assert(EH == 64 || EH == 128, "K parts of 64 or 128 experts");
+  constexpr int KPP = 16 / KBY;              // keys per 16-byte piece
   extern __shared__ __align__(1024) unsigned char lt_smem[];
   unsigned char* sa = lt_smem;
   unsigned char* sb = lt_smem + A_BYTES;
   LoadsTcShared* sh = reinterpret_cast<LoadsTcShared*>(sb + B_BYTES);
-  int32_t* sinfo = reinterpret_cast<int32_t*>(sb + B_BYTES + 64);        // [2G]: koff, base
-  uint16_t* skeys = reinterpret_cast<uint16_t*>(sb + B_BYTES + 64 + 256);  // packed key rows
+  int32_t* sinfo = reinterpret_cast<int32_t*>(sb + B_BYTES + 64);        // [2G]: koff, base (or s_g)
+  KT* skeys = reinterpret_cast<KT*>(sb + B_BYTES + 64 + 256);  // packed key rows (SPLIT: [G][WS])
   unsigned char* stg = sa;  // the A tile's space, free once the tile's MMAs completed
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -218,33 +233,41 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
   const int64_t lb = blockIdx.y;  // layer within the batch
   const int64_t l = layer0 + lb;
   const int32_t* hl = hist + l * T * E;
-  uint16_t* out = out_keys + lb * T * Cp;
+  KT* out = out_keys + lb * T * Cp;
 
   if (tid == 0) {
     tc::mbar_init(&sh->mma_bar, 1);
     tc::fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc<kLtN>(&sh->tmem_base);
-  {  // key rows -> shared memory (16-byte pieces; the global copy is padded to 16 bytes)
-    const int pieces = (keys_total * 2 + 15) / 16;
+  if (!SPLIT) {  // key rows -> shared memory (16-byte pieces; the global copy is padded to 16 bytes)
+    const int pieces = (keys_total * KBY + 15) / 16;
     for (int i = tid; i < pieces; i += kLtThreads)
       reinterpret_cast<uint4*>(skeys)[i] = __ldg(reinterpret_cast<const uint4*>(gkeys) + i);
+  } else {  // the first WS keys of every [G][WG] row (WS, WG multiples of 8)
+    const int pr = WS / KPP;
+    for (int i = tid; i < G * pr; i += kLtThreads) {
+      const int g = i / pr, q = i - g * pr;
+      reinterpret_cast<uint4*>(skeys)[i] = __ldg(reinterpret_cast<const uint4*>(gkeys + (int64_t)g * WG) + q);
+    }
   }
   if (tid < G) {
     // rowinfo: [g] = s_g (first load of the row), [G+g] = row offset (entries)
     const int32_t sk = (int32_t)tc::smem_u32(skeys);
     const int32_t s0 = rowinfo[tid], rb = rowinfo[G + tid];
-    sinfo[tid] = sk + 2 * (rb - s0);  // koff: 2n + koff = address of key[g][n]
-    sinfo[G + tid] = sk + 2 * rb;     // base: address of key[g][s_g]
+    sinfo[tid] = SPLIT ? s0 : sk + KBY * (rb - s0);  // koff: KBY*n + koff = address of key[g][n]
+    sinfo[G + tid] = sk + KBY * rb;                   // base: address of key[g][s_g]
   }
-  // one-hot B: row r = j*G + g (candidate j of the tile, GPU g); K chunk q < E/16
-  // holds experts 16q.. as 1, chunk q >= E/16 the same experts as 16
-  for (int i = tid; i < kLtN * KCH; i += kLtThreads) {
-    const int r = i / KCH, q = i % KCH;
+  // one-hot B: row r = j*G + g (candidate j of the tile, GPU g); in K part p,
+  // chunk q < EH/16 holds experts p*EH + 16q.. as 1, chunk q >= EH/16 the
+  // same experts as 16
+  for (int i = tid; i < kLtN * KCH * KH; i += kLtThreads) {
+    const int r = i / (KCH * KH), qq = i % (KCH * KH);
+    const int part = qq / KCH, q = qq % KCH;
     uint32_t w[4] = {0u, 0u, 0u, 0u};
     const int j = r / G, g = r % G;
-    const bool hiq = q >= E / 16;
-    const int e0 = (hiq ? q - E / 16 : q) * 16;
+    const bool hiq = q >= EH / 16;
+    const int e0 = part * EH + (hiq ? q - EH / 16 : q) * 16;
     const uint32_t one = hiq ? 16u : 1u;
     if (c0 + j < C) {
       const int8_t* m = cand + ((c0 + j) * L + l) * E + e0;
@@ -252,7 +275,7 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
       for (int x = 0; x < 16; ++x)
         if (m[x] == g) w[x >> 2] |= one << ((x & 3) * 8);
     }
-    *reinterpret_cast<uint4*>(sb + (size_t)q * LBO_B + (size_t)r * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(sb + (size_t)qq * LBO_B + (size_t)r * 16) = make_uint4(w[0], w[1], w[2], w[3]);
   }
   tc::fence_async_smem();
   tc::tc_fence_before();
@@ -267,54 +290,71 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     koff[g] = sinfo[g];
-    kbase[g] = sinfo[G + g];
+    if (!SPLIT) kbase[g] = sinfo[G + g];
   }
+  const uint32_t sk_addr = tc::smem_u32(skeys);
 
-  // H rows: each warp reads whole rows (coalesced), the next tile's rows are in
-  // flight during the current tile's MMA and epilogue
+  // H rows of one K part: each warp reads whole rows (coalesced); the next
+  // part's rows are in flight during the current part's MMA (and epilogue)
   constexpr int RPW = 128 / (kLtThreads / 32);  // rows per warp (16)
-  constexpr int LPR = E / 4;                     // lanes per row (4 experts each)
+  constexpr int LPR = EH / 4;                    // lanes per row (4 experts each)
   constexpr int RPI = 32 / LPR;                  // rows per warp instruction
   constexpr int NX = RPW / RPI;
   int4 x[NX];
-  auto load_rows = [&](int i) {
+  auto load_rows = [&](int i, int part) {
 #pragma unroll
     for (int v = 0; v < NX; ++v) {
       const int row = warp * RPW + v * RPI + lane / LPR;
       const int64_t t = (int64_t)i * 128 + row;
-      x[v] = t < T ? __ldg(reinterpret_cast<const int4*>(hl + t * E) + (lane % LPR)) : make_int4(0, 0, 0, 0);
+      x[v] = t < T ? __ldg(reinterpret_cast<const int4*>(hl + t * E + part * EH) + (lane % LPR))
+                   : make_int4(0, 0, 0, 0);
     }
   };
-  load_rows(0);
-  for (int i = 0; i < ntiles; ++i) {
-    // ---- A tile i: u8 limbs, lo bytes at K = e, 16*hi at K = E + e (h < 4096)
+  auto write_a = [&]() {  // u8 limbs, lo bytes at K = e, 16*hi at K = EH + e (h < 4096)
 #pragma unroll
     for (int v = 0; v < NX; ++v) {
       const int row = warp * RPW + v * RPI + lane / LPR;
-      const int e4 = lane % LPR;  // experts 4*e4 .. 4*e4+3
+      const int e4 = lane % LPR;  // experts 4*e4 .. 4*e4+3 of the part
       const uint32_t lo = __byte_perm(__byte_perm((uint32_t)x[v].x, (uint32_t)x[v].y, 0x0040),
                                       __byte_perm((uint32_t)x[v].z, (uint32_t)x[v].w, 0x0040), 0x5410);
       const uint32_t hi = __byte_perm(__byte_perm((uint32_t)x[v].x, (uint32_t)x[v].y, 0x0051),
                                       __byte_perm((uint32_t)x[v].z, (uint32_t)x[v].w, 0x0051), 0x5410) << 4;
       unsigned char* rowp = sa + (size_t)row * 16 + (e4 & 3) * 4;
       *reinterpret_cast<uint32_t*>(rowp + (size_t)(e4 >> 2) * LBO_A) = lo;
-      *reinterpret_cast<uint32_t*>(rowp + (size_t)(E / 16 + (e4 >> 2)) * LBO_A) = hi;
+      *reinterpret_cast<uint32_t*>(rowp + (size_t)(EH / 16 + (e4 >> 2)) * LBO_A) = hi;
     }
     tc::fence_async_smem();
-    __syncthreads();
+  };
+  auto issue_mma = [&](int part) {
     if (tid == 0) {
       tc::tc_fence_after();
 #pragma unroll
-      for (int k = 0; k < KB / 32; ++k) {
+      for (int k = 0; k < KBH / 32; ++k) {
         const uint64_t ad = tc::smem_desc(sa_addr + k * 2 * LBO_A, LBO_A, 128);
-        const uint64_t bd = tc::smem_desc(sb_addr + k * 2 * LBO_B, LBO_B, 128);
-        tc::mma_i8(tmem, ad, bd, idesc, k > 0 ? 1u : 0u);
+        const uint64_t bd = tc::smem_desc(sb_addr + (part * KCH + k * 2) * LBO_B, LBO_B, 128);
+        tc::mma_i8(tmem, ad, bd, idesc, (part > 0 || k > 0) ? 1u : 0u);
       }
       tc::mma_commit(&sh->mma_bar);
     }
-    if (i + 1 < ntiles) load_rows(i + 1);
-    tc::mbar_wait(&sh->mma_bar, (uint32_t)(i & 1));
-    tc::tc_fence_after();
+  };
+  uint32_t mma_phase = 0;
+  load_rows(0, 0);
+  for (int i = 0; i < ntiles; ++i) {
+#pragma unroll
+    for (int part = 0; part < KH; ++part) {
+      write_a();
+      __syncthreads();
+      issue_mma(part);
+      if (part + 1 < KH) load_rows(i, part + 1);
+      else if (i + 1 < ntiles) load_rows(i + 1, 0);
+      tc::mbar_wait(&sh->mma_bar, mma_phase);
+      mma_phase ^= 1u;
+      tc::tc_fence_after();
+      if (part + 1 < KH) {
+        tc::tc_fence_before();
+        __syncthreads();  // the A buffer is free for the next part
+      }
+    }
     // ---- epilogue: warp w drains TMEM lanes 32(w%4).. (one step per lane) and
     // column half w/4 in 32-column chunks; load n of GPU g -> key; the maximum
     // over a candidate's G columns is its step key
@@ -331,38 +371,70 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
           uint32_t m = 0;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
-            const int32_t addr = max((int32_t)v[j * G + g] * 2 + koff[g], kbase[g]);
-            uint16_t key;
-            asm("ld.shared.u16 %0, [%1];" : "=h"(key) : "r"(addr));
-            m = max(m, (uint32_t)key);
+            uint32_t key;
+            if (!SPLIT) {
+              const int32_t addr = max((int32_t)v[j * G + g] * KBY + koff[g], kbase[g]);
+              if constexpr (KBY == 2) {
+                uint16_t k16;
+                asm("ld.shared.u16 %0, [%1];" : "=h"(k16) : "r"(addr));
+                key = k16;
+              } else {
+                asm("ld.shared.u32 %0, [%1];" : "=r"(key) : "r"(addr));
+              }
+            } else {
+              const int32_t o = max((int32_t)v[j * G + g] - koff[g], 0);  // koff = s_g here
+              const uint32_t sak = sk_addr + (uint32_t)KBY * (uint32_t)(g * WS + o);
+              const KT* ga = gkeys + (int64_t)g * WG + o;
+              if constexpr (KBY == 2) {
+                uint16_t k16;
+                asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t"
+                    "@p ld.shared.u16 %0, [%3];\n\t@!p ld.global.nc.u16 %0, [%4];\n\t}"
+                    : "=h"(k16)
+                    : "r"(o), "r"(WS), "r"(sak), "l"(ga));
+                key = k16;
+              } else {
+                asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t"
+                    "@p ld.shared.u32 %0, [%3];\n\t@!p ld.global.nc.u32 %0, [%4];\n\t}"
+                    : "=r"(key)
+                    : "r"(o), "r"(WS), "r"(sak), "l"(ga));
+              }
+            }
+            m = max(m, key);
           }
           kk[ch * CPL + j] = m;
         }
       }
       // the A tile is free (its MMAs completed): stage the keys, then store rows
-      // of KPT keys (2*KPT bytes) per step, 16-byte pieces
+      // of KPT keys per step, 16-byte pieces
       unsigned char* wst = stg + warp * 32 * STG_ROW;
+      if constexpr (KBY == 2) {
 #pragma unroll
-      for (int x8 = 0; x8 < KPT / 8; ++x8)
-        *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x8 * 16) =
-            make_uint4(kk[8 * x8] | (kk[8 * x8 + 1] << 16), kk[8 * x8 + 2] | (kk[8 * x8 + 3] << 16),
-                       kk[8 * x8 + 4] | (kk[8 * x8 + 5] << 16), kk[8 * x8 + 6] | (kk[8 * x8 + 7] << 16));
-      if (KPT % 8 == 4)
-        *reinterpret_cast<uint2*>(wst + lane * STG_ROW + (KPT / 8) * 16) =
-            make_uint2(kk[KPT - 4] | (kk[KPT - 3] << 16), kk[KPT - 2] | (kk[KPT - 1] << 16));
+        for (int x8 = 0; x8 < KPT / 8; ++x8)
+          *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x8 * 16) =
+              make_uint4(kk[8 * x8] | (kk[8 * x8 + 1] << 16), kk[8 * x8 + 2] | (kk[8 * x8 + 3] << 16),
+                         kk[8 * x8 + 4] | (kk[8 * x8 + 5] << 16), kk[8 * x8 + 6] | (kk[8 * x8 + 7] << 16));
+        if (KPT % 8 == 4)
+          *reinterpret_cast<uint2*>(wst + lane * STG_ROW + (KPT / 8) * 16) =
+              make_uint2(kk[KPT - 4] | (kk[KPT - 3] << 16), kk[KPT - 2] | (kk[KPT - 1] << 16));
+      } else {
+#pragma unroll
+        for (int x4 = 0; x4 < KPT / 4; ++x4)
+          *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x4 * 16) =
+              make_uint4(kk[4 * x4], kk[4 * x4 + 1], kk[4 * x4 + 2], kk[4 * x4 + 3]);
+      }
       __syncwarp();
       const int64_t tbase = (int64_t)i * 128 + lg * 32;
       const int64_t cbase = c0 + half * KPT;
-      if (KPT >= 8) {
-        constexpr int PPR = KPT / 8;  // 16-byte pieces per row
+      if constexpr (KPT >= KPP) {
+        constexpr int PPR = KPT / KPP;  // 16-byte pieces per row
         for (int q = lane; q < 32 * PPR; q += 32) {
           const int r = q / PPR, piece = q % PPR;
           const int64_t t = tbase + r;
           if (t < T)
-            *reinterpret_cast<uint4*>(out + t * Cp + cbase + piece * 8) =
+            *reinterpret_cast<uint4*>(out + t * Cp + cbase + piece * KPP) =
                 *reinterpret_cast<const uint4*>(wst + r * STG_ROW + piece * 16);
         }
-      } else {  // KPT == 4: one 8-byte piece per row
+      } else {  // u16, KPT == 4: one 8-byte piece per row
         const int64_t t = tbase + lane;
         if (t < T)
           *reinterpret_cast<uint2*>(out + t * Cp + cbase) = *reinterpret_cast<const uint2*>(wst + lane * STG_ROW);
@@ -380,9 +452,28 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
 // multiple of 8: candidate tiles are 256/G >= 8 wide). vals[0, kSumSmemVals)
 // sits in shared memory (99.9% of step maxima at C4 rank below 8,192); a
 // miss goes to L2 on the chain's critical path.
+// four 4-key groups of a step: u16 keys in 8 bytes, u32 keys in 16
+template <typename KT> struct Key4;
+template <> struct Key4<uint16_t> {
+  using V = uint2;
+  __device__ static uint32_t get(const V& v, int j) {
+    const uint32_t w = j < 2 ? v.x : v.y;
+    return (j & 1) ? (w >> 16) : (w & 0xffffu);
+  }
+  __device__ static V zero() { return make_uint2(0u, 0u); }
+};
+template <> struct Key4<uint32_t> {
+  using V = uint4;
+  __device__ static uint32_t get(const V& v, int j) { return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w; }
+  __device__ static V zero() { return make_uint4(0u, 0u, 0u, 0u); }
+};
+
+template <typename KT>
 __global__ void __launch_bounds__(kSumThreads, 3)
-keysum_kernel(const uint16_t* __restrict__ keys, int64_t T, int64_t C, int64_t Cp, int64_t L, int64_t layer0,
+keysum_kernel(const KT* __restrict__ keys, int64_t T, int64_t C, int64_t Cp, int64_t L, int64_t layer0,
               const double* __restrict__ vals, const int32_t* __restrict__ nvals, double* __restrict__ layer_scores) {
+  using K4 = Key4<KT>;
+  using V = typename K4::V;
   extern __shared__ double s_vals[];  // [kSumSmemVals]
   const int K = min(*nvals, kSumSmemVals);
   for (int i = threadIdx.x; i < K; i += blockDim.x) s_vals[i] = vals[i];
@@ -390,33 +481,33 @@ keysum_kernel(const uint16_t* __restrict__ keys, int64_t T, int64_t C, int64_t C
   const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int64_t lb = blockIdx.y;
   if (c0 >= C) return;
-  const uint2* p = reinterpret_cast<const uint2*>(keys + lb * T * Cp + c0);
-  const int64_t stride = Cp / 4;  // uint2 per step
+  const V* p = reinterpret_cast<const V*>(keys + lb * T * Cp + c0);
+  const int64_t stride = Cp / 4;  // V per step
   auto val = [&](uint32_t k) -> double { return k < (uint32_t)kSumSmemVals ? s_vals[k] : __ldg(vals + k); };
   // keys 8 steps ahead of the serial fp64 chains (which stay in t order)
   constexpr int D = 8;
-  uint2 q[D];
+  V q[D];
 #pragma unroll
-  for (int d = 0; d < D; ++d) q[d] = d < T ? __ldcs(p + (int64_t)d * stride) : make_uint2(0u, 0u);
+  for (int d = 0; d < D; ++d) q[d] = d < T ? __ldcs(p + (int64_t)d * stride) : K4::zero();
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int64_t t = 0;
   for (; t + D <= T; t += D) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const uint2 k = q[d];
-      q[d] = t + D + d < T ? __ldcs(p + (t + D + d) * stride) : make_uint2(0u, 0u);
-      s0 = dadd(s0, val(k.x & 0xffffu));
-      s1 = dadd(s1, val(k.x >> 16));
-      s2 = dadd(s2, val(k.y & 0xffffu));
-      s3 = dadd(s3, val(k.y >> 16));
+      const V k = q[d];
+      q[d] = t + D + d < T ? __ldcs(p + (t + D + d) * stride) : K4::zero();
+      s0 = dadd(s0, val(K4::get(k, 0)));
+      s1 = dadd(s1, val(K4::get(k, 1)));
+      s2 = dadd(s2, val(K4::get(k, 2)));
+      s3 = dadd(s3, val(K4::get(k, 3)));
     }
   }
   for (int d = 0; t < T; ++t, ++d) {
-    const uint2 k = q[d];
-    s0 = dadd(s0, val(k.x & 0xffffu));
-    s1 = dadd(s1, val(k.x >> 16));
-    s2 = dadd(s2, val(k.y & 0xffffu));
-    s3 = dadd(s3, val(k.y >> 16));
+    const V k = q[d];
+    s0 = dadd(s0, val(K4::get(k, 0)));
+    s1 = dadd(s1, val(K4::get(k, 1)));
+    s2 = dadd(s2, val(K4::get(k, 2)));
+    s3 = dadd(s3, val(K4::get(k, 3)));
   }
   const double sv[4] = {s0, s1, s2, s3};
 #pragma unroll
@@ -424,23 +515,36 @@ keysum_kernel(const uint16_t* __restrict__ keys, int64_t T, int64_t C, int64_t C
     if (c0 + j < C) layer_scores[(c0 + j) * L + layer0 + lb] = sv[j];
 }
 
-template <int E>
-static int launch_maxkey(int G, dim3 grid, size_t smem, cudaStream_t st, const int32_t* hist, int64_t T,
-                         const int8_t* cand, int64_t C, int64_t L, int64_t l0, int64_t Cp, const uint16_t* keys,
-                         int keys_total, const int32_t* rowinfo, uint16_t* out) {
+// the key staging of one tile (8 warps x 32 steps x KPT keys + pad) must fit the A tile
+template <int E, int G, typename KT>
+constexpr bool maxkey_fits() {
+  constexpr int KH = E == 256 ? 2 : 1;
+  return 8 * 32 * ((kLtN / G / 2) * (int)sizeof(KT) + 16) <= (128 * 16 + 16) * (2 * (E / KH) / 16);
+}
+
+template <int E, typename KT>
+static int launch_maxkey(int G, bool split, dim3 grid, size_t smem, cudaStream_t st, const int32_t* hist,
+                         int64_t T, const int8_t* cand, int64_t C, int64_t L, int64_t l0, int64_t Cp,
+                         const KT* keys, int keys_total, const int32_t* rowinfo, int WS, int WG, KT* out) {
+  constexpr int KH = E == 256 ? 2 : 1;
   auto pick = [&](auto kern) -> int {
     GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, kLtThreads, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, keys_total, rowinfo, out);
+    kern<<<grid, kLtThreads, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, keys_total, rowinfo, WS, WG, out);
     GEM_CHECK_LAUNCH("maxkey_tc_kernel");
     return GEM_OK;
   };
+  auto pick2 = [&](auto k_full, auto k_split) -> int { return split ? pick(k_split) : pick(k_full); };
   switch (G) {
     case 4:
-      if constexpr (E == 128) return pick(maxkey_tc_kernel<E, 4>);
+      if constexpr (maxkey_fits<E, 4, KT>())
+        return pick2(maxkey_tc_kernel<E, 4, KH, false, KT>, maxkey_tc_kernel<E, 4, KH, true, KT>);
       else return 1;
-    case 8: return pick(maxkey_tc_kernel<E, 8>);
-    case 16: return pick(maxkey_tc_kernel<E, 16>);
-    default: return pick(maxkey_tc_kernel<E, 32>);
+    case 8:
+      if constexpr (maxkey_fits<E, 8, KT>())
+        return pick2(maxkey_tc_kernel<E, 8, KH, false, KT>, maxkey_tc_kernel<E, 8, KH, true, KT>);
+      else return 1;
+    case 16: return pick2(maxkey_tc_kernel<E, 16, KH, false, KT>, maxkey_tc_kernel<E, 16, KH, true, KT>);
+    default: return pick2(maxkey_tc_kernel<E, 32, KH, false, KT>, maxkey_tc_kernel<E, 32, KH, true, KT>);
   }
 }
 
@@ -454,7 +558,8 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
                                   int64_t C, const double* lut, int64_t nmax, double* layer_scores,
                                   int32_t* err_flag, void* stream) {
   (void)err_flag;
-  if (!(E == 64 || E == 128) || !(G == 4 || G == 8 || G == 16 || G == 32) || (E == 64 && G == 4)) return 1;
+  if (!(E == 64 || E == 128 || E == 256) || !(G == 4 || G == 8 || G == 16 || G == 32) || (E == 64 && G == 4))
+    return 1;
   if (T < 1 || C < 1 || nmax < 0 || L > 65535) return 1;
   cudaStream_t st = as_stream(stream);
   keep_pool();
@@ -507,80 +612,122 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
     U = imax64(U, bnd[2 + l]);
     hmax = imax64(hmax, bnd[2 + L + l]);
   }
-  if (U > nmax || U >= 65536) return 1;  // table range
+  if (U > nmax || U >= (1 << 20)) return 1;  // table range
   const int W = (int)U + 1;
+  if (hmax > 4095) return 1;  // u8 limbs (h < 4096)
   // key rows [s_g, U], s_g = min(thr_g, U): rowinfo [g] = s_g, [G+g] = row offset, [2G] = total
-  std::vector<int32_t> rowinfo((size_t)2 * G + 1);
-  int keys_total = 0;
+  std::vector<int32_t> packed((size_t)2 * G + 1);
+  int npacked = 0, wmax = 0;
   const bool noclamp = std::getenv("GEM_SCORE_NOCLAMP") != nullptr;
   for (int g = 0; g < G; ++g) {
     const int sg = noclamp ? 0 : (int)imin64(imax64(bnd[4 + 2 * L + g], 0), U);
-    rowinfo[g] = sg;
-    rowinfo[G + g] = keys_total;
-    keys_total += W - sg;
+    packed[g] = sg;
+    packed[G + g] = npacked;
+    npacked += W - sg;
+    wmax = wmax > W - sg ? wmax : W - sg;
   }
-  rowinfo[2 * G] = keys_total;
-  const size_t key_bytes = (((size_t)keys_total * 2) + 15) & ~size_t(15);
-  const size_t lt_smem = (size_t)(128 * 16 + 16) * (2 * E / 16) + (size_t)kLtN * 2 * E + 64 + 256 + key_bytes;
-  if (hmax > 4095 || lt_smem > (size_t)optin) return 1;  // u8 limbs (h < 4096), shared memory
+  packed[2 * G] = npacked;
 
-  // ---- order keys of the load window: sort the distinct fp64 values
-  const int64_t cnt = (int64_t)G * W;
-  auto* bits = static_cast<unsigned long long*>(alloc((size_t)cnt * 8));
-  auto* sorted = static_cast<unsigned long long*>(alloc((size_t)cnt * 8));
-  auto* uniq = static_cast<unsigned long long*>(alloc((size_t)cnt * 8));
-  auto* nu = static_cast<int32_t*>(alloc(8));  // [0] distinct count, [1] bad entry flag
-  auto* keys = static_cast<uint16_t*>(alloc(key_bytes));
-  int32_t* rowinfo_d = static_cast<int32_t*>(alloc(rowinfo.size() * 4));
-  if (!bits || !sorted || !uniq || !nu || !keys || !rowinfo_d)
-    return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc keys");
+  // ---- order keys: sort the distinct fp64 values of the rows (only those can be gathered)
+  auto* bits = static_cast<unsigned long long*>(alloc((size_t)npacked * 8));
+  auto* sorted = static_cast<unsigned long long*>(alloc((size_t)npacked * 8));
+  auto* uniq = static_cast<unsigned long long*>(alloc((size_t)npacked * 8));
+  auto* nu = static_cast<int32_t*>(alloc(8));  // [0] distinct count
+  int32_t* packed_d = static_cast<int32_t*>(alloc(packed.size() * 4));
+  if (!bits || !sorted || !uniq || !nu || !packed_d) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc keys");
   GEM_CHECK_CUDA(cudaMemsetAsync(nu, 0, 8, st));
-  GEM_CHECK_CUDA(cudaMemcpyAsync(rowinfo_d, rowinfo.data(), rowinfo.size() * 4, cudaMemcpyHostToDevice, st));
-  window_bits_kernel<<<(unsigned)imin64((cnt + 255) / 256, 4096), 256, 0, st>>>(lut, G, nmax + 1, W, bits, nu + 1);
-  GEM_CHECK_LAUNCH("window_bits_kernel");
+  GEM_CHECK_CUDA(cudaMemcpyAsync(packed_d, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice, st));
+  row_bits_kernel<<<(unsigned)imin64((npacked + 255) / 256, 4096), 256, 0, st>>>(lut, nmax + 1, G, packed_d, bits);
+  GEM_CHECK_LAUNCH("row_bits_kernel");
   size_t t1 = 0, t2 = 0;
-  GEM_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, t1, bits, sorted, (int)cnt, 0, 64, st));
-  GEM_CHECK_CUDA(cub::DeviceSelect::Unique(nullptr, t2, sorted, uniq, nu, (int)cnt, st));
+  GEM_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, t1, bits, sorted, npacked, 0, 64, st));
+  GEM_CHECK_CUDA(cub::DeviceSelect::Unique(nullptr, t2, sorted, uniq, nu, npacked, st));
   void* tmp = alloc(t1 > t2 ? t1 : t2);
   if (!tmp) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc cub");
-  GEM_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t1, bits, sorted, (int)cnt, 0, 64, st));
-  GEM_CHECK_CUDA(cub::DeviceSelect::Unique(tmp, t2, sorted, uniq, nu, (int)cnt, st));
-  if (cnt > kMaxKeys) {  // only then can the distinct count exceed the u16 key range
+  GEM_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t1, bits, sorted, npacked, 0, 64, st));
+  GEM_CHECK_CUDA(cub::DeviceSelect::Unique(tmp, t2, sorted, uniq, nu, npacked, st));
+  bool wide = std::getenv("GEM_SCORE_KEY32") != nullptr;  // tests: force u32 keys
+  if (npacked > kMaxKeys) {  // only then can the distinct count exceed the u16 key range (second sync)
     int32_t nk = 0;
     GEM_CHECK_CUDA(cudaMemcpyAsync(&nk, nu, 4, cudaMemcpyDeviceToHost, st));
     GEM_CHECK_CUDA(cudaStreamSynchronize(st));
-    if (nk < 1 || nk > kMaxKeys) return 1;
+    if (nk < 1) return 1;
+    wide = wide || nk > kMaxKeys;
   }
-  key_rows_kernel<<<(unsigned)imin64((keys_total + 255) / 256, 4096), 256, 0, st>>>(bits, G, W, rowinfo_d, uniq, nu,
-                                                                                    keys);
+  if (wide && (G == 4 || (G == 8 && E == 64))) return 1;  // the u32 key staging does not fit the A tile
+  const int KBY = wide ? 4 : 2;
+
+  // ---- shared memory: A (one K part of E/KH experts), B (K = 2E), barriers, row info, key rows
+  const int KH = E == 256 ? 2 : 1;
+  const size_t fixed = (size_t)(128 * 16 + 16) * (2 * (E / KH) / 16) + (size_t)kLtN * 2 * E + 64 + 256;
+  std::vector<int32_t> rowinfo = packed;
+  int keys_total = npacked;
+  size_t key_smem = (((size_t)keys_total * KBY) + 15) & ~size_t(15);
+  bool split = false;
+  int WS = 0, WG = 0;
+  if (fixed + key_smem > (size_t)optin || std::getenv("GEM_SCORE_SPLIT")) {
+    // rows too long for shared memory: the first WS keys of each row there, all of it in a global [G][WG] table
+    split = true;
+    WG = (wmax + 7) & ~7;
+    const int64_t room = ((int64_t)optin - (int64_t)fixed) / ((int64_t)KBY * G);
+    WS = (int)imin64(room & ~int64_t(7), WG);
+    if (std::getenv("GEM_SCORE_SPLIT")) WS = (int)imin64(WS, imax64(8, (WG / 4) & ~7));  // tests: force misses
+    if (WS < 8) return 1;
+    for (int g = 0; g < G; ++g) rowinfo[G + g] = g * WG;
+    rowinfo[2 * G] = keys_total = G * WG;
+    key_smem = (size_t)G * WS * KBY;
+  }
+  const size_t lt_smem = fixed + key_smem;
+  if (lt_smem > (size_t)optin) return 1;
+  void* keys = alloc((((size_t)keys_total * KBY) + 15) & ~size_t(15));
+  int32_t* rowinfo_d = static_cast<int32_t*>(alloc(rowinfo.size() * 4));
+  if (!keys || !rowinfo_d) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc key rows");
+  GEM_CHECK_CUDA(cudaMemcpyAsync(rowinfo_d, rowinfo.data(), rowinfo.size() * 4, cudaMemcpyHostToDevice, st));
+  const unsigned kr_grid = (unsigned)imin64((keys_total + 255) / 256, 4096);
+  if (wide)
+    key_rows_kernel<uint32_t><<<kr_grid, 256, 0, st>>>(lut, nmax + 1, G, W, rowinfo_d, uniq, nu,
+                                                        static_cast<uint32_t*>(keys));
+  else
+    key_rows_kernel<uint16_t><<<kr_grid, 256, 0, st>>>(lut, nmax + 1, G, W, rowinfo_d, uniq, nu,
+                                                        static_cast<uint16_t*>(keys));
   GEM_CHECK_LAUNCH("key_rows_kernel");
   const double* vals = reinterpret_cast<const double*>(uniq);  // the bit patterns are the values
 
-  // ---- layer batches: P layers of u16 step keys [P][T][Cp] in flight (<= ~32 GB)
+  // ---- layer batches: P layers of step keys [P][T][Cp] in flight (<= ~32 GB)
   const int CT = kLtN / G;
   const int64_t ntile = (C + CT - 1) / CT;
   const int64_t Cp = ntile * CT;
-  const size_t per_layer = (size_t)T * Cp * 2;
+  const size_t per_layer = (size_t)T * Cp * KBY;
   int64_t P = imin64((int64_t)(32ull << 30) / (int64_t)per_layer, L);
   if (P < 1) return 1;
-  auto* kbuf = static_cast<uint16_t*>(alloc(per_layer * P));
+  void* kbuf = alloc(per_layer * P);
   if (!kbuf) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc key buffer");
-  GEM_CHECK_CUDA(cudaFuncSetAttribute(keysum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kSumSmemVals * 8));
-  GEM_CHECK_CUDA(cudaFuncSetAttribute(keysum_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                      cudaSharedmemCarveoutMaxShared));  // 3 CTAs x 64 KB per SM
-  for (int64_t l0 = 0; l0 < L; l0 += P) {
-    const int64_t nb = imin64(P, L - l0);
-    const dim3 g1((unsigned)ntile, (unsigned)nb);
-    const int rc = E == 128 ? launch_maxkey<128>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, keys_total,
-                                                 rowinfo_d, kbuf)
-                            : launch_maxkey<64>(G, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, keys, keys_total,
-                                                rowinfo_d, kbuf);
-    if (rc) return rc;
-    keysum_kernel<<<dim3((unsigned)((C + 4 * kSumThreads - 1) / (4 * kSumThreads)), (unsigned)nb), kSumThreads,
-                    (size_t)kSumSmemVals * 8, st>>>(
-        kbuf, T, C, Cp, L, l0, vals, nu, layer_scores);
-    GEM_CHECK_LAUNCH("keysum_kernel");
-  }
+  auto run = [&](auto kt) -> int {
+    using KT = decltype(kt);
+    auto ks = keysum_kernel<KT>;
+    GEM_CHECK_CUDA(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, kSumSmemVals * 8));
+    GEM_CHECK_CUDA(cudaFuncSetAttribute(ks, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        cudaSharedmemCarveoutMaxShared));  // 3 CTAs x 64 KB per SM
+    const KT* kt_keys = static_cast<const KT*>(keys);
+    KT* kt_buf = static_cast<KT*>(kbuf);
+    for (int64_t l0 = 0; l0 < L; l0 += P) {
+      const int64_t nb = imin64(P, L - l0);
+      const dim3 g1((unsigned)ntile, (unsigned)nb);
+      const int rc =
+          E == 256 ? launch_maxkey<256, KT>(G, split, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
+                                            keys_total, rowinfo_d, WS, WG, kt_buf)
+          : E == 128 ? launch_maxkey<128, KT>(G, split, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
+                                              keys_total, rowinfo_d, WS, WG, kt_buf)
+                     : launch_maxkey<64, KT>(G, split, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
+                                             keys_total, rowinfo_d, WS, WG, kt_buf);
+      if (rc) return rc;
+      ks<<<dim3((unsigned)((C + 4 * kSumThreads - 1) / (4 * kSumThreads)), (unsigned)nb), kSumThreads,
+           (size_t)kSumSmemVals * 8, st>>>(kt_buf, T, C, Cp, L, l0, vals, nu, layer_scores);
+      GEM_CHECK_LAUNCH("keysum_kernel");
+    }
+    return GEM_OK;
+  };
+  const int rc = wide ? run(uint32_t{}) : run(uint16_t{});
+  if (rc) return rc;
   return GEM_OK;
 }

@@ -315,13 +315,25 @@ def test_score_candidates_batch_matches_oracle(oracle):
 @pytest.mark.parametrize("L,T,E,G,C,high,balanced", [(2, 300, 128, 8, 100, 120, True), (3, 129, 64, 8, 70, 400, True),
                                                       (1, 1000, 128, 4, 33, 60, True), (2, 77, 64, 16, 40, 300, True),
                                                       (2, 200, 128, 8, 45, 90, False), (1, 64, 128, 1, 5, 50, True),
-                                                      (2, 90, 128, 32, 20, 500, True), (1, 130, 64, 32, 9, 700, True)])
-def test_score_batch_tensor_cores_vs_cuda_cores(oracle, L, T, E, G, C, high, balanced):
-    """K5 v3 (tcgen05 one-hot loads + exact order keys) == K5 v1 == oracle, bit for bit:
-    ragged T and candidate tiles, G = 4/8/16/32, unbalanced candidate tables; G = 1
-    is declined by the tensor-core path (the caller runs v1)."""
+                                                      (2, 90, 128, 32, 20, 500, True), (1, 130, 64, 32, 9, 700, True),
+                                                      (2, 150, 256, 32, 21, 60, True), (1, 260, 256, 8, 40, 40, True),
+                                                      (2, 131, 256, 32, 13, 400, False)])
+@pytest.mark.parametrize("split,key32", [(False, False), (True, False), (False, True), (True, True)])
+def test_score_batch_tensor_cores_vs_cuda_cores(oracle, monkeypatch, L, T, E, G, C, high, balanced, split, key32):
+    """K5 (tcgen05 kind::i8 one-hot loads + exact order keys) == K5 v1 == oracle, bit for bit:
+    ragged T and candidate tiles, G = 4/8/16/32, E = 64/128/256 (E = 256: two K
+    parts through one A buffer), unbalanced candidate tables; split=True keeps
+    only a quarter of every key row in shared memory (the rest is gathered
+    from the global table, the DeepSeek-V3 path); G = 1 is declined by the
+    tensor-core path (the caller runs v1); key32=True forces the u32 order
+    keys (used when the window holds more than 65,536 distinct latencies;
+    declined for G = 4 and E = 64/G = 8, where u32 staging does not fit)."""
     from paper_2605_19945_b200 import _device, _lib
 
+    if split:
+        monkeypatch.setenv("GEM_SCORE_SPLIT", "1")
+    if key32:
+        monkeypatch.setenv("GEM_SCORE_KEY32", "1")
     rng = np.random.default_rng(L * 1000 + T + E + G)
     tok = np.stack([random_counts(rng, T, E, high=high) for _ in range(L)])
     p = mixed_profile(gem, rng, G) if G > 1 else staircase_profile(gem, rng, 1, tile=64, tiles=256)
@@ -340,7 +352,7 @@ def test_score_batch_tensor_cores_vs_cuda_cores(oracle, L, T, E, G, C, high, bal
         err = torch.zeros((1,), dtype=torch.int32, device="cuda")
         rc = getattr(_lib.lib(), fn)(hist.data_ptr(), L, T, E, G, cd.data_ptr(), C, lut.data_ptr(), dc.lut_nmax,
                                      ls.data_ptr(), err.data_ptr(), st)
-        if fn == "gem_score_batch_tc" and G not in (4, 8, 16, 32):
+        if fn == "gem_score_batch_tc" and (G not in (4, 8, 16, 32) or (key32 and (G == 4 or (G == 8 and E == 64)))):
             assert rc == 1
             continue
         assert rc == 0, (fn, rc, _lib.lib().gem_last_error())
