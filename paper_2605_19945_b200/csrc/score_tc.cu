@@ -28,6 +28,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
+#include <cstdint>
 #include <cstdlib>
 #include <vector>
 
@@ -197,12 +198,25 @@ __global__ void row_bits_kernel(const double* __restrict__ lut, int64_t width, i
 // windows): shared memory holds the first WS keys of every row (uniform
 // stride, loads [s_g, s_g + WS)), the full rows [s_g, U] stay in a global
 // [G][WG] table (L2) for the rest; each gather is one predicated LDS or LDG.
+// Per-GPU key-row constants, passed by value: the unrolled GPU loop reads them
+// as constant-bank operands (no registers; at G = 32 two register arrays of
+// 32 spilled). Byte offsets relative to the shared key rows:
+//   rel = max(KBY*n + koff[g], kbase[g])  -- the clamped key's offset;
+//   SPLIT: rel < kend[g] reads shared memory, else the global table at byte
+//   offset rel + goff[g].
+struct KeyRowConsts {
+  int32_t koff[32];
+  int32_t kbase[32];
+  int32_t kend[32];
+  int32_t goff[32];
+};
+
 // KT: u16 keys, or u32 when the window holds more than 65,536 distinct latencies.
 template <int E, int G, int KH, bool SPLIT, typename KT>
 __global__ void __launch_bounds__(kLtThreads, 1)
 maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __restrict__ cand, int64_t C,
                  int64_t L, int64_t layer0, int64_t Cp, const KT* __restrict__ gkeys, int keys_total,
-                 const int32_t* __restrict__ rowinfo, int WS, int WG, KT* __restrict__ out_keys) {
+                 const __grid_constant__ KeyRowConsts kr, int WS, int WG, KT* __restrict__ out_keys) {
   constexpr int KBY = (int)sizeof(KT);       // bytes per key
   constexpr int EH = E / KH;                 // experts per K part
   constexpr int KBH = 2 * EH;                // K bytes per step row per part: [lo | hi16]
@@ -224,7 +238,6 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
   unsigned char* sa = lt_smem;
   unsigned char* sb = lt_smem + A_BYTES;
   LoadsTcShared* sh = reinterpret_cast<LoadsTcShared*>(sb + B_BYTES);
-  int32_t* sinfo = reinterpret_cast<int32_t*>(sb + B_BYTES + 64);        // [2G]: koff, base (or s_g)
   KT* skeys = reinterpret_cast<KT*>(sb + B_BYTES + 64 + 256);  // packed key rows (SPLIT: [G][WS])
   unsigned char* stg = sa;  // the A tile's space, free once the tile's MMAs completed
 
@@ -250,13 +263,6 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
       const int g = i / pr, q = i - g * pr;
       reinterpret_cast<uint4*>(skeys)[i] = __ldg(reinterpret_cast<const uint4*>(gkeys + (int64_t)g * WG) + q);
     }
-  }
-  if (tid < G) {
-    // rowinfo: [g] = s_g (first load of the row), [G+g] = row offset (entries)
-    const int32_t sk = (int32_t)tc::smem_u32(skeys);
-    const int32_t s0 = rowinfo[tid], rb = rowinfo[G + tid];
-    sinfo[tid] = SPLIT ? s0 : sk + KBY * (rb - s0);  // koff: KBY*n + koff = address of key[g][n]
-    sinfo[G + tid] = sk + KBY * rb;                   // base: address of key[g][s_g]
   }
   // one-hot B: row r = j*G + g (candidate j of the tile, GPU g); in K part p,
   // chunk q < EH/16 holds experts p*EH + 16q.. as 1, chunk q >= EH/16 the
@@ -286,13 +292,8 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
   const uint32_t idesc = tc::instr_desc(/*S32*/ 2, /*u8*/ 0, /*u8*/ 0, 128, kLtN);
   const int ntiles = (int)((T + 127) / 128);
   const int lg = warp & 3, half = warp >> 2;
-  int32_t koff[G], kbase[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    koff[g] = sinfo[g];
-    if (!SPLIT) kbase[g] = sinfo[G + g];
-  }
   const uint32_t sk_addr = tc::smem_u32(skeys);
+  const char* gk_bytes = reinterpret_cast<const char*>(gkeys);
 
   // H rows of one K part: each warp reads whole rows (coalesced); the next
   // part's rows are in flight during the current part's MMA (and epilogue)
@@ -372,31 +373,30 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             uint32_t key;
+            const int32_t rel = max((int32_t)v[j * G + g] * KBY + kr.koff[g], kr.kbase[g]);
+            const uint32_t sak = sk_addr + (uint32_t)rel;
             if (!SPLIT) {
-              const int32_t addr = max((int32_t)v[j * G + g] * KBY + koff[g], kbase[g]);
               if constexpr (KBY == 2) {
                 uint16_t k16;
-                asm("ld.shared.u16 %0, [%1];" : "=h"(k16) : "r"(addr));
+                asm("ld.shared.u16 %0, [%1];" : "=h"(k16) : "r"(sak));
                 key = k16;
               } else {
-                asm("ld.shared.u32 %0, [%1];" : "=r"(key) : "r"(addr));
+                asm("ld.shared.u32 %0, [%1];" : "=r"(key) : "r"(sak));
               }
             } else {
-              const int32_t o = max((int32_t)v[j * G + g] - koff[g], 0);  // koff = s_g here
-              const uint32_t sak = sk_addr + (uint32_t)KBY * (uint32_t)(g * WS + o);
-              const KT* ga = gkeys + (int64_t)g * WG + o;
+              const char* ga = gk_bytes + (rel + kr.goff[g]);
               if constexpr (KBY == 2) {
                 uint16_t k16;
                 asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t"
                     "@p ld.shared.u16 %0, [%3];\n\t@!p ld.global.nc.u16 %0, [%4];\n\t}"
                     : "=h"(k16)
-                    : "r"(o), "r"(WS), "r"(sak), "l"(ga));
+                    : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga));
                 key = k16;
               } else {
                 asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t"
                     "@p ld.shared.u32 %0, [%3];\n\t@!p ld.global.nc.u32 %0, [%4];\n\t}"
                     : "=r"(key)
-                    : "r"(o), "r"(WS), "r"(sak), "l"(ga));
+                    : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga));
               }
             }
             m = max(m, key);
@@ -525,11 +525,11 @@ constexpr bool maxkey_fits() {
 template <int E, typename KT>
 static int launch_maxkey(int G, bool split, dim3 grid, size_t smem, cudaStream_t st, const int32_t* hist,
                          int64_t T, const int8_t* cand, int64_t C, int64_t L, int64_t l0, int64_t Cp,
-                         const KT* keys, int keys_total, const int32_t* rowinfo, int WS, int WG, KT* out) {
+                         const KT* keys, int keys_total, const KeyRowConsts& kr, int WS, int WG, KT* out) {
   constexpr int KH = E == 256 ? 2 : 1;
   auto pick = [&](auto kern) -> int {
     GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, kLtThreads, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, keys_total, rowinfo, WS, WG, out);
+    kern<<<grid, kLtThreads, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, keys_total, kr, WS, WG, out);
     GEM_CHECK_LAUNCH("maxkey_tc_kernel");
     return GEM_OK;
   };
@@ -679,6 +679,15 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   }
   const size_t lt_smem = fixed + key_smem;
   if (lt_smem > (size_t)optin) return 1;
+  KeyRowConsts kr{};
+  for (int g = 0; g < G; ++g) {
+    const int sg = rowinfo[g];
+    const int srow = split ? g * WS : rowinfo[G + g];  // row start in shared memory (entries)
+    kr.koff[g] = KBY * (srow - sg);                    // KBY*n + koff = offset of key[g][n]
+    kr.kbase[g] = KBY * srow;                          // offset of key[g][s_g]
+    kr.kend[g] = split ? KBY * (srow + WS) : INT32_MAX;
+    kr.goff[g] = split ? KBY * (g * WG) - kr.kbase[g] : 0;  // shared offset -> global byte offset
+  }
   void* keys = alloc((((size_t)keys_total * KBY) + 15) & ~size_t(15));
   int32_t* rowinfo_d = static_cast<int32_t*>(alloc(rowinfo.size() * 4));
   if (!keys || !rowinfo_d) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc key rows");
@@ -715,11 +724,11 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
       const dim3 g1((unsigned)ntile, (unsigned)nb);
       const int rc =
           E == 256 ? launch_maxkey<256, KT>(G, split, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
-                                            keys_total, rowinfo_d, WS, WG, kt_buf)
+                                            keys_total, kr, WS, WG, kt_buf)
           : E == 128 ? launch_maxkey<128, KT>(G, split, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
-                                              keys_total, rowinfo_d, WS, WG, kt_buf)
+                                              keys_total, kr, WS, WG, kt_buf)
                      : launch_maxkey<64, KT>(G, split, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
-                                             keys_total, rowinfo_d, WS, WG, kt_buf);
+                                             keys_total, kr, WS, WG, kt_buf);
       if (rc) return rc;
       ks<<<dim3((unsigned)((C + 4 * kSumThreads - 1) / (4 * kSumThreads)), (unsigned)nb), kSumThreads,
            (size_t)kSumSmemVals * 8, st>>>(kt_buf, T, C, Cp, L, l0, vals, nu, layer_scores);
