@@ -213,15 +213,15 @@ int gem_score_batch(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_
 
 /* The two implementations behind gem_score_batch (which tries the first and
  * falls back to the second):
- *  - gem_score_batch_tc: candidate loads as a one-hot fp16 GEMM on tcgen05
- *    (exact: counts <= 2048, loads < 2^24); every load is looked up in a
- *    u16 order-key table of the load window (keys rank the distinct fp64
- *    latencies, so the step maximum is an integer max) and each
- *    (candidate, layer) chain adds the exact fp64 value of its step maxima
- *    serially in t. Needs E in {64, 128}, G in {4, 8, 16, 32}. Returns 1
- *    (nothing done) when a precondition fails. Stream-ordered scratch; ONE
- *    host sync (the launch geometry depends on the load window), two only
- *    when G x window > 65,536 entries.
+ *  - gem_score_batch_tc: candidate loads as a one-hot GEMM on tcgen05
+ *    (kind::i8: u8 limbs of counts < 4096, exact s32 loads); every load is
+ *    looked up in an order-key table (u16, or u32 past 65,536 distinct
+ *    latencies; rows split between shared memory and a global table when too
+ *    long) and each (candidate, layer) chain adds the exact fp64 value of its
+ *    step maxima serially in t. Needs E in {64, 128, 256}, G in {4, 8, 16,
+ *    32}. Returns 1 (nothing done) when a precondition fails. Stream-ordered
+ *    scratch; ONE host sync (the launch geometry depends on the load window),
+ *    two when the clamped rows hold more than 65,536 entries.
  *  - gem_score_batch_v1: CUDA cores, any shape (E <= 256). */
 int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int32_t E, int32_t G,
                        const int8_t* cand, int64_t C, const double* lut, int64_t nmax,

@@ -1,31 +1,32 @@
-// K5 v3: straggler scoring of thousands of candidate mappings on B200.
+// K5 v4: straggler scoring of thousands of candidate mappings on B200.
 //
 //   score[c][l] = sum_t (serial fp64)  max_g C_g( n_g(c,l,t) ),
 //   n_g(c,l,t)  = sum_{e : cand[c][l][e] == g} h[l][t][e]        (mapping.py:146-166)
 //
 // Order keys. Every latency the scorer can meet is a table value lut[g][n]
-// with n in the load window [0, U] (U = max over steps of the sum of the
-// `maxcnt` largest counts, maxcnt = the most experts any candidate puts on one
-// GPU: no load can exceed it). The distinct values of that window, sorted,
-// give each (n, g) a 16-bit key = the rank of lut[g][n]: keys compare exactly
-// like the fp64 values (equal values share a key), so the per-step maximum is
-// an integer max over G keys and its exact value is vals[key].
+// with n in [s_g, U] (U = max over steps of the sum of the `maxcnt` largest
+// counts, maxcnt = the most experts any candidate puts on one GPU: no load can
+// exceed it; s_g = the gather clamp, below which a load may read the key at
+// s_g without changing any step maximum). The distinct values of those rows,
+// sorted, give each (n, g) a key = the rank of lut[g][n] (u16, or u32 past
+// 65,536 distinct values): keys compare exactly like the fp64 values (equal
+// values share a key), so the per-step maximum is an integer max over G keys
+// and its exact value is vals[key].
 //
-//  pass 1 (maxkey_tc_kernel, tcgen05): the per-GPU loads of every candidate
-//    are a one-hot GEMM  D[t][(c,g)] = sum_e H[t][e] * O[e][(c,g)]  with H in
-//    fp16 (counts <= 2048 are exact) and O the 0/1 one-hot of the candidate
-//    tables, accumulated in fp32 in TMEM (loads < 2^24 are exact). M = 128
-//    steps, N = 256 (candidate, GPU) columns, K = E. The epilogue drains TMEM
-//    (tcgen05.ld: one step per lane), looks every load up in the key table
-//    (shared memory, [g][n] u16: random n spread over all banks) and writes the step's maximum key per
-//    candidate: u16 [layer][t][c] -- 1/G of the bytes of the loads themselves.
-//  pass 2 (keysum_kernel): one thread per (candidate, layer) walks t in order
-//    and adds vals[key] to the fp64 chain exactly as the reference sums
-//    (_util.py:8-18); the low end of vals sits in shared memory.
+//  pass 1 (maxkey_tc_kernel, tcgen05 kind::i8): the per-GPU loads of every
+//    candidate are a one-hot GEMM D[t][(c,g)] = sum_e H[t][e] * O[e][(c,g)]
+//    with H split into u8 limbs [lo | 16*hi] along K and O as [O | 16*O], so
+//    the s32 accumulator in TMEM is the load itself. M = 128 steps, N = 256
+//    (candidate, GPU) columns, K = 2E bytes (E = 256: two K parts through one
+//    A buffer). The epilogue drains TMEM (tcgen05.ld: one step per lane),
+//    looks every load up in the key rows (shared memory; rows too long for it
+//    split with a global table) and writes the step's maximum key per
+//    candidate: [layer][t][c] -- 1/G of the bytes of the loads themselves.
+//  pass 2 (keysum_kernel): one thread per 4 candidates of a layer walks t in
+//    order and adds vals[key] to each fp64 chain exactly as the reference
+//    sums (_util.py:8-18); the low end of vals sits in shared memory.
 //
 // Bit-exact with score_layers_kernel and the oracle by construction.
-#include <cuda_fp16.h>
-
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <cstdint>

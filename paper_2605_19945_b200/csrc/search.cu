@@ -138,30 +138,37 @@ __device__ __forceinline__ double lut_at(const double* __restrict__ lut, int64_t
 }
 
 // ---------------------------------------------------------------------------
-// K7: greedy placement, one CTA per run
+// K7: greedy placement, one CTA per run (the exact v1 kernel: any G up to
+// kMaxGpus; the screened K7 v3 below handles G <= 32). Per chunk of tchunk
+// steps every thread fills the exact terms of every GPU with capacity, then
+// thread g extends GPU g's serial chain in t order; the strict-< lowest-index
+// rule (search.py:156) picks the GPU.
+constexpr int kMaxGpus = 127;  // assignments are int8
 __global__ void __launch_bounds__(kSearchThreads)
 greedy_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, const double* __restrict__ lut,
               int64_t nmax, const int32_t* __restrict__ run_layer, const uint8_t* __restrict__ needs_greedy,
-              const int16_t* __restrict__ order, int8_t* __restrict__ assign, int32_t* __restrict__ loads_ws) {
+              const int16_t* __restrict__ order, int8_t* __restrict__ assign, int32_t* __restrict__ loads_ws,
+              int tchunk) {
   extern __shared__ double gsm[];
-  double* cost = gsm;  // [G][kGreedyTChunk]
-  __shared__ int counts[32];
+  double* cost = gsm;  // [G][tchunk]
+  __shared__ int counts[kMaxGpus + 1];
+  __shared__ double sums[kMaxGpus + 1];
   __shared__ int s_best;
   const int64_t r = blockIdx.x;
   if (!needs_greedy[r]) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int64_t width = nmax + 1;
   const int32_t* h = hist + (int64_t)run_layer[r] * T * E;
   int32_t* ld = loads_ws + r * T * G;
   for (int64_t i = tid; i < T * G; i += blockDim.x) ld[i] = 0;
-  if (tid < 32) counts[tid] = 0;
+  for (int g = tid; g <= kMaxGpus; g += blockDim.x) counts[g] = 0;
   const int cap = E / G;
   __syncthreads();
   for (int idx = 0; idx < E; ++idx) {
     const int e = order[r * E + idx];
-    double sum = 0.0;  // lane g of warp 0 owns GPU g's chain
-    for (int64_t t0 = 0; t0 < T; t0 += kGreedyTChunk) {
-      const int tn = (int)imin64(kGreedyTChunk, T - t0);
+    double sum = 0.0;  // thread g owns GPU g's chain
+    for (int64_t t0 = 0; t0 < T; t0 += tchunk) {
+      const int tn = (int)imin64(tchunk, T - t0);
       for (int tt = tid; tt < tn; tt += blockDim.x) {
         const int64_t t = t0 + tt;
         const int32_t* lrow = ld + t * G;
@@ -183,26 +190,27 @@ greedy_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, const d
           } else {
             sc = cl;
           }
-          cost[g * kGreedyTChunk + tt] = sc;
+          cost[g * tchunk + tt] = sc;
         }
       }
       __syncthreads();
-      if (warp == 0 && lane < G && counts[lane] < cap) {
-        const double* cg = cost + lane * kGreedyTChunk;
+      if (tid < G && counts[tid] < cap) {
+        const double* cg = cost + tid * tchunk;
         for (int tt = 0; tt < tn; ++tt) sum = dadd(sum, cg[tt]);
       }
       __syncthreads();
     }
-    if (warp == 0) {
-      // strict < in ascending GPU order among GPUs with capacity
+    if (tid < G) sums[tid] = sum;
+    __syncthreads();
+    if (tid == 0) {  // strict < in ascending GPU order among GPUs with capacity
       double best = 0.0;
       int bg = -1;
       for (int g = 0; g < G; ++g) {
-        const double s = __shfl_sync(0xffffffffu, sum, g);
         if (counts[g] == cap) continue;
-        if (bg < 0 || s < best) { best = s; bg = g; }
+        if (bg < 0 || sums[g] < best) { best = sums[g]; bg = g; }
       }
-      if (lane == 0) { s_best = bg; counts[bg] += 1; }
+      s_best = bg;
+      counts[bg] += 1;
     }
     __syncthreads();
     const int bg = s_best;
@@ -1829,7 +1837,7 @@ static int check_search_args(const int32_t* hist, int64_t L, int64_t T, int32_t 
                              int64_t nmax, int64_t R, const int32_t* run_layer, size_t ws_bytes, void* workspace) {
   GEM_REQUIRE(hist && lut && run_layer && workspace && L >= 1 && T >= 1 && E >= 1 && G >= 1 && R >= 1,
               "gem_search: bad arguments");
-  GEM_REQUIRE(G <= 32 && E <= 127 * 32 && E <= 32767, "gem_search: G <= 32 required (got G=%d)", G);
+  GEM_REQUIRE(G <= kMaxGpus && E <= 32767, "gem_search: G <= %d required (got G=%d)", kMaxGpus, G);
   GEM_REQUIRE(E % G == 0, "gem_search: %d experts cannot be split evenly across %d GPUs", E, G);
   GEM_REQUIRE(E <= 2048, "gem_search: E <= 2048 required");
   GEM_REQUIRE(nmax >= 0 && nmax < (1LL << 31), "gem_search: nmax out of range");
@@ -1999,10 +2007,13 @@ static int launch_greedy(const int32_t* hist, int64_t T, int32_t E, int32_t G, c
       return GEM_OK;
     }
   }
-  const size_t gsmem = (size_t)G * kGreedyTChunk * sizeof(double);
+  // per-GPU cost chunks in shared memory: 256 steps, fewer when G is large
+  int tchunk = kGreedyTChunk;
+  while (tchunk > 32 && (size_t)G * tchunk * sizeof(double) > (size_t)optin - 4096) tchunk /= 2;
+  const size_t gsmem = (size_t)G * tchunk * sizeof(double);
   GEM_CHECK_CUDA(cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
   greedy_kernel<<<(unsigned)R, kSearchThreads, gsmem, st>>>(hist, T, E, G, lut, nmax, run_layer, needs_greedy, order,
-                                                            assign, ws.loads);
+                                                            assign, ws.loads, tchunk);
   GEM_CHECK_LAUNCH("greedy_kernel");
   return GEM_OK;
 }
@@ -2032,7 +2043,9 @@ static int prepare_screen(const int32_t* hist, int64_t L, int64_t T, int32_t E, 
                           int64_t nmax, Screen& sc, SearchWs& ws, cudaStream_t st) {
   sc.st = st;
   keep_pool();
-  if (G < 2 || T > (1LL << 24)) return GEM_OK;
+  // G > 32: the screened kernels keep GPU sets in 32-bit masks -- the exact
+  // v1 kernels (any G) run instead
+  if (G < 2 || G > 32 || T > (1LL << 24)) return GEM_OK;
   const int64_t n = (int64_t)G * (nmax + 1);
   GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.lut32), (size_t)n * sizeof(float), st));
   lut_to_f32_kernel<<<(unsigned)imin64((n + 255) / 256, 4096), 256, 0, st>>>(lut, n, sc.lut32);

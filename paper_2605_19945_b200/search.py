@@ -274,11 +274,9 @@ def run_search_device(hist: torch.Tensor, nmax: int, profile: VariabilityProfile
     """Run greedy + refinement for every run of `batch` on the device."""
     L, T, E = hist.shape
     G = profile.num_gpus
-    if G > 32:
-        # known gap vs the reference (search.py:98-131 takes any G): the device
-        # search keeps per-run GPU sets in 32-bit masks (DESIGN.md §9)
-        raise ValidationError(f"the device search supports at most 32 GPUs per mapping, got {G} "
-                              "(known gap vs the reference search; scoring and replay accept any G)")
+    if G > 127:
+        # assignments are int8 on the device (the reference takes any G; 127 GPUs per mapping here)
+        raise ValidationError(f"the device search supports at most 127 GPUs per mapping, got {G}")
     _check_divisible(E, G)
     R = len(batch.provenance)
     dc = _device.DeviceCurves.from_profile(profile)

@@ -427,10 +427,12 @@ def test_search_golden():
 
 
 @pytest.mark.parametrize("G,E,T,high", [(2, 8, 16, 300), (4, 16, 40, 300), (8, 64, 128, 300), (3, 12, 1, 300),
-                                        (8, 8, 30, 300), (2, 128, 12, 300), (32, 256, 6, 40), (4, 16, 20, 4000)])
+                                        (8, 8, 30, 300), (2, 128, 12, 300), (32, 256, 6, 40), (4, 16, 20, 4000),
+                                        (64, 128, 10, 60), (48, 96, 7, 80)])
 def test_search_matches_oracle(oracle, G, E, T, high):
     """Covers the shared-memory swap scan (one pass, multi-pass with 64x64 expert pairs per GPU pair,
-    16 runs per CTA at G=32) and the L1 fallback (step totals > 11k: the two table rows exceed smem)."""
+    16 runs per CTA at G=32), the L1 fallback (step totals > 11k: the two table rows exceed smem)
+    and G > 32 (the exact v1 greedy and scan: the reference takes any number of GPUs)."""
     rng = np.random.default_rng(G * 1000 + E + T)
     tok = random_counts(rng, T, E, high=high)
     p = mixed_profile(gem, rng, G) if E < 64 else staircase_profile(gem, rng, G, tile=64, tiles=256)
