@@ -448,6 +448,20 @@ def run_ours(args):
                                 "sharding": f"candidates {c0}..{c1 - 1} on this rank of {world} (all-gather of "
                                             f"the histogram shards + one all-gather of the scores, timed)"
                                 if use_dist else "single GPU"}
+        # K5 roofline (tensor): the one-hot load GEMM's useful int8 ops --
+        # 2 x T steps x (C x G) columns x 2E K bytes (u8 limbs) per layer --
+        # over the whole scoring time; the leg is bound by the key gathers
+        # (C*L*T*G random shared-memory loads), which DESIGN.md §4 sizes
+        tp = tensor_peaks()
+        mma_ops = 2.0 * T * (C // world if use_dist else C) * G * 2 * E * L
+        if tp.get("int8_tops"):
+            ach = mma_ops / (cms / 1e3) / 1e12
+            result["candidates"]["roofline"] = {
+                "kernel": "maxkey_tc_kernel (K5, tcgen05 kind::i8) + keysum_kernel", "bound": "tensor",
+                "achieved": ach, "peak": tp["int8_tops"], "unit": "TOPS", "frac": ach / tp["int8_tops"],
+                "peak_source": "profiles/r02_peaks.json (cuBLAS int8 GEMM)",
+                "note": "the MMA is a minor share: the leg is bound by C*L*T*G shared-memory key gathers "
+                        "(floor ~34 ms at C4, DESIGN.md K5 bound)"}
         del cand_d
 
     if not args.no_search:
@@ -480,6 +494,9 @@ def run_ours(args):
             return info
 
         result["time_to_mapping"] = ttm_info(args.search_steps or T)
+        result["time_to_mapping"]["roofline_note"] = (
+            "dominated by K6 approx_scan5 (random fp32 table gathers in shared memory, ~84% of the shared-memory "
+            "wavefront peak per ncu, profiles/r02_ncu_k6.json); no HBM or tensor-pipe bound applies")
         if not args.search_steps and T > 16:  # the paper's 16-step window (the reference arm measures the same)
             w16 = ttm_info(16)
             w16["includes"] = "K1..K3b statistics of the full trace, search of every layer's first 16 steps"

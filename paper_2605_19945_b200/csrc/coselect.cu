@@ -133,7 +133,10 @@ coselect_tc_kernel(const IdT* __restrict__ ids, int64_t N, int k, int E, int64_t
         const int64_t seg = imin64(s1 - p, N - p % N);
         for (int64_t j = 0; j < seg; j += kCsTok, ++g) {
           const int is = (int)(g % G::ISTAGES);
-          if (g >= G::ISTAGES) tc::mbar_wait(&sh->ids_empty[is], (g / G::ISTAGES - 1) & 1);
+          if (g >= G::ISTAGES) {
+            tc::mbar_wait(&sh->ids_empty[is], (g / G::ISTAGES - 1) & 1);
+            tc::fence_async_smem();  // the producers' generic reads of the slot before the async-proxy refill
+          }
           const uint32_t bytes = (uint32_t)(imin64(kCsTok, seg - j) * tok_bytes);
           tc::mbar_arrive_expect_tx(&sh->ids_full[is], bytes);
           tc::bulk_load_1d(idr + is * IDB, ids + (p + j) * k, bytes, &sh->ids_full[is]);

@@ -693,6 +693,8 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   int32_t* rowinfo_d = static_cast<int32_t*>(alloc(rowinfo.size() * 4));
   if (!keys || !rowinfo_d) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc key rows");
   GEM_CHECK_CUDA(cudaMemcpyAsync(rowinfo_d, rowinfo.data(), rowinfo.size() * 4, cudaMemcpyHostToDevice, st));
+  // row padding and the tail of the last 16-byte piece are copied to shared memory, never read
+  GEM_CHECK_CUDA(cudaMemsetAsync(keys, 0, (((size_t)keys_total * KBY) + 15) & ~size_t(15), st));
   const unsigned kr_grid = (unsigned)imin64((keys_total + 255) / 256, 4096);
   if (wide)
     key_rows_kernel<uint32_t><<<kr_grid, 256, 0, st>>>(lut, nmax + 1, G, W, rowinfo_d, uniq, nu,
