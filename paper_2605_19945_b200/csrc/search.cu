@@ -405,14 +405,16 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
         parg = ta[t];
       }
       uint32_t lrow[GM];
-      if (GM == 8) {
-        const uint4 v = *reinterpret_cast<const uint4*>(ld + t * GM);
+      // the step's GM u16 loads: GM/8 16-byte loads (rows are 16-byte aligned)
+#pragma unroll
+      for (int qv = 0; qv < GM / 8; ++qv) {
+        const uint4 v = reinterpret_cast<const uint4*>(ld + t * GM)[qv];
         const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) { lrow[2 * q] = w4[q] & 0xffffu; lrow[2 * q + 1] = w4[q] >> 16; }
-      } else {
-#pragma unroll
-        for (int g = 0; g < GM; ++g) lrow[g] = ld[t * GM + g];
+        for (int q = 0; q < 4; ++q) {
+          lrow[8 * qv + 2 * q] = w4[q] & 0xffffu;
+          lrow[8 * qv + 2 * q + 1] = w4[q] >> 16;
+        }
       }
       // rows of GPUs g >= G (GM padding) read row G-1 and are masked by select: no branches
       float pre[GM + 1], suf[GM + 1];

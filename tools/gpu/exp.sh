@@ -1,7 +1,10 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-bash tools/config_sweep.sh > gpurun_out/sweep.txt 2>&1
-tail -2 gpurun_out/smoke.log; cut -c1-400 gpurun_out/bench.json; tail -2 gpurun_out/bench.err; cat gpurun_out/sweep.txt | tail -7
+timeout 1500 python -m pytest tests -m gpu -x -q -k "search or greedy or config_slice" > gpurun_out/pytest_k7.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_k7.log
+tail -2 gpurun_out/pytest_k7.log
+for c in deepseek-v3 qwen3-235b; do
+GEM_SEARCH_TRACE=1 timeout 900 python bench.py --config $c --steps 1 --warmup 3 --no-cpu --no-e2e --no-coselect --no-candidates > gpurun_out/tr_$c.json 2> gpurun_out/tr_$c.err
+echo "$c $(grep greedy gpurun_out/tr_$c.err | sed -n 2p) $(python -c "
+import json
+d=json.loads(open('gpurun_out/tr_$c.json').read().strip().splitlines()[-1]); print(d['time_to_mapping']['value'], d['time_to_mapping']['aggregate_score'], d['time_to_mapping_w16']['value'], d['time_to_mapping_w16']['aggregate_score'])")"
+done
