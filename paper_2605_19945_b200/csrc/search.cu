@@ -1140,7 +1140,8 @@ __host__ __device__ inline size_t swap5_smem(int E, int G, int64_t W, int Y) {
 template <int GT, int Y>
 __global__ void __launch_bounds__(kSwap3Threads, GEM_SCAN_MINB)
 approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int32_t* __restrict__ run_layer,
-                    const int8_t* __restrict__ assign, int32_t n_active, SearchWs ws, int64_t tseg) {
+                    const int8_t* __restrict__ assign, int32_t n_active, SearchWs ws, int64_t tseg,
+                    const uint8_t* __restrict__ prune) {
   extern __shared__ __align__(16) unsigned char s5[];
   const int G = GT > 0 ? GT : G_;
   const Swap3Geom geo = swap3_geom(E, G, Y);
@@ -1157,6 +1158,17 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
   // blockIdx.z-th segment of tseg steps; split CTAs add their partial sums to
   // ws.split_acc and split_window_kernel finishes the tiles
   const bool split = tseg > 0;
+  if (prune != nullptr) {  // search: tiles whose bound rejects every pair (tile_bound_kernel) are skipped
+    bool all = true;
+    for (int w = 0; w < nruns; ++w) all = all && prune[(int64_t)(slot0 + w) * NP + blockIdx.x] != 0;
+    if (all) {
+      if ((int)threadIdx.x < nruns) {
+        const int r = ws.run_list[slot0 + threadIdx.x];
+        ws.loc_min[(int64_t)r * NP + blockIdx.x] = __longlong_as_double(0x7ff0000000000000LL);
+      }
+      return;
+    }
+  }
   const int64_t Tp = ws.Tp;  // row stride of the transposed arrays
   const int64_t tb = split ? (int64_t)blockIdx.z * tseg : 0;
   const int64_t te = split ? imin64(Tp, tb + tseg) : Tp;  // this CTA's steps: [tb, te)
@@ -1705,6 +1717,49 @@ __global__ void top3_kernel(int32_t n_active, int64_t Tp, int G, SearchWs ws) {
 }
 
 // fp64 latency table -> its fp32 rounding (round to nearest: monotone)
+// Search-only tile pruning (K6). For a swap on GPUs (a, b) every step's term
+// is max(pother_ab, C_a, C_b) >= pother_ab = the maximum over the OTHER GPUs,
+// so every pair of the tile scores at least LB_ab = sum_t pother_ab(t) (the
+// serial fp64 sum is monotone in its terms). With M, m2, m3 the step's three
+// largest latencies and g1, g2 the GPUs of the first two:
+//   sum_t (M - pother_ab) = X_a + X_b + Y_ab,
+//   X_g = sum_{t: g1 = g} (M - m2),  Y_ab = sum_{t: {g1,g2} = {a,b}} (m2 - m3).
+// If LB_ab already fails the acceptance test (search.py:222-227), no pair of
+// the tile can be accepted: the run either takes a pair of another tile (the
+// exact minimum cannot be in this one) or stops -- the same outcome, so the
+// scan skips the tile. Sums from the fp32 top-3 in any order; the margin
+// 2^-21 * score covers their rounding (<= 2^-23 score) and every summation
+// error. One CTA per active run; prune[slot][p] = 1 for skipped tiles.
+__global__ void tile_bound_kernel(int32_t n_active, int64_t Tp, int G, double thr, SearchWs ws,
+                                  uint8_t* __restrict__ prune) {
+  __shared__ double X[32], Y[32 * 32];
+  const int slot = blockIdx.x;
+  if (slot >= n_active) return;
+  const int r = ws.run_list[slot];
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) X[i] = 0.0;
+  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) Y[i] = 0.0;
+  __syncthreads();
+  const uint32_t* tb = ws.top3 + (int64_t)r * 4 * Tp;
+  for (int64_t t = threadIdx.x; t < Tp; t += blockDim.x) {
+    const float v1 = __uint_as_float(tb[t]), v2 = __uint_as_float(tb[Tp + t]), v3 = __uint_as_float(tb[2 * Tp + t]);
+    const uint32_t pk = tb[3 * Tp + t];
+    const uint32_t g1 = pk & 255u, g2 = (pk >> 8) & 255u;
+    if (g1 < 32u && v1 > v2) atomicAdd(&X[g1], (double)v1 - (double)v2);
+    if (g1 < 32u && g2 < 32u && v2 > v3) atomicAdd(&Y[min(g1, g2) * 32 + max(g1, g2)], (double)v2 - (double)v3);
+  }
+  __syncthreads();
+  const double score = ws.run_score[r];
+  const int NP = G * (G - 1) / 2;
+  for (int p = threadIdx.x; p < NP; p += blockDim.x) {
+    int q = p, a = 0;
+    while (q >= G - 1 - a) { q -= G - 1 - a; ++a; }
+    const int b = a + 1 + q;
+    const double lb = score - (X[a] + X[b] + Y[a * 32 + b]) - score * 0x1p-21;
+    const bool reject = !(lb < score) || __dsub_rn(1.0, __ddiv_rn(lb, score)) < thr;
+    prune[(int64_t)slot * NP + p] = (G >= 3 && reject) ? 1 : 0;  // G = 2: no other GPU bounds the pair
+  }
+}
+
 __global__ void lut_to_f32_kernel(const double* __restrict__ lut, int64_t n, float* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = __double2float_rn(lut[i]);
@@ -1913,9 +1968,26 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
       g5.z = (unsigned)((ws.Tp + tseg - 1) / tseg);
       GEM_CHECK_CUDA(cudaMemsetAsync(ws.split_acc, 0, (size_t)R * NP * n * n * 8, st));
     }
+    // search mode (thr >= 0), unsplit scans: skip the tiles whose pother bound rejects every pair
+    uint8_t* prune = nullptr;
+    // (G >= 16: with few GPUs every pair touches a step maximum often enough that no tile is
+    // provably rejected -- none at the Qwen3-235B shape -- and the bound pass only costs)
+    if (thr >= 0.0 && tseg == 0 && G >= 16 && G <= 32 && !std::getenv("GEM_SCAN_NOPRUNE")) {
+      GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prune), (size_t)n_active * NP, st));
+      tile_bound_kernel<<<(unsigned)n_active, 256, 0, st>>>((int32_t)n_active, ws.Tp, G, thr, ws, prune);
+      GEM_CHECK_LAUNCH("tile_bound_kernel");
+    }
+    struct FreePrune {
+      uint8_t* p;
+      cudaStream_t s;
+      ~FreePrune() {
+        if (p) cudaFreeAsync(p, s);
+      }
+    } free_prune{prune, st};
     auto go5 = [&](auto kern) -> int {
       GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
-      kern<<<g5, kSwap3Threads, smem5, st>>>(E, G, nmax, W5, clamp, run_layer, assign, (int32_t)n_active, ws, tseg);
+      kern<<<g5, kSwap3Threads, smem5, st>>>(E, G, nmax, W5, clamp, run_layer, assign, (int32_t)n_active, ws, tseg,
+                                             prune);
       GEM_CHECK_LAUNCH("approx_scan5_kernel");
       if (tseg > 0) {
         split_window_kernel<<<dim3((unsigned)NP, (unsigned)n_active), 256, 0, st>>>(E, G, assign, (int32_t)n_active,
