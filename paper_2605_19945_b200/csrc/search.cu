@@ -1149,7 +1149,10 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
   const int NP = G * (G - 1) / 2;
   const int slot0 = blockIdx.y * RPC;
   if (slot0 >= n_active) return;
-  const int nruns = min(RPC, n_active - slot0);
+  const int nslots = min(RPC, n_active - slot0);
+  // the CTA's runs whose tile survives the bound (tile_bound_kernel; all when
+  // prune == nullptr), compacted: unit s works on active slot slot0 + s_live[s]
+  __shared__ int s_live[16], s_nlive;
   int p = blockIdx.x, a = 0;
   while (p >= G - 1 - a) { p -= G - 1 - a; ++a; }
   const int b = a + 1 + p;
@@ -1158,17 +1161,21 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
   // blockIdx.z-th segment of tseg steps; split CTAs add their partial sums to
   // ws.split_acc and split_window_kernel finishes the tiles
   const bool split = tseg > 0;
-  if (prune != nullptr) {  // search: tiles whose bound rejects every pair (tile_bound_kernel) are skipped
-    bool all = true;
-    for (int w = 0; w < nruns; ++w) all = all && prune[(int64_t)(slot0 + w) * NP + blockIdx.x] != 0;
-    if (all) {
-      if ((int)threadIdx.x < nruns) {
-        const int r = ws.run_list[slot0 + threadIdx.x];
-        ws.loc_min[(int64_t)r * NP + blockIdx.x] = __longlong_as_double(0x7ff0000000000000LL);
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int w = 0; w < nslots; ++w) {
+      if (prune != nullptr && prune[(int64_t)(slot0 + w) * NP + blockIdx.x] != 0) {
+        // no pair of this tile can be accepted: it takes no part in the minimum
+        ws.loc_min[(int64_t)ws.run_list[slot0 + w] * NP + blockIdx.x] = __longlong_as_double(0x7ff0000000000000LL);
+      } else {
+        s_live[c++] = w;
       }
-      return;
     }
+    s_nlive = c;
   }
+  __syncthreads();
+  const int nruns = s_nlive;
+  if (nruns == 0) return;
   const int64_t Tp = ws.Tp;  // row stride of the transposed arrays
   const int64_t tb = split ? (int64_t)blockIdx.z * tseg : 0;
   const int64_t te = split ? imin64(Tp, tb + tseg) : Tp;  // this CTA's steps: [tb, te)
@@ -1226,13 +1233,13 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
   }
   if (tid < RPC) smin[tid] = ord_bits(__longlong_as_double(0x7ff0000000000000LL));
   if (tid < nruns) {
-    const int r = ws.run_list[slot0 + tid];
+    const int r = ws.run_list[slot0 + s_live[tid]];
     hsrc[tid] = ws.ht16s + (int64_t)run_layer[r] * E * Tp;
     lsrc[tid] = ws.loadT + (int64_t)r * G * Tp;
     fsrc[tid] = reinterpret_cast<const float*>(ws.top3) + (int64_t)r * 4 * Tp;
   }
   for (int w = wid; w < nruns; w += nw) {
-    const int r = ws.run_list[slot0 + w];
+    const int r = ws.run_list[slot0 + s_live[w]];
     const int8_t* as = assign + (int64_t)r * E;
     int base_a = 0, base_b = 0;
     for (int e0 = 0; e0 < E; e0 += 32) {
@@ -1420,7 +1427,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
     }
     if (split) {  // partial sums of this step range (fp64 adds in any order: within the screen's bound)
       if (live) {
-        const int r = ws.run_list[slot0 + s];
+        const int r = ws.run_list[slot0 + s_live[s]];
         double* pa = ws.split_acc + (((int64_t)r * NP + blockIdx.x) * n + x) * n;
 #pragma unroll
         for (int q = 0; q < Y; ++q)
@@ -1437,7 +1444,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
     }
     __syncthreads();
     if (live) {
-      const int r = ws.run_list[slot0 + s];
+      const int r = ws.run_list[slot0 + s_live[s]];
       const int64_t tile = (int64_t)r * NP + blockIdx.x;
       const double lim = __longlong_as_double((long long)smin[s]) * kWindow5;
       const int xe = lists[(s * 2 + 0) * n + x];
@@ -1458,7 +1465,7 @@ approx_scan5_kernel(int E, int G_, int64_t nmax, int W, int monotone, const int3
   if (split) return;
   __syncthreads();
   if (tid < nruns) {
-    const int r = ws.run_list[slot0 + tid];
+    const int r = ws.run_list[slot0 + s_live[tid]];
     ws.loc_min[(int64_t)r * NP + blockIdx.x] = __longlong_as_double((long long)smin[tid]);
   }
 }
