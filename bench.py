@@ -369,7 +369,12 @@ def run_ours(args):
                 st = ingest.trace_statistics(dev_ids, B, E)
                 mu, cls = st.mean_utilization, st.classes.cls
                 st.check()
-            res = (mu.to("cpu", non_blocking=True), cls.to("cpu", non_blocking=True))
+            # the whole TraceStats back to the host: utilisation, active fraction, Pearson, classes
+            if use_dist:
+                outs = (ss.finalized[0], ss.finalized[1], ss.finalized[2], ss.finalized[3])
+            else:
+                outs = (st.mean_utilization, st.active_fraction, st.correlation, st.classes.cls)
+            res = tuple(t.to("cpu", non_blocking=True) for t in outs if t is not None)
             torch.cuda.current_stream().synchronize()
             torch.cuda.nvtx.range_pop()
             return res
@@ -390,7 +395,7 @@ def run_ours(args):
             dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
         e2e_s = float(e2e_ms.item()) / 1e3
         result["e2e"] = {"value": N / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(ids.numel() * 2),
-                         "d2h_bytes_per_step": int(L * E * 8 + L * E), "ms_per_step": e2e_s * 1e3,
+                         "d2h_bytes_per_step": int(2 * L * E * 8 + L * E * E * 8 + L * E), "ms_per_step": e2e_s * 1e3,
                          "bytes_are": "per rank" if use_dist else "whole job",
                          "path": ("dist.sharded_statistics" if use_dist else "ingest.trace_statistics")
                          + "(ids copied from pinned host memory every step)"}
@@ -488,7 +493,8 @@ def run_ours(args):
             if results is not None:
                 swaps = [r.swap_count for res in results for r in res.per_restart]
                 info.update({"runs": len(swaps), "swaps_median": float(np.median(swaps)),
-                             "swaps_max": int(max(swaps)), "aggregate_score": aggregate_score(results)})
+                             "swaps_max": int(max(swaps)), "aggregate_score": aggregate_score(results),
+                             "layer0_best_score": results[0].best_score})
             else:
                 info["aggregate_score"] = shm.aggregate
             return info
@@ -569,6 +575,70 @@ def cpu_stats_baseline(spec, ids_dev):
                       f"(oracle/_ref Cython build), {secs:.2f} s"}
 
 
+# ---- the benchmark's own synthetic router trace (K9) for the reference arm,
+#      generated on the host by the C oracle (oracle/gem_oracle.c, the exact
+#      restatement of gem_gen_topk): the reference arm sees the same ids as ours
+
+def k9_params(config):
+    """(weight [L,E] u32, role [L,E] i8, p_cons, p_burst, burst_mult, seed) of bench.CONFIGS[config]:
+    the planted layout of ingest.TopkTraceSpec/planted_layout restated in numpy (tests/test_host.py
+    pins the equality) so the reference arm never imports this package."""
+    import numpy as np
+
+    L, N, k, E, B, G, C = CONFIGS[config]
+    zipf_s, seed = 1.1, 0
+    consistent, num_groups, group_size = (3, 2, 2) if E >= 16 else (2, 1, 2)
+    weight = np.zeros((L, E), dtype=np.uint32)
+    role = np.zeros((L, E), dtype=np.int8)
+    base = np.maximum(1, np.rint((1 << 20) / np.power(np.arange(E) + 1.0, zipf_s))).astype(np.uint32)
+    for l in range(L):
+        perm = np.random.default_rng([seed, l]).permutation(E)
+        weight[l, perm] = base
+        r = 0
+        for _ in range(consistent):
+            role[l, perm[r]] = 1
+            r += 1
+        for g in range(num_groups):
+            for _ in range(group_size):
+                role[l, perm[r]] = 2 + g
+                r += 1
+    prob = lambda x: min(int(round(x * 4294967296.0)), 0xFFFFFFFF)  # noqa: E731
+    return weight, role, prob(0.85), prob(0.17), 3, seed
+
+
+def _k9_ids(args):
+    """ids [n, k] of layer l, global tokens [t0, t0 + n) (C oracle)."""
+    config, l, t0, n = args
+    from oracle import oracle as o
+
+    L, N, k, E, B, G, C = CONFIGS[config]
+    weight, role, pc, pb, bm, seed = k9_params(config)
+    return o.gen_topk(1, n, k, B, E, weight[l:l + 1], role[l:l + 1], pc, pb, bm, seed, token_offset=t0,
+                      layer_offset=l)[0]
+
+
+def _hist(ids, B, E):
+    import numpy as np
+
+    step = (np.arange(ids.shape[0]) // B).repeat(ids.shape[1])
+    T = -(-ids.shape[0] // B)
+    return np.bincount(step * E + ids.ravel().astype(np.int64), minlength=T * E).reshape(T, E)
+
+
+def _ref_stats_layer(args):
+    """Generate one layer's sample (untimed), then time the reference statistics on it."""
+    config, l, n = args
+    from oracle import oracle as o
+
+    L, N, k, E, B, G, C = CONFIGS[config]
+    ids = _k9_ids((config, l, 0, n))
+    gemap = o.import_reference()
+    s0 = time.perf_counter()
+    st = gemap.compute_stats(gemap.ExpertTrace(_hist(ids, B, E)))
+    secs = time.perf_counter() - s0
+    return secs, float(st.mean_utilization[0])
+
+
 def _ref_profile(gemap, G, nmax):
     return gemap.generate_profile(gemap.VariabilitySetupSpec(num_gpus=G, setup="moderate", tile_size=64,
                                                              max_tokens=nmax, rng_seed=0))
@@ -626,10 +696,10 @@ def _cpu_run_units(args):
     return t_greedy, time.perf_counter() - s0
 
 
-def cpu_search_and_scoring(L, k, E, B, G, C, T, cores, p):
+def cpu_search_and_scoring(config, L, k, E, B, G, C, T, cores):
     """The reference's search (16-step window: all L layers measured; full T: one
     layer measured, x L) and candidate scoring (full T, extrapolated from a
-    timed sample), on every host core."""
+    timed sample), on every host core, on the benchmark's own K9 trace."""
     import numpy as np
     from concurrent.futures import ProcessPoolExecutor
 
@@ -637,17 +707,25 @@ def cpu_search_and_scoring(L, k, E, B, G, C, T, cores, p):
     nmax = B * k
     out = {}
     with ProcessPoolExecutor(max_workers=cores, initializer=_single_thread_env) as ex:
-        w16 = [(rng.multinomial(nmax, p, size=16).astype(np.int64), G, nmax) for _ in range(L)]
+        # every layer's first 16 steps (the window the GPU arm's time_to_mapping_w16 searches)
+        w16 = [(_hist(ids, B, E), G, nmax) for ids in ex.map(_k9_ids, [(config, l, 0, 16 * B) for l in range(L)])]
         list(ex.map(_cpu_search_layer, w16[:cores]))  # warm-up: imports in every worker
         s0 = time.perf_counter()
-        list(ex.map(_cpu_search_layer, w16))
+        best = list(ex.map(_cpu_search_layer, w16))
         secs = time.perf_counter() - s0
+        agg = 0.0
+        for b in best:  # the multi-layer aggregate: serial fp64 sum in layer order (cli.py:427)
+            agg = agg + b
         out["time_to_mapping_w16"] = {
-            "value": secs, "unit": "s", "steps_searched": 16, "layers": L, "cores": cores,
-            "sample": f"all {L} layers measured: reference gemap.search (default SearchConfig, seed 0) on a "
-                      f"16-step multinomial(B*k, Zipf 1.1) window per layer, one process per layer, "
-                      f"{cores} processes (statistics of the full trace not included)"}
-        full = rng.multinomial(nmax, p, size=T).astype(np.int64)
+            "value": secs, "unit": "s", "steps_searched": 16, "layers": L, "cores": cores, "aggregate_score": agg,
+            "sample": f"all {L} layers measured: reference gemap.search (default SearchConfig, seed 0) on every "
+                      f"layer's first 16 steps of the benchmark's K9 trace, one process per layer, {cores} "
+                      f"processes (statistics of the full trace not included); aggregate_score equals the GPU "
+                      f"arm's time_to_mapping_w16.aggregate_score when both compute the same mappings"}
+        # layer 0 in full (token ranges generated in parallel)
+        chunk = -(-T // cores) * B
+        parts = list(ex.map(_k9_ids, [(config, 0, t0, min(chunk, T * B - t0)) for t0 in range(0, T * B, chunk)]))
+        full = _hist(np.concatenate(parts), B, E).astype(np.int64)
         base = np.repeat(np.arange(G), E // G)
         per = 2
         work = [(full, G, nmax, [rng.permutation(base) for _ in range(per)]) for _ in range(cores)]
@@ -678,7 +756,7 @@ def cpu_search_and_scoring(L, k, E, B, G, C, T, cores, p):
     swaps = [r.swap_count for r in res.per_restart]
     out["time_to_mapping"] = {
         "value": L * t_layer, "unit": "s", "steps_searched": T, "layers": L, "cores": cores,
-        "kind": "extrapolated from one measured layer",
+        "kind": "extrapolated from one measured layer", "layer0_best_score": res.best_score,
         "sample": f"reference gemap.search of one {T}-step layer (default SearchConfig, seed 0, restarts on "
                   f"{cores} threads): {t_layer:.1f} s, swaps per run median {float(np.median(swaps)):.0f} max "
                   f"{max(swaps)}; x {L} layers. Lower bound from unit costs (greedy {t_greedy:.2f} s, best_swap "
@@ -699,19 +777,21 @@ def run_reference(args):
         return
     L, N, k, E, B, G, C = CONFIGS[args.config]
     T = N // B
-    # same-shape synthetic ids: Zipf(1.1)-popular experts, sampled with numpy (the
-    # CPU arm must not run our kernels, and the reference's cost does not depend
-    # on which ids are drawn, only on how many)
+    # the benchmark's own K9 ids (C oracle on the host), one process per layer:
+    # each generates its layer's sample (untimed) and times the reference's
+    # bincount ingestion + compute_stats; the layers run concurrently, so the
+    # step time is the slowest layer's
     cores = len(os.sched_getaffinity(0)) or 1  # every host core this process may use
     layers = min(L, cores)
     sample_tokens = min(N, 4096 * B)
-    rng = np.random.default_rng(0)
-    p = 1.0 / np.power(np.arange(1, E + 1), 1.1)
-    p /= p.sum()
-    ids = np.stack([rng.choice(E, size=(sample_tokens, k), p=p).astype(np.int16) for _ in range(layers)])
-    for _ in range(args.warmup if args.warmup < 2 else 1):
-        cpu_stats_run(ids[:, : B * 16], B, E, min(cores, layers))
-    times = [cpu_stats_run(ids, B, E, min(cores, layers)) for _ in range(max(1, min(args.steps, 3)))]
+    from concurrent.futures import ProcessPoolExecutor
+
+    with ProcessPoolExecutor(max_workers=layers, initializer=_single_thread_env) as ex:
+        list(ex.map(_ref_stats_layer, [(args.config, l, 16 * B) for l in range(layers)]))  # warm-up: imports
+        times = []
+        for _ in range(max(1, min(args.steps, 3))):
+            times.append(max(t for t, _ in ex.map(_ref_stats_layer, [(args.config, l, sample_tokens)
+                                                                      for l in range(layers)])))
     secs = float(np.median(times))
     value = sample_tokens * layers / L / secs
     line = {
@@ -721,13 +801,15 @@ def run_reference(args):
         "config": {"workload": f"{args.config}: stats phase (bounded CPU sample)", "layers": L, "tokens": N,
                    "top_k": k, "experts": E},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": min(cores, layers), "kind": "reference",
-                         "sample": f"{layers} layers x {sample_tokens} tokens; np.bincount ingestion restatement + "
-                                   "reference gemap.compute_stats (Cython build in oracle/_ref)"},
+                         "sample": f"{layers} layers x {sample_tokens} tokens of the benchmark's own K9 trace "
+                                   "(generated by the C oracle, untimed); np.bincount ingestion restatement + "
+                                   "reference gemap.compute_stats (Cython build in oracle/_ref), one process per "
+                                   "layer, step = the slowest layer"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     if not args.no_search:
         try:
-            line.update(cpu_search_and_scoring(L, k, E, B, G, C, T, cores, p))
+            line.update(cpu_search_and_scoring(args.config, L, k, E, B, G, C, T, cores))
         except Exception as exc:  # reported next to the headline, never required
             line["search_error"] = repr(exc)
     print(json.dumps(line), flush=True)

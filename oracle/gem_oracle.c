@@ -397,9 +397,20 @@ static uint32_t draw(uint64_t seed, uint32_t a, uint32_t b, uint32_t c, uint32_t
 }
 
 /* the generator contract of gem_gen_topk (include/gemcore.h) */
+/* layers [layer0, layer0 + L) of the trace (weight/role rows of those layers) */
+void or_gen_topk_l(int64_t L, int64_t layer0, int64_t N, int64_t k, int64_t B, int64_t E, const uint32_t* weight,
+                   const int8_t* role, uint32_t p_cons, uint32_t p_burst, uint32_t burst_mult, uint64_t seed,
+                   int64_t token_offset, int id_bytes, void* ids);
+
 void or_gen_topk(int64_t L, int64_t N, int64_t k, int64_t B, int64_t E, const uint32_t* weight, const int8_t* role,
                  uint32_t p_cons, uint32_t p_burst, uint32_t burst_mult, uint64_t seed, int64_t token_offset,
                  int id_bytes, void* ids) {
+  or_gen_topk_l(L, 0, N, k, B, E, weight, role, p_cons, p_burst, burst_mult, seed, token_offset, id_bytes, ids);
+}
+
+void or_gen_topk_l(int64_t L, int64_t layer0, int64_t N, int64_t k, int64_t B, int64_t E, const uint32_t* weight,
+                   const int8_t* role, uint32_t p_cons, uint32_t p_burst, uint32_t burst_mult, uint64_t seed,
+                   int64_t token_offset, int id_bytes, void* ids) {
   uint64_t* w = (uint64_t*)malloc(sizeof(uint64_t) * (E + 1));
   uint64_t* cdf = (uint64_t*)malloc(sizeof(uint64_t) * (E + 1));
   int64_t chosen[64];
@@ -415,9 +426,9 @@ void or_gen_topk(int64_t L, int64_t N, int64_t k, int64_t B, int64_t E, const ui
           int r = role[l * E + e];
           uint64_t v = weight[l * E + e];
           if (r == 1) {
-            if (draw(seed, (uint32_t)step, (uint32_t)(step >> 32), (uint32_t)l, 0x80000000u | (uint32_t)e) >= p_cons) v = 0;
+            if (draw(seed, (uint32_t)step, (uint32_t)(step >> 32), (uint32_t)(l + layer0), 0x80000000u | (uint32_t)e) >= p_cons) v = 0;
           } else if (r >= 2) {
-            if (draw(seed, (uint32_t)step, (uint32_t)(step >> 32), (uint32_t)l, 0xC0000000u | (uint32_t)(r - 2)) < p_burst)
+            if (draw(seed, (uint32_t)step, (uint32_t)(step >> 32), (uint32_t)(l + layer0), 0xC0000000u | (uint32_t)(r - 2)) < p_burst)
               v *= burst_mult;
             else
               v = 0;
@@ -432,7 +443,7 @@ void or_gen_topk(int64_t L, int64_t N, int64_t k, int64_t B, int64_t E, const ui
         int64_t pick = -1;
         if (total > 0) {
           for (int a = 0; a < 32 && pick < 0; ++a) {
-            uint32_t u = draw(seed, (uint32_t)gt, (uint32_t)(gt >> 32), (uint32_t)l, (uint32_t)(s * 64 + a));
+            uint32_t u = draw(seed, (uint32_t)gt, (uint32_t)(gt >> 32), (uint32_t)(l + layer0), (uint32_t)(s * 64 + a));
             uint64_t r = ((uint64_t)u * total) >> 32;
             int64_t e = 0;
             while (cdf[e] <= r) ++e; /* first e with cdf[e] > r */

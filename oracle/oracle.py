@@ -86,6 +86,9 @@ def lib():
     L.or_gen_topk.restype = None
     L.or_gen_topk.argtypes = [I64, I64, I64, I64, I64, u32p, i8p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                               ctypes.c_uint64, I64, ctypes.c_int, ctypes.c_void_p]
+    L.or_gen_topk_l.restype = None
+    L.or_gen_topk_l.argtypes = [I64, I64, I64, I64, I64, I64, u32p, i8p, ctypes.c_uint32, ctypes.c_uint32,
+                                ctypes.c_uint32, ctypes.c_uint64, I64, ctypes.c_int, ctypes.c_void_p]
     _lib = L
     return L
 
@@ -415,11 +418,13 @@ def philox4x32_10(counter, key):
     return out
 
 
-def gen_topk(L, N, k, B, E, weight, role, p_cons, p_burst, burst_mult, seed, token_offset=0, id_bytes=2):
+def gen_topk(L, N, k, B, E, weight, role, p_cons, p_burst, burst_mult, seed, token_offset=0, id_bytes=2,
+             layer_offset=0):
+    """ids [L, N, k] of layers [layer_offset, layer_offset + L) (weight/role: those layers' rows)."""
     ids = np.zeros((L, N, k), dtype=np.int16 if id_bytes == 2 else np.int32)
-    lib().or_gen_topk(L, N, k, B, E, np.ascontiguousarray(weight, dtype=np.uint32),
-                      np.ascontiguousarray(role, dtype=np.int8), int(p_cons), int(p_burst), int(burst_mult),
-                      int(seed), int(token_offset), id_bytes, ids.ctypes.data)
+    lib().or_gen_topk_l(L, int(layer_offset), N, k, B, E, np.ascontiguousarray(weight, dtype=np.uint32),
+                        np.ascontiguousarray(role, dtype=np.int8), int(p_cons), int(p_burst), int(burst_mult),
+                        int(seed), int(token_offset), id_bytes, ids.ctypes.data)
     return ids
 
 

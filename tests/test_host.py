@@ -288,3 +288,29 @@ def test_eplb_assignments_equals_per_row():
         got = eplb_assignments(mu, G)
         want = np.stack([eplb_assignment(mu[l], G) for l in range(mu.shape[0])])
         assert np.array_equal(got, want)
+
+
+def test_bench_reference_arm_trace_is_the_benchmark_trace():
+    """bench.k9_params (the reference arm's numpy restatement of the planted
+    layout, so that arm never imports this package) == ingest.planted_layout
+    for every BASELINE config, and the C oracle's layer/token-offset generation
+    reproduces the matching slice of the whole trace."""
+    import numpy as np
+
+    import bench
+    from oracle import oracle
+    from paper_2605_19945_b200 import ingest
+
+    for name, (L, N, k, E, B, G, C) in bench.CONFIGS.items():
+        planted = {} if E >= 16 else {"consistent": 2, "num_groups": 1}
+        spec = ingest.TopkTraceSpec(num_layers=L, num_tokens=N, top_k=k, num_experts=E, tokens_per_step=B, seed=0,
+                                    **planted)
+        w, r = ingest.planted_layout(spec)
+        bw, br, pc, pb, bm, seed = bench.k9_params(name)
+        assert np.array_equal(w, bw) and np.array_equal(r, br), name
+        assert (pc, pb, bm, seed) == (ingest._prob_u32(spec.consistent_probability),
+                                       ingest._prob_u32(spec.burst_probability), spec.burst_multiplier, spec.seed)
+    w, r, pc, pb, bm, seed = bench.k9_params("mixtral")
+    whole = oracle.gen_topk(3, 3 * 1024, 2, 1024, 8, w[:3], r[:3], pc, pb, bm, seed)
+    part = bench._k9_ids(("mixtral", 2, 1024, 2048))
+    assert np.array_equal(whole[2, 1024:3072], part)
