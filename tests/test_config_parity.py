@@ -7,8 +7,9 @@ steps) goes through
 
   * the B200 path: K1 ingestion, statistics, the batched device search with
     the default SearchConfig (30 restarts + baseline seeds, seed 0) and the
-    batched candidate scorer (gem_score_batch: the tcgen05 path where it
-    applies, the CUDA-core v1 path at E = 256 / G = 32 and E = 8);
+    batched candidate scorer (gem_score_batch: the tcgen05 path, at
+    E = 256 / G = 32 with split key rows and u32 keys; the CUDA-core v1 path
+    at E = 8);
   * the reference itself, built from /root/reference into oracle/_ref by
     oracle/build_ref.sh (shipped to the GPU box with the repo snapshot):
     gemap.compute_stats, gemap.search, gemap.score_mapping
