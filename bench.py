@@ -292,17 +292,22 @@ def run_ours(args):
                    "tokens": N, "top_k": k, "experts": E, "tokens_per_step": B, "steps_per_layer": T,
                    "virtual_gpus": G, "id_dtype": "int16", "l2": "inputs 25 GB >> 126 MB L2 (no flush needed)",
                    "parallelism": f"token-range shards x{world}, NCCL all-reduce of integer stats"},
-        "gpu_launches": 5 * args.steps,  # K1 ring + heavy-row pass, K2, K3, K3b
+        # K1 (+ its heavy-row pass above 160 experts), K2, K3, K3b
+        "gpu_launches": (4 + (E > 160)) * args.steps,
         "step_breakdown_ms": {name: sum(e[i].elapsed_time(e[i + 1]) for e in pev) / len(pev)
                               for i, name in enumerate(phases)},
         "clocks": clk.summary(),
     }
-    # roofline of the dominant kernel (K1 = gem_topk_hist: the ring kernel and
-    # its heavy-step row pass): ids read + histogram written + histogram re-read
-    algo_bytes = L * n_local * k * 2 + 2 * L * (t1 - t0) * E * 4
+    # roofline of the dominant kernel (K1 = gem_topk_hist): ids read + histogram
+    # rows written; above 160 experts (the CTA kernel) + the heavy-step pass's
+    # re-read of the rows (the ring kernel counts heavy steps in its reduction)
+    hist_passes = 1 if E <= 160 else 2
+    algo_bytes = L * n_local * k * 2 + hist_passes * L * (t1 - t0) * E * 4
+    k1_name = ("topk_hist_ring_kernel (K1, heavy steps counted in its reduction)" if E <= 160 else
+               "gem_topk_hist (K1: topk_hist_creg_kernel + hist_heavy_rows_kernel)")
     peak, peak_src = peaks()
     achieved = algo_bytes / (k1_ms / 1e3) / 1e9
-    result["roofline"] = {"kernel": "gem_topk_hist (K1: topk_hist_ring_kernel + hist_heavy_rows_kernel)",
+    result["roofline"] = {"kernel": k1_name,
                           "bound": "hbm", "achieved": achieved, "peak": peak,
                           "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic() if args.config == "qwen3-235b" and world == 1 else None,
                           "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": k1_ms,

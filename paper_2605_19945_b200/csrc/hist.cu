@@ -461,11 +461,13 @@ __host__ __device__ constexpr int ring_rows(int E) {
 // WIDE: u32 counters, rows E + 1; packed (even E only): u16x2 counters, pair
 // rows E/2 + 1 (row E/2 low half = overflow), halves summed separately in the
 // cumulative reduction (a lane's half counts at most B*k <= 65535 per unit).
-template <bool WIDE, int MAXR>
+// HV: count heavy steps in the per-step reduction (row total = warp sum of
+// the row differences) instead of a separate pass over the written rows
+template <bool WIDE, int MAXR, bool HV>
 __global__ void __launch_bounds__(32)
 topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int k, int B, int E, int64_t T,
                       int64_t HT, int32_t* __restrict__ hist, int64_t* __restrict__ colsum,
-                      int32_t* __restrict__ active, int64_t* __restrict__ dropped_out) {
+                      int32_t* __restrict__ active, int32_t* __restrict__ heavy, int64_t* __restrict__ dropped_out) {
   extern __shared__ __align__(16) uint4 rsm[];
   constexpr int BATCH = kRingUnroll * 32;  // uint4 per warp batch (4 KB)
   const int lane = threadIdx.x;
@@ -499,9 +501,9 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
       if (sidx < nb) issue(sidx);
       ring_commit();
     }
-    uint32_t prev[MAXR * BINS], act[MAXR * BINS];
+    uint32_t prev[MAXR * BINS], act[MAXR * BINS], hvy[MAXR * BINS];
 #pragma unroll
-    for (int q = 0; q < MAXR * BINS; ++q) { prev[q] = 0; act[q] = 0; }
+    for (int q = 0; q < MAXR * BINS; ++q) { prev[q] = 0; act[q] = 0; hvy[q] = 0; }
     int in_step = 0;
     int64_t t = t_begin;
     for (int64_t bt = 0; bt < nb; ++bt) {
@@ -535,6 +537,15 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
           }
           sa[q] = a;
           sb[q] = b;
+        }
+        if (HV && WIDE) {  // the step's row total (the overflow row E holds dropped ids: not counted)
+          uint32_t part = 0;
+#pragma unroll
+          for (int q = 0; q < MAXR; ++q)
+            if (lane + q * 32 < hrows) part += sa[q] - prev[q];
+          const uint32_t stot = __reduce_add_sync(0xffffffffu, part);
+#pragma unroll
+          for (int q = 0; q < MAXR; ++q) hvy[q] += is_heavy(sa[q] - prev[q], uE, stot);
         }
 #pragma unroll
         for (int q = 0; q < MAXR; ++q) {
@@ -576,6 +587,7 @@ topk_hist_ring_kernel(const int16_t* __restrict__ ids, int64_t L, int64_t N, int
         const uint32_t cs = prev[q * BINS + bb], ac = act[q * BINS + bb];
         if (cs) atomicAdd((unsigned long long*)&colsum[l * E + bin], (unsigned long long)cs);
         if (ac) atomicAdd(&active[l * E + bin], (int)ac);
+        if (HV && hvy[q * BINS + bb]) atomicAdd(&heavy[l * E + bin], (int)hvy[q * BINS + bb]);
       }
     }
     if (lane == 0 && dropped) atomicAdd((unsigned long long*)&dropped_out[l], (unsigned long long)dropped);
@@ -587,7 +599,8 @@ static int launch_hist_ring(const void* ids, int64_t L, int64_t N, int k, int B,
                             int32_t* hist, int64_t* colsum, int32_t* active, int32_t* heavy, int64_t* dropped, cudaStream_t st) {
   const int rows = ring_rows<WIDE, MAXR>(E);
   const size_t smem = (size_t)kRingStages * kRingUnroll * 32 * 16 + (size_t)rows * 32 * 4;
-  auto kern = topk_hist_ring_kernel<WIDE, MAXR>;
+  const bool hv = WIDE && !std::getenv("GEM_HIST_HEAVY_PASS");  // heavy steps counted in the ring's reduction
+  auto kern = hv ? topk_hist_ring_kernel<WIDE, MAXR, WIDE> : topk_hist_ring_kernel<WIDE, MAXR, false>;
   GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                       cudaSharedmemCarveoutMaxShared));
@@ -597,10 +610,10 @@ static int launch_hist_ring(const void* ids, int64_t L, int64_t N, int k, int B,
   const int64_t units = L * ((T + kHistStepsPerUnit - 1) / kHistStepsPerUnit);
   int64_t blocks = (int64_t)num_sms() * per_sm;
   if (blocks > units) blocks = units;
-  kern<<<(unsigned)blocks, 32, smem, st>>>((const int16_t*)ids, L, N, k, B, E, T, HT, hist, colsum, active,
+  kern<<<(unsigned)blocks, 32, smem, st>>>((const int16_t*)ids, L, N, k, B, E, T, HT, hist, colsum, active, heavy,
                                            dropped);
   GEM_CHECK_LAUNCH("topk_hist_ring_kernel");
-  return launch_heavy_rows(hist, L, T, HT, E, heavy, st);
+  return hv ? GEM_OK : launch_heavy_rows(hist, L, T, HT, E, heavy, st);
 }
 
 // ---------------------------------------------------------------------------
