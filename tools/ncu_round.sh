@@ -7,7 +7,7 @@ R=/tmp/ncu_reps; mkdir -p $R
 N="timeout 900 ncu --set full --clock-control none --import-source on -c 1"
 $N -k regex:topk_hist_ring -o $R/k1 python tools/kbench.py hist --reps 1 --warm 0 > /dev/null 2>&1
 $N -k regex:topk_hist_creg -o $R/k1c5 python tools/kbench.py hist --layers 58 --experts 256 --reps 1 --warm 0 > /dev/null 2>&1
-$N -k regex:hist_heavy -o $R/k1h python tools/kbench.py hist --reps 1 --warm 0 > /dev/null 2>&1
+$N -k regex:hist_heavy -o $R/k1h python tools/kbench.py hist --layers 58 --experts 256 --reps 1 --warm 0 > /dev/null 2>&1
 $N -k regex:gram_tc -o $R/k2 python tools/kbench.py gram --reps 1 --warm 0 > /dev/null 2>&1
 $N -k regex:coselect_tc -o $R/k2b python tools/kbench.py coselect --reps 1 --warm 0 --paths gem_coselect_tc > /dev/null 2>&1
 $N -k regex:maxkey -o $R/k5 python tools/kbench.py score --cands 10000 --reps 1 --warm 0 > /dev/null 2>&1
