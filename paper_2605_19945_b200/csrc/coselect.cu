@@ -51,6 +51,9 @@ constexpr int kCsProd = 4;                      // producer / epilogue warps (32
 constexpr int kCsThreads = (kCsProd + 2) * 32;  // + MMA warp + TMA warp
 constexpr int kCsMaxTokBytes = 32;              // k * id_bytes on the tensor-core path
 
+#ifndef GEM_CS_IDRING
+#define GEM_CS_IDRING 32768  // bytes of the TMA id ring per CTA
+#endif
 #ifndef GEM_CS_STAGES1
 #define GEM_CS_STAGES1 4  // E <= 128: 4 x 16 KB operand stages -> two CTAs per SM
 #endif
@@ -68,8 +71,9 @@ struct CsGeo {
   static constexpr int LBO = SLICE + 64;
   static constexpr int STAGE = LBO * (kCsTok / 16);  // one-hot bytes per stage
   static constexpr int STAGES = EB == 1 ? GEM_CS_STAGES1 : 4;  // powers of two: ring
-  static constexpr int ISTAGES = 32768 / IDB;                  // indices are masks
-  static constexpr int CTAS_PER_SM = EB == 1 && STAGES <= 4 ? 2 : 1;
+  static constexpr int ISTAGES = GEM_CS_IDRING / IDB;
+  static constexpr size_t SMEM_EST = (size_t)STAGES * STAGE + (size_t)ISTAGES * IDB + 512;
+  static constexpr int CTAS_PER_SM = EB == 1 ? (SMEM_EST <= 74 * 1024 ? 3 : (STAGES <= 4 ? 2 : 1)) : 1;
   static constexpr uint32_t TMEM_COLS = EB == 1 ? 128 : 512;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE + (size_t)ISTAGES * IDB + 512;
 };
