@@ -30,6 +30,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -42,7 +43,10 @@ __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, i
                                   const int32_t* __restrict__ n_dev, int32_t* __restrict__ bound,
                                   int32_t* __restrict__ top1, int32_t* __restrict__ rowmin);  // search.cu
 
-constexpr int kLtThreads = 256;
+#ifndef GEM_LT_WARPS
+#define GEM_LT_WARPS 8
+#endif
+constexpr int kLtWarps = GEM_LT_WARPS;  // maxkey CTA: 8 or 16 warps (4 per TMEM lane quarter per column group)
 constexpr int kLtN = 256;        // MMA N (candidate x GPU columns per CTA)
 constexpr int kMaxKeys = 65536;  // u16 keys
 constexpr int kSumThreads = 256;
@@ -213,8 +217,8 @@ struct KeyRowConsts {
 };
 
 // KT: u16 keys, or u32 when the window holds more than 65,536 distinct latencies.
-template <int E, int G, int KH, bool SPLIT, typename KT>
-__global__ void __launch_bounds__(kLtThreads, 1)
+template <int E, int G, int KH, bool SPLIT, typename KT, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
 maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __restrict__ cand, int64_t C,
                  int64_t L, int64_t layer0, int64_t Cp, const KT* __restrict__ gkeys, int keys_total,
                  const __grid_constant__ KeyRowConsts kr, int WS, int WG, KT* __restrict__ out_keys) {
@@ -227,10 +231,12 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
   constexpr int A_BYTES = (int)LBO_A * KCH;
   constexpr int B_BYTES = kLtN * KBH * KH;
   constexpr int CT = kLtN / G;               // candidates per CTA
-  constexpr int KPT = CT / 2;                // keys per thread per tile (one column half)
+  constexpr int NQ = NW / 4;                 // column groups (warps per TMEM lane quarter)
+  constexpr int NT = NW * 32;                // threads
+  constexpr int KPT = CT / NQ;               // keys per thread per tile (one column group)
   constexpr int CPL = 32 / G;                // candidates per 32-column TMEM load
   constexpr int STG_ROW = KPT * KBY + 16;    // staging row: the thread's keys + 16 B pad
-  constexpr int STG_BYTES = 8 * 32 * STG_ROW;
+  constexpr int STG_BYTES = NW * 32 * STG_ROW;
   static_assert(STG_BYTES <= A_BYTES, "key staging must fit the A tile");
   static_assert(G >= 4 && G <= 32 && (kLtN % G) == 0, "G in {4, 8, 16, 32}");
   static_assert(EH == 64 || EH == 128, "K parts of 64 or 128 experts");
@@ -256,11 +262,11 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
   if (warp == 0) tc::tmem_alloc<kLtN>(&sh->tmem_base);
   if (!SPLIT) {  // key rows -> shared memory (16-byte pieces; the global copy is padded to 16 bytes)
     const int pieces = (keys_total * KBY + 15) / 16;
-    for (int i = tid; i < pieces; i += kLtThreads)
+    for (int i = tid; i < pieces; i += NT)
       reinterpret_cast<uint4*>(skeys)[i] = __ldg(reinterpret_cast<const uint4*>(gkeys) + i);
   } else {  // the first WS keys of every [G][WG] row (WS, WG multiples of 8)
     const int pr = WS / KPP;
-    for (int i = tid; i < G * pr; i += kLtThreads) {
+    for (int i = tid; i < G * pr; i += NT) {
       const int g = i / pr, q = i - g * pr;
       reinterpret_cast<uint4*>(skeys)[i] = __ldg(reinterpret_cast<const uint4*>(gkeys + (int64_t)g * WG) + q);
     }
@@ -268,7 +274,7 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
   // one-hot B: row r = j*G + g (candidate j of the tile, GPU g); in K part p,
   // chunk q < EH/16 holds experts p*EH + 16q.. as 1, chunk q >= EH/16 the
   // same experts as 16
-  for (int i = tid; i < kLtN * KCH * KH; i += kLtThreads) {
+  for (int i = tid; i < kLtN * KCH * KH; i += NT) {
     const int r = i / (KCH * KH), qq = i % (KCH * KH);
     const int part = qq / KCH, q = qq % KCH;
     uint32_t w[4] = {0u, 0u, 0u, 0u};
@@ -292,13 +298,13 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
   const uint32_t sa_addr = tc::smem_u32(sa), sb_addr = tc::smem_u32(sb);
   const uint32_t idesc = tc::instr_desc(/*S32*/ 2, /*u8*/ 0, /*u8*/ 0, 128, kLtN);
   const int ntiles = (int)((T + 127) / 128);
-  const int lg = warp & 3, half = warp >> 2;
+  const int lg = warp & 3, cg = warp >> 2;
   const uint32_t sk_addr = tc::smem_u32(skeys);
   const char* gk_bytes = reinterpret_cast<const char*>(gkeys);
 
   // H rows of one K part: each warp reads whole rows (coalesced); the next
   // part's rows are in flight during the current part's MMA (and epilogue)
-  constexpr int RPW = 128 / (kLtThreads / 32);  // rows per warp (16)
+  constexpr int RPW = 128 / NW;                  // rows per warp
   constexpr int LPR = EH / 4;                    // lanes per row (4 experts each)
   constexpr int RPI = 32 / LPR;                  // rows per warp instruction
   constexpr int NX = RPW / RPI;
@@ -358,15 +364,15 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
       }
     }
     // ---- epilogue: warp w drains TMEM lanes 32(w%4).. (one step per lane) and
-    // column half w/4 in 32-column chunks; load n of GPU g -> key; the maximum
+    // column group w/4 in 32-column chunks; load n of GPU g -> key; the maximum
     // over a candidate's G columns is its step key
     {
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16);
       uint32_t kk[KPT];
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
+      for (int ch = 0; ch < kLtN / NQ / 32; ++ch) {
         uint32_t v[32];
-        tc::tmem_ld32(trow + half * (kLtN / 2) + ch * 32, v);
+        tc::tmem_ld32(trow + cg * (kLtN / NQ) + ch * 32, v);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
@@ -417,15 +423,17 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
         if (KPT % 8 == 4)
           *reinterpret_cast<uint2*>(wst + lane * STG_ROW + (KPT / 8) * 16) =
               make_uint2(kk[KPT - 4] | (kk[KPT - 3] << 16), kk[KPT - 2] | (kk[KPT - 1] << 16));
+        if (KPT == 2) *reinterpret_cast<uint32_t*>(wst + lane * STG_ROW) = kk[0] | (kk[1] << 16);
       } else {
 #pragma unroll
         for (int x4 = 0; x4 < KPT / 4; ++x4)
           *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x4 * 16) =
               make_uint4(kk[4 * x4], kk[4 * x4 + 1], kk[4 * x4 + 2], kk[4 * x4 + 3]);
+        if (KPT == 2) *reinterpret_cast<uint2*>(wst + lane * STG_ROW) = make_uint2(kk[0], kk[1]);
       }
       __syncwarp();
       const int64_t tbase = (int64_t)i * 128 + lg * 32;
-      const int64_t cbase = c0 + half * KPT;
+      const int64_t cbase = c0 + cg * KPT;
       if constexpr (KPT >= KPP) {
         constexpr int PPR = KPT / KPP;  // 16-byte pieces per row
         for (int q = lane; q < 32 * PPR; q += 32) {
@@ -435,10 +443,15 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
             *reinterpret_cast<uint4*>(out + t * Cp + cbase + piece * KPP) =
                 *reinterpret_cast<const uint4*>(wst + r * STG_ROW + piece * 16);
         }
-      } else {  // u16, KPT == 4: one 8-byte piece per row
+      } else if constexpr (KPT * KBY == 8) {  // one 8-byte piece per row
         const int64_t t = tbase + lane;
         if (t < T)
           *reinterpret_cast<uint2*>(out + t * Cp + cbase) = *reinterpret_cast<const uint2*>(wst + lane * STG_ROW);
+      } else {  // u16, KPT == 2: one 4-byte piece per row
+        static_assert(KPT * KBY == 4, "key row pieces of 4, 8 or 16k bytes");
+        const int64_t t = tbase + lane;
+        if (t < T)
+          *reinterpret_cast<uint32_t*>(out + t * Cp + cbase) = *reinterpret_cast<const uint32_t*>(wst + lane * STG_ROW);
       }
     }
     tc::tc_fence_before();
@@ -517,10 +530,10 @@ keysum_kernel(const KT* __restrict__ keys, int64_t T, int64_t C, int64_t Cp, int
 }
 
 // the key staging of one tile (8 warps x 32 steps x KPT keys + pad) must fit the A tile
-template <int E, int G, typename KT>
+template <int E, int G, typename KT, int NW>
 constexpr bool maxkey_fits() {
   constexpr int KH = E == 256 ? 2 : 1;
-  return 8 * 32 * ((kLtN / G / 2) * (int)sizeof(KT) + 16) <= (128 * 16 + 16) * (2 * (E / KH) / 16);
+  return NW * 32 * ((kLtN / G / (NW / 4)) * (int)sizeof(KT) + 16) <= (128 * 16 + 16) * (2 * (E / KH) / 16);
 }
 
 template <int E, typename KT>
@@ -528,24 +541,31 @@ static int launch_maxkey(int G, bool split, dim3 grid, size_t smem, cudaStream_t
                          int64_t T, const int8_t* cand, int64_t C, int64_t L, int64_t l0, int64_t Cp,
                          const KT* keys, int keys_total, const KeyRowConsts& kr, int WS, int WG, KT* out) {
   constexpr int KH = E == 256 ? 2 : 1;
+  constexpr int NW = kLtWarps;
   auto pick = [&](auto kern) -> int {
     GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, kLtThreads, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, keys_total, kr, WS, WG, out);
+    kern<<<grid, NW * 32, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, keys_total, kr, WS, WG, out);
     GEM_CHECK_LAUNCH("maxkey_tc_kernel");
     return GEM_OK;
   };
   auto pick2 = [&](auto k_full, auto k_split) -> int { return split ? pick(k_split) : pick(k_full); };
   switch (G) {
     case 4:
-      if constexpr (maxkey_fits<E, 4, KT>())
-        return pick2(maxkey_tc_kernel<E, 4, KH, false, KT>, maxkey_tc_kernel<E, 4, KH, true, KT>);
+      if constexpr (maxkey_fits<E, 4, KT, NW>())
+        return pick2(maxkey_tc_kernel<E, 4, KH, false, KT, NW>, maxkey_tc_kernel<E, 4, KH, true, KT, NW>);
       else return 1;
     case 8:
-      if constexpr (maxkey_fits<E, 8, KT>())
-        return pick2(maxkey_tc_kernel<E, 8, KH, false, KT>, maxkey_tc_kernel<E, 8, KH, true, KT>);
+      if constexpr (maxkey_fits<E, 8, KT, NW>())
+        return pick2(maxkey_tc_kernel<E, 8, KH, false, KT, NW>, maxkey_tc_kernel<E, 8, KH, true, KT, NW>);
       else return 1;
-    case 16: return pick2(maxkey_tc_kernel<E, 16, KH, false, KT>, maxkey_tc_kernel<E, 16, KH, true, KT>);
-    default: return pick2(maxkey_tc_kernel<E, 32, KH, false, KT>, maxkey_tc_kernel<E, 32, KH, true, KT>);
+    case 16:
+      if constexpr (maxkey_fits<E, 16, KT, NW>())
+        return pick2(maxkey_tc_kernel<E, 16, KH, false, KT, NW>, maxkey_tc_kernel<E, 16, KH, true, KT, NW>);
+      else return 1;
+    default:
+      if constexpr (maxkey_fits<E, 32, KT, NW>())
+        return pick2(maxkey_tc_kernel<E, 32, KH, false, KT, NW>, maxkey_tc_kernel<E, 32, KH, true, KT, NW>);
+      else return 1;
   }
 }
 
@@ -679,6 +699,12 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
     key_smem = (size_t)G * WS * KBY;
   }
   const size_t lt_smem = fixed + key_smem;
+  if (std::getenv("GEM_SCORE_DEBUG")) {  // geometry of the launch, for tools/kbench.py experiments
+    fprintf(stderr, "score_tc: U=%lld W=%d npacked=%d wide=%d split=%d WS=%d WG=%d smem=%zu s_g:", (long long)U, W,
+            npacked, (int)wide, (int)split, WS, WG, lt_smem);
+    for (int g = 0; g < G; ++g) fprintf(stderr, " %d", packed[g]);
+    fprintf(stderr, "\n");
+  }
   if (lt_smem > (size_t)optin) return 1;
   KeyRowConsts kr{};
   for (int g = 0; g < G; ++g) {

@@ -137,6 +137,28 @@ __device__ __forceinline__ double lut_at(const double* __restrict__ lut, int64_t
   return __ldg(lut + g * width + n);
 }
 
+// max over g < G, g != xa, g != xb of C_g(lrow[g]) (-inf when empty): the
+// loads, then the gathers, 8 GPUs per batch in flight (a runtime loop of
+// load -> dependent gather costs two L2 round trips per GPU)
+__device__ __forceinline__ double max_lat_excl(const int32_t* __restrict__ lrow, int G, const double* __restrict__ lut,
+                                               int64_t width, int xa, int xb) {
+  double m = __longlong_as_double(0xfff0000000000000LL);
+  for (int g0 = 0; g0 < G; g0 += 8) {
+    int32_t n[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) n[q] = g0 + q < G ? lrow[g0 + q] : 0;
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int g = g0 + q;
+      v[q] = (g < G && g != xa && g != xb) ? lut_at(lut, width, g, n[q]) : __longlong_as_double(0xfff0000000000000LL);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) m = v[q] > m ? v[q] : m;
+  }
+  return m;
+}
+
 // ---------------------------------------------------------------------------
 // K7: greedy placement, one CTA per run (the exact v1 kernel: any G up to
 // kMaxGpus; the screened K7 v3 below handles G <= 32). Per chunk of tchunk
@@ -624,44 +646,44 @@ __global__ void init_loads_kernel(const int32_t* __restrict__ hist, int64_t T, i
 // the chain over chunk c while warps 1.. fill chunk c+1 (double buffer), so
 // the chain -- the latency floor -- is not serialised with the table gathers.
 constexpr int kScoreChunk = 1024;  // steps per block_score buffer (several gathers in flight per producer)
-__device__ double block_score(const int32_t* __restrict__ ld, int64_t T, int G, const double* __restrict__ lut,
-                              int64_t width, double* buf /*[2][kScoreChunk]*/) {
+// One serial fp64 chain over T terms per CTA: warps 1.. fill chunk k+1 of
+// term(t) into shared memory while thread 0 folds chunk k in t order.
+template <int CHUNK = kScoreChunk, typename Term>
+__device__ double block_chain(int64_t T, double* buf /*[2][CHUNK]*/, Term term) {
   const int nw = blockDim.x >> 5;
   const int ptid = nw > 1 ? (int)threadIdx.x - 32 : (int)threadIdx.x;  // producer index (warps 1..)
   const int np = nw > 1 ? (int)blockDim.x - 32 : (int)blockDim.x;
   auto fill = [&](int64_t t0, double* b) {
-    const int tn = (int)imin64(kScoreChunk, T - t0);
-    for (int tt = ptid; tt < tn; tt += np) {
-      const int32_t* lrow = ld + (t0 + tt) * G;
-      double m = lut_at(lut, width, 0, lrow[0]);
-      for (int g = 1; g < G; ++g) {
-        const double v = lut_at(lut, width, g, lrow[g]);
-        m = v > m ? v : m;
-      }
-      b[tt] = m;
-    }
+    const int tn = (int)imin64(CHUNK, T - t0);
+#pragma unroll 4
+    for (int tt = ptid; tt < tn; tt += np) b[tt] = term(t0 + tt);
   };
   double sum = 0.0;
   if (ptid >= 0) fill(0, buf);
   __syncthreads();
   int k = 0;
-  for (int64_t t0 = 0; t0 < T; t0 += kScoreChunk, k ^= 1) {
-    const int tn = (int)imin64(kScoreChunk, T - t0);
+  for (int64_t t0 = 0; t0 < T; t0 += CHUNK, k ^= 1) {
+    const int tn = (int)imin64(CHUNK, T - t0);
     if (nw == 1) {
       if (threadIdx.x == 0)
-        for (int tt = 0; tt < tn; ++tt) sum = dadd(sum, buf[k * kScoreChunk + tt]);
+        for (int tt = 0; tt < tn; ++tt) sum = dadd(sum, buf[k * CHUNK + tt]);
       __syncthreads();
-      if (t0 + kScoreChunk < T) fill(t0 + kScoreChunk, buf + (k ^ 1) * kScoreChunk);
+      if (t0 + CHUNK < T) fill(t0 + CHUNK, buf + (k ^ 1) * CHUNK);
     } else if (threadIdx.x == 0) {
-      const double* b = buf + k * kScoreChunk;
+      const double* b = buf + k * CHUNK;
 #pragma unroll 8
       for (int tt = 0; tt < tn; ++tt) sum = dadd(sum, b[tt]);
-    } else if (ptid >= 0 && t0 + kScoreChunk < T) {
-      fill(t0 + kScoreChunk, buf + (k ^ 1) * kScoreChunk);
+    } else if (ptid >= 0 && t0 + CHUNK < T) {
+      fill(t0 + CHUNK, buf + (k ^ 1) * CHUNK);
     }
     __syncthreads();
   }
   return sum;  // valid in thread 0
+}
+
+__device__ double block_score(const int32_t* __restrict__ ld, int64_t T, int G, const double* __restrict__ lut,
+                              int64_t width, double* buf /*[2][kScoreChunk]*/) {
+  return block_chain(T, buf, [&](int64_t t) { return max_lat_excl(ld + t * G, G, lut, width, -1, -1); });
 }
 
 __global__ void __launch_bounds__(kSearchThreads)
@@ -1559,12 +1581,16 @@ __global__ void window_kernel(int32_t n_active, int G, double window, double thr
   }
 }
 
-// exact candidate score of one (run, expert pair): one warp, lanes evaluate 32
-// steps in parallel, the fp64 sum is one serial chain in t order (v1's terms).
-__global__ void exact_pairs_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G,
-                                   const double* __restrict__ lut, int64_t nmax,
-                                   const int32_t* __restrict__ run_layer, const int8_t* __restrict__ assign,
-                                   int32_t n_active, SearchWs ws) {
+// exact candidate score of one (run, expert pair) per CTA iteration (grid-
+// strided over the n_active x kCandK slots): warps 1.. evaluate v1's terms,
+// thread 0 extends the serial fp64 chain in t order (block_chain)
+// exact candidate score of one (run, expert pair) per warp (many active runs):
+// lanes fill 256 terms per chunk, lane 0 extends the serial fp64 chain from
+// shared memory
+__global__ void exact_pairs_warp_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G,
+                                        const double* __restrict__ lut, int64_t nmax,
+                                        const int32_t* __restrict__ run_layer, const int8_t* __restrict__ assign,
+                                        int32_t n_active, SearchWs ws) {
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int slot = warp_global / kCandK, k = warp_global % kCandK;
@@ -1577,26 +1603,19 @@ __global__ void exact_pairs_kernel(const int32_t* __restrict__ hist, int64_t T, 
   const int64_t width = nmax + 1;
   const int32_t* h = hist + (int64_t)run_layer[r] * T * E;
   const int32_t* ld = ws.loads + (int64_t)r * T * G;
-  // lanes fill 256 exact terms per chunk (coalesced rows), lane 0 extends the
-  // serial fp64 chain from shared memory (no shuffle round trip per term)
   __shared__ double xbuf[8][256];  // blockDim.x == 256: one row per warp
   double* xb = xbuf[(threadIdx.x >> 5) & 7];
   double sum = 0.0;
   for (int64_t t0 = 0; t0 < T; t0 += 256) {
     const int tn = (int)imin64(256, T - t0);
+#pragma unroll 2
     for (int q = lane; q < tn; q += 32) {
       const int64_t t = t0 + q;
       const int32_t* lrow = ld + t * G;
-      double po = __longlong_as_double(0xfff0000000000000LL);
-      for (int g = 0; g < G; ++g) {
-        if (g == a || g == b) continue;
-        const double v = __ldg(lut + g * width + lrow[g]);
-        po = v > po ? v : po;
-      }
-      const int32_t hi = h[t * E + i], hj = h[t * E + j];
-      const double va = __ldg(lut + a * width + (lrow[a] - hi + hj));
-      const double vb = __ldg(lut + b * width + (lrow[b] - hj + hi));
-      double m = po;
+      const int32_t hi = h[t * E + i], hj = h[t * E + j], la = lrow[a], lb = lrow[b];
+      const double va = __ldg(lut + a * width + (la - hi + hj));
+      const double vb = __ldg(lut + b * width + (lb - hj + hi));
+      double m = max_lat_excl(lrow, G, lut, width, a, b);
       m = va > m ? va : m;
       m = vb > m ? vb : m;
       xb[q] = m;
@@ -1607,6 +1626,42 @@ __global__ void exact_pairs_kernel(const int32_t* __restrict__ hist, int64_t T, 
     __syncwarp();
   }
   if (lane == 0) ws.cand_exact[(int64_t)r * kCandK + k] = sum;
+}
+
+constexpr int kPairThreads = 128;  // exact_pairs: three producer warps + the chain thread's warp
+constexpr int kPairChunk = 512;
+#ifndef GEM_PAIR_CTA_RUNS
+#define GEM_PAIR_CTA_RUNS 320
+#endif
+constexpr int kPairCtaRuns = GEM_PAIR_CTA_RUNS;  // exact_pairs: CTA per pair at <= this many active runs
+__global__ void __launch_bounds__(kPairThreads)
+exact_pairs_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G, const double* __restrict__ lut,
+                   int64_t nmax, const int32_t* __restrict__ run_layer, const int8_t* __restrict__ assign,
+                   int32_t n_active, SearchWs ws) {
+  __shared__ double buf[2 * kPairChunk];
+  const int64_t width = nmax + 1;
+  for (int64_t idx = blockIdx.x; idx < (int64_t)n_active * kCandK; idx += gridDim.x) {
+    const int slot = (int)(idx / kCandK), k = (int)(idx % kCandK);
+    const int r = ws.run_list[slot];
+    if (ws.need_exact[r] || k >= ws.cand_n[r]) continue;  // uniform over the CTA
+    const int f = ws.cand_flat[(int64_t)r * kCandK + k];
+    const int i = f / E, j = f % E;
+    const int a = assign[(int64_t)r * E + i], b = assign[(int64_t)r * E + j];
+    const int32_t* h = hist + (int64_t)run_layer[r] * T * E;
+    const int32_t* ld = ws.loads + (int64_t)r * T * G;
+    const double sum = block_chain<kPairChunk>(T, buf, [&](int64_t t) {
+      const int32_t* lrow = ld + t * G;
+      const int32_t hi = h[t * E + i], hj = h[t * E + j], la = lrow[a], lb = lrow[b];
+      const double va = __ldg(lut + a * width + (la - hi + hj));
+      const double vb = __ldg(lut + b * width + (lb - hj + hi));
+      double m = max_lat_excl(lrow, G, lut, width, a, b);
+      m = va > m ? va : m;
+      m = vb > m ? vb : m;
+      return m;
+    });
+    if (threadIdx.x == 0) ws.cand_exact[(int64_t)r * kCandK + k] = sum;
+    __syncthreads();  // buf is reused by the next slot
+  }
 }
 
 // per active run without overflow: lexicographic (exact cand, flat) minimum
@@ -2017,9 +2072,13 @@ static int launch_scan(const int32_t* hist, int64_t T, int32_t E, int32_t G, con
   }
   window_kernel<<<(unsigned)((n_active + 127) / 128), 128, 0, st>>>((int32_t)n_active, G, window, thr, ws);
   GEM_CHECK_LAUNCH("window_kernel");
-  const int64_t warps = n_active * kCandK;
-  exact_pairs_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(hist, T, E, G, lut, nmax, run_layer,
-                                                                           assign, (int32_t)n_active, ws);
+  const int64_t slots = n_active * kCandK;
+  if (n_active > kPairCtaRuns)  // many runs: a warp per pair keeps more chains in flight
+    exact_pairs_warp_kernel<<<(unsigned)((slots * 32 + 255) / 256), 256, 0, st>>>(
+        hist, T, E, G, lut, nmax, run_layer, assign, (int32_t)n_active, ws);
+  else  // few runs: a CTA per pair, its chain fed by three producer warps
+    exact_pairs_kernel<<<(unsigned)imin64(slots, 16 * num_sms()), kPairThreads, 0, st>>>(
+        hist, T, E, G, lut, nmax, run_layer, assign, (int32_t)n_active, ws);
   GEM_CHECK_LAUNCH("exact_pairs_kernel");
   select_pairs_kernel<<<(unsigned)((n_active + 127) / 128), 128, 0, st>>>((int32_t)n_active, E, ws);
   GEM_CHECK_LAUNCH("select_pairs_kernel");
