@@ -26,6 +26,11 @@ namespace gem {
 
 constexpr int kSearchThreads = 256;
 constexpr int kGreedyTChunk = 256;
+#ifndef GEM_GREEDY_REFINE
+#define GEM_GREEDY_REFINE 1
+#endif
+constexpr bool kGreedyRefine = GEM_GREEDY_REFINE;         // fp64 parallel screen before the exact chains
+constexpr double kRefineWindow = 1.0 + 1.0 / 68719476736.0;  // 1 + 2^-36
 constexpr int kSwapTChunk = 64;
 constexpr int kSwapPairsPerThread = 4;
 // screening window: exact winners satisfy approx <= min(approx) * (1 + 2^-20) (see K6 v3 / K7 v2)
@@ -501,10 +506,76 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
       if (gstar < G) s_cand[nc++] = gstar;
       s_ncand = nc;
       s_best = s_cand[0];
-      if (nc > 1) atomicAdd(&ws.counters[2], 1);  // statistics: exact re-scores
     }
     __syncthreads();
+    if (s_ncand > 1 && kGreedyRefine) {
+      // ---- fp64 screen of the window's GPUs: the exact terms (v1 arithmetic)
+      // summed in parallel (per thread, then a warp tree, then warps in order:
+      // <= T/threads + 5 + warps adds per term), so every score is within
+      // 2^-38.9 of its serial chain (which is within T 2^-53 of the real sum);
+      // GPUs above min * kRefineWindow cannot hold the strict-< minimum. A
+      // single survivor is the winner; ties and near-ties go to the chains.
+      const int nc = s_ncand;
+      double a64[GM];
+#pragma unroll
+      for (int c = 0; c < GM; ++c) a64[c] = 0.0;
+      for (int64_t t = tid; t < T; t += blockDim.x) {
+        double m1 = -1.0, m2 = -1.0;
+        int i1 = -1;
+        if (TOP2) {
+          const double2 d = td[t];
+          m1 = d.x;
+          m2 = d.y;
+          i1 = ta[t];
+        } else {
+          for (int q = 0; q < G; ++q) {
+            const double v = __ldg(lut + q * width + ld[LDI(t, q)]);
+            if (v > m1) { m2 = m1; m1 = v; i1 = q; }
+            else if (v > m2) { m2 = v; }
+          }
+        }
+        const int hv = hcol[t];
+#pragma unroll
+        for (int c = 0; c < GM; ++c) {
+          if (c >= nc) break;
+          const int g = s_cand[c];
+          const double cl = __ldg(lut + g * width + (int64_t)ld[LDI(t, g)] + hv);
+          double scv = cl;
+          if (G > 1) {
+            const double others = (i1 == g) ? m2 : m1;
+            scv = others > cl ? others : cl;
+          }
+          a64[c] += scv;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < GM; ++c) {
+        if (c >= nc) break;
+        double v = a64[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[warp * GM + c] = v;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double mn = __longlong_as_double(0x7ff0000000000000LL);
+        for (int c = 0; c < nc; ++c) {
+          double v = 0.0;
+          for (int w = 0; w < nwarps; ++w) v += red[w * GM + c];
+          red[c] = v;  // warp 0's slots are consumed in order
+          mn = fmin(mn, v);
+        }
+        const double lim = mn * kRefineWindow;
+        int k = 0;
+        for (int c = 0; c < nc; ++c)
+          if (red[c] <= lim) s_cand[k++] = s_cand[c];  // ascending GPU order is kept
+        s_ncand = k;
+        s_best = s_cand[0];
+      }
+      __syncthreads();
+    }
     if (s_ncand > 1) {
+      if (tid == 0) atomicAdd(&ws.counters[2], 1);  // statistics: exact re-scores
       // ---- exact serial scores of the window's GPUs (v1 arithmetic, t order):
       // per chunk all threads fill the exact terms of every window GPU (one
       // exact top-2 per step), then thread c extends candidate c's serial chain

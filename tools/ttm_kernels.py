@@ -1,6 +1,7 @@
 """Device-time breakdown of one full-trace time-to-mapping search (GPU box).
 
-usage: python tools/ttm_kernels.py [window_steps]   (default: the full trace)
+usage: python tools/ttm_kernels.py [window_steps] [--c5]   (default: the full trace, Qwen3-235B shape;
+       --c5: DeepSeek-V3 shape, 58 layers x 256 experts on 32 GPUs)
 Prints wall time, summed kernel time and the per-kernel totals (CUPTI via torch.profiler).
 """
 import sys
@@ -15,7 +16,7 @@ import importlib  # noqa: E402
 from paper_2605_19945_b200 import ingest  # noqa: E402
 S = importlib.import_module("paper_2605_19945_b200.search")
 
-L, N, k, E, B, G = 94, 1 << 24, 8, 128, 1024, 8
+L, N, k, E, B, G = (58, 1 << 24, 8, 256, 1024, 32) if "--c5" in sys.argv else (94, 1 << 24, 8, 128, 1024, 8)
 spec = ingest.TopkTraceSpec(num_layers=L, num_tokens=N, top_k=k, num_experts=E, tokens_per_step=B, seed=0)
 ids = ingest.generate_topk_ids(spec)
 st = ingest.trace_statistics(ids, B, E)
@@ -43,7 +44,7 @@ tot = sum(r[1] for r in rows)
 print(f"profiled wall {1e3 * wall:.1f} ms, kernel total {tot:.1f} ms")
 for name, ms, n in rows[:25]:
     print(f"{ms:10.2f} ms {n:6d}  {name[:90]}")
-if "--rounds" in sys.argv or True:
+if True:  # per-launch device times of the refinement kernels, in launch order
     seq = {}
     for e in p.events():
         if e.device_time_total > 0 and any(s in e.name for s in ("approx_scan5", "exact_pairs", "apply_swap", "best_swap")):
