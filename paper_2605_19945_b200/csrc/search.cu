@@ -334,6 +334,49 @@ __global__ void hist_t16_kernel(const int32_t* __restrict__ hist, int64_t T, int
   }
 }
 
+// Piecewise-linear fp32 rows for K7's approximate pass when the fp32 table is
+// off-chip (G = 32 with a wide window): bucket j >= 1 covers the loads
+// (64(j-1), 64j] -- the profiles' tile staircase and the sparse interpolation
+// segments above the dense limit are linear on them -- and bucket 0 the load
+// 0: C'(n) = a_j + b_j (n - n0_j), n0_j = 64(j-1)+1, with (a_j, b_j) =
+// (fl32 C(n0_j), fl32 of the bucket's slope). pw_check_kernel flags any row
+// where some n in [0, W) misses C(n) by more than 2^-22 C(n); the greedy then
+// keeps the global fp32 table. 64 B of shared memory per 64 loads per GPU
+// instead of 256 B in L1/L2.
+constexpr int kPwShift = 6;
+__host__ __device__ constexpr int pw_buckets(int W) { return ((W - 1 + (1 << kPwShift) - 1) >> kPwShift) + 1; }
+__device__ __forceinline__ int pw_bucket(uint32_t n) { return (int)((n + (1u << kPwShift) - 1u) >> kPwShift); }
+__device__ __forceinline__ float pw_eval(float2 ab, uint32_t n, int j) {
+  return fmaf(ab.y, (float)((int)n - (((j - 1) << kPwShift) + 1)), ab.x);
+}
+__global__ void pw_table_kernel(const double* __restrict__ lut, int64_t width, int G, int W, float2* __restrict__ pw) {
+  const int K = pw_buckets(W);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < G * K; i += gridDim.x * blockDim.x) {
+    const int g = i / K, j = i - g * K;
+    const double* row = lut + (int64_t)g * width;
+    if (j == 0) {
+      pw[i] = make_float2((float)row[0], 0.0f);
+      continue;
+    }
+    const int n0 = ((j - 1) << kPwShift) + 1, n1 = min(j << kPwShift, W - 1);
+    const double c0 = row[n0];
+    const float b = n1 > n0 ? (float)((row[n1] - c0) / (double)(n1 - n0)) : 0.0f;
+    pw[i] = make_float2((float)c0, b);
+  }
+}
+__global__ void pw_check_kernel(const double* __restrict__ lut, int64_t width, int G, int W,
+                                const float2* __restrict__ pw, int32_t* __restrict__ bad) {
+  const int K = pw_buckets(W);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)G * W;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int g = (int)(i / W), n = (int)(i - (int64_t)g * W);
+    const int j = pw_bucket((uint32_t)n);
+    const double c = lut[(int64_t)g * width + n];
+    const double a = (double)pw_eval(pw[g * K + j], (uint32_t)n, j);
+    if (!(c >= 0.0) || !(fabs(a - c) <= c * 0x1p-22)) atomicOr(bad, 1);
+  }
+}
+
 // FULL: G == GM (no padded GPU columns: the per-GPU guards vanish at compile time)
 // SL: the fp32 table window [G][W] sits in shared memory; otherwise (G = 32
 // with a wide window) the gathers read ws.lut32 through L1/L2
@@ -349,13 +392,15 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
                const double* __restrict__ lut, int64_t nmax, int W, const int32_t* __restrict__ run_layer,
                const uint8_t* __restrict__ needs_greedy, const int16_t* __restrict__ order,
                int8_t* __restrict__ assign, uint16_t* __restrict__ loads16, SearchWs ws,
-               float2* __restrict__ top_p, double2* __restrict__ top_d, uint8_t* __restrict__ top_a) {
+               float2* __restrict__ top_p, double2* __restrict__ top_d, uint8_t* __restrict__ top_a,
+               const float2* __restrict__ pw, const int32_t* __restrict__ pw_bad) {
   const int G = FULL ? GM : G_;
   extern __shared__ __align__(16) unsigned char g2s[];
   float* s_lut = reinterpret_cast<float*>(g2s);                                        // [G][W] (SL)
   const uint32_t lut_base = (uint32_t)__cvta_generic_to_shared(s_lut);
   double* red = reinterpret_cast<double*>(g2s + (SL ? (((size_t)G * W * 4 + 15) & ~size_t(15)) : 0));  // [warps][GM]
   double* buf = red + (g2_threads(GM) / 32) * GM;                                          // [kGreedyTChunk]
+  float2* s_pw = reinterpret_cast<float2*>(buf + kGreedyTChunk * GM);                       // [G][K] (!SL, pw)
   __shared__ int counts[GM];
   __shared__ int s_best, s_ncand;
   __shared__ int s_cand[GM];
@@ -379,6 +424,11 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
     if (SL) return lds_f32(row_addr[g] + 4u * nn);
     return __ldg(ws.lut32 + (int64_t)(g < G ? g : G - 1) * width + nn);
   };
+  // !SL: the piecewise rows in shared memory when they reproduce the table (pw_check_kernel)
+  const bool usepw = !SL && pw != nullptr && *pw_bad == 0;
+  const int pwK = pw_buckets(W);
+  if (usepw)
+    for (int i = tid; i < G * pwK; i += blockDim.x) s_pw[i] = pw[i];
   if (tid < GM) counts[tid] = 0;
   if (tid == 0) s_exc = 0u;
   for (int64_t i = tid; i < T * GM; i += blockDim.x) ld[i] = 0;
@@ -421,7 +471,8 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
       acc[g] = 0.0;
       row_addr[g] = lut_base + 4u * (uint32_t)(g < G ? g : G - 1) * (uint32_t)W;
     }
-    {
+    auto approx_pass = [&](auto pw_tag) {
+      constexpr bool PW = decltype(pw_tag)::value;
 #pragma unroll kGreedyUnroll
     for (int64_t t = tid; t < T; t += blockDim.x) {
       const uint32_t hv = (uint32_t)hcol[t];
@@ -463,12 +514,27 @@ greedy2_kernel(const int32_t* __restrict__ hist, int64_t T, int E, int G_,
       for (int g = 0; g < GM; ++g) {
         // a GPU with free capacity never exceeds the window (l + h <= U); a
         // full one (ignored by the selection) is clamped to stay inside it
-        const float cl = tab(row_addr, g, min(lrow[g] + hv, wlast));
+        float cl;
+        if constexpr (PW) {  // within 2^-22 of C: the exc test below keeps a 2^-20 margin
+          const uint32_t nn = min(lrow[g] + hv, wlast);
+          const int j = pw_bucket(nn);
+          cl = pw_eval(s_pw[(g < G ? g : G - 1) * pwK + j], nn, j);
+        } else {
+          cl = tab(row_addr, g, min(lrow[g] + hv, wlast));
+        }
         const float pm = TOP2 ? (g == parg ? p12.y : p12.x) : fmaxf(pre[g], suf[g + 1]);
         acc[g] += (double)fmaxf(pm, cl);  // g >= G: ignored by the selection
-        if (hv != 0u && cl >= pm) exc |= 1u << g;  // hv == 0: the term is the step maximum exactly
+        // hv == 0: the term is the step maximum exactly; PW: cl may sit 2^-22
+        // below C, so only cl (1 + 2^-20) < pm proves C < the others' maximum
+        if (hv != 0u && (PW ? cl * (1.0f + 0x1p-20f) >= pm : cl >= pm)) exc |= 1u << g;
       }
     }
+    };
+    if constexpr (!SL) {
+      if (usepw) approx_pass(std::true_type{});
+      else approx_pass(std::false_type{});
+    } else {
+      approx_pass(std::false_type{});
     }
 #pragma unroll
     for (int g = 0; g < GM; ++g) {
@@ -2185,11 +2251,26 @@ static int launch_greedy(const int32_t* hist, int64_t T, int32_t E, int32_t G, c
         GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&td), (size_t)R * T * sizeof(double2), st));
         GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ta), (size_t)R * T, st));
       }
+      // off-chip table: piecewise rows in shared memory when they reproduce it (GEM_GREEDY_NOPW=1 disables)
+      float2* pw = nullptr;
+      int32_t* pw_bad = nullptr;
+      const size_t pw_bytes = (size_t)G * pw_buckets(W) * sizeof(float2);
+      if (!sl && !std::getenv("GEM_GREEDY_NOPW") && smem + pw_bytes <= (size_t)optin) {
+        GEM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pw), pw_bytes + 16, st));
+        pw_bad = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(pw) + pw_bytes);
+        GEM_CHECK_CUDA(cudaMemsetAsync(pw_bad, 0, 4, st));
+        pw_table_kernel<<<(unsigned)((G * pw_buckets(W) + 255) / 256), 256, 0, st>>>(lut, nmax + 1, G, W, pw);
+        GEM_CHECK_LAUNCH("pw_table_kernel");
+        pw_check_kernel<<<(unsigned)imin64(((int64_t)G * W + 255) / 256, 4 * num_sms()), 256, 0, st>>>(
+            lut, nmax + 1, G, W, pw, pw_bad);
+        GEM_CHECK_LAUNCH("pw_check_kernel");
+        smem += pw_bytes;
+      }
       auto go = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         kern<<<(unsigned)R, g2_threads(GM), smem, st>>>(hist, T, E, G, lut, nmax, W, run_layer, needs_greedy, order,
-                                                    assign, l16, ws, tp, td, ta);
+                                                    assign, l16, ws, tp, td, ta, pw, pw_bad);
         return cudaGetLastError();
       };
       auto pick = [&](auto tag) -> cudaError_t {
@@ -2209,6 +2290,7 @@ static int launch_greedy(const int32_t* hist, int64_t T, int32_t E, int32_t G, c
       };
       const cudaError_t ek = top2 ? pick(std::true_type{}) : pick(std::false_type{});
       cudaFreeAsync(l16, st);
+      if (pw) cudaFreeAsync(pw, st);
       if (top2) {
         cudaFreeAsync(tp, st);
         cudaFreeAsync(td, st);
