@@ -46,7 +46,13 @@ __global__ void topn_bound_kernel(const int32_t* __restrict__ hist, int64_t L, i
 #ifndef GEM_LT_WARPS
 #define GEM_LT_WARPS 8
 #endif
+#ifndef GEM_LT_WARPS_SKIP
+#define GEM_LT_WARPS_SKIP 16
+#endif
 constexpr int kLtWarps = GEM_LT_WARPS;  // maxkey CTA: 8 or 16 warps (4 per TMEM lane quarter per column group)
+// with step floors (G >= 16): the skipped columns free registers (122 at
+// DeepSeek-V3 shapes), and 16 warps hide the gathers' latency better
+constexpr int kLtWarpsSkip = GEM_LT_WARPS_SKIP;
 constexpr int kLtN = 256;        // MMA N (candidate x GPU columns per CTA)
 constexpr int kMaxKeys = 65536;  // u16 keys
 constexpr int kSumThreads = 256;
@@ -168,6 +174,83 @@ __global__ void key_rows_kernel(const double* __restrict__ lut, int64_t width, i
   }
 }
 
+// Per-GPU key-row constants of K5 (byte offsets; see maxkey_tc_kernel)
+struct KeyRowConsts {
+  int32_t koff[32];
+  int32_t kbase[32];
+  int32_t kend[32];
+  int32_t goff[32];
+};
+
+// Step floor (K5 at G >= 16). Every expert sits on some GPU, so a step whose
+// largest expert count is h has a GPU with load >= h, and with nondecreasing
+// rows its maximum is >= v(h) = min_g lut[g][h]. A GPU whose load n is <= the
+// step's skip level s(h) = min_g (last n' with lut[g][n'] <= v(h)) has latency
+// <= v(h), so it cannot raise the maximum above the floor: the epilogue starts
+// each step's maximum at the floor's key and gathers only the GPUs above s(h)
+// (skipped with a warp-uniform branch when all 32 steps of a warp are at or
+// below it -- at DeepSeek-V3 shapes only the GPUs that hold the step's heavy
+// experts). The floor key is the clamped key of (argmin g, h) -- the same entry
+// the gather itself would read, which is <= the key of the maximum (h >= s_g:
+// it is v(h) itself; h < s_g: the gather-clamp value, <= every maximum).
+// Rows that decrease anywhere (bad bit 1) disable the skip: level -1, key 0.
+// table[h] = {s(h), key}, h in [0, W)
+template <typename KT>
+__global__ void floor_table_kernel(const double* __restrict__ lut, int64_t width, int G, int W,
+                                   const int32_t* __restrict__ bad, const KT* __restrict__ gkeys,
+                                   const __grid_constant__ KeyRowConsts kr, int2* __restrict__ table) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= W) return;
+  if (*bad & 2) {
+    table[h] = make_int2(-1, 0);
+    return;
+  }
+  double v = lut[h];
+  int gp = 0;
+  for (int g = 1; g < G; ++g) {
+    const double x = lut[(int64_t)g * width + h];
+    if (x < v) v = x, gp = g;
+  }
+  int smin = INT32_MAX;
+  for (int g = 0; g < G; ++g) {  // first n with row[n] > v, minus one (>= h for g = gp)
+    const double* row = lut + (int64_t)g * width;
+    int lo = 0, hi = W;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (row[mid] <= v) lo = mid + 1; else hi = mid;
+    }
+    smin = min(smin, lo - 1);
+  }
+  const int32_t rel = max((int32_t)sizeof(KT) * h + kr.koff[gp], kr.kbase[gp]);
+  const KT key = *reinterpret_cast<const KT*>(reinterpret_cast<const char*>(gkeys) + rel + kr.goff[gp]);
+  table[h] = make_int2(smin, (int)key);
+}
+
+// per step of every layer: {skip level, floor key} of its largest expert count
+// (kmin: the smallest floor key -- no step maximum ranks below it; keysum
+// stages the values from there)
+__global__ void step_floor_kernel(const int32_t* __restrict__ hist, int64_t rows, int E, int W,
+                                  const int2* __restrict__ table, int2* __restrict__ floor_out,
+                                  int32_t* __restrict__ kmin) {
+  const int lane = threadIdx.x & 31;
+  int32_t kl = INT32_MAX;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w0; r < rows; r += nw) {
+    const int32_t* row = hist + r * E;
+    int32_t m = 0;
+    for (int e = lane; e < E; e += 32) m = max(m, row[e]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+      const int2 f = table[min(m, W - 1)];  // m <= U = W - 1 (the load bound)
+      floor_out[r] = f;
+      kl = min(kl, f.y);
+    }
+  }
+  if (lane == 0 && kl != INT32_MAX) atomicMin(kmin, kl);
+}
+
 // bits[i] = the fp64 pattern of lut[g][n] over the packed rows n in [s_g, U]
 // (rowinfo as in key_rows_kernel): only these values can be gathered
 __global__ void row_bits_kernel(const double* __restrict__ lut, int64_t width, int G,
@@ -208,20 +291,28 @@ __global__ void row_bits_kernel(const double* __restrict__ lut, int64_t width, i
 // 32 spilled). Byte offsets relative to the shared key rows:
 //   rel = max(KBY*n + koff[g], kbase[g])  -- the clamped key's offset;
 //   SPLIT: rel < kend[g] reads shared memory, else the global table at byte
-//   offset rel + goff[g].
-struct KeyRowConsts {
-  int32_t koff[32];
-  int32_t kbase[32];
-  int32_t kend[32];
-  int32_t goff[32];
-};
+//   offset rel + goff[g].  (KeyRowConsts above.)
 
 // KT: u16 keys, or u32 when the window holds more than 65,536 distinct latencies.
-template <int E, int G, int KH, bool SPLIT, typename KT, int NW>
+// key gathers: volatile under SKIP so they stay inside their warp-uniform
+// branch (not speculated above it); free to schedule otherwise
+#define GEM_KEY_LD(...)                 \
+  do {                                  \
+    if constexpr (SKIP)                 \
+      asm volatile(__VA_ARGS__);        \
+    else                                \
+      asm(__VA_ARGS__);                 \
+  } while (0)
+
+// SKIP: step floors (floor_tab [L][T] = {skip level, floor key}, see
+// floor_table_kernel): a GPU column is gathered only when one of the warp's 32
+// steps has its load above the step's skip level.
+template <int E, int G, int KH, bool SPLIT, typename KT, int NW, bool SKIP>
 __global__ void __launch_bounds__(NW * 32, 1)
 maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __restrict__ cand, int64_t C,
                  int64_t L, int64_t layer0, int64_t Cp, const KT* __restrict__ gkeys, int keys_total,
-                 const __grid_constant__ KeyRowConsts kr, int WS, int WG, KT* __restrict__ out_keys) {
+                 const __grid_constant__ KeyRowConsts kr, int WS, int WG, const int2* __restrict__ floor_tab,
+                 KT* __restrict__ out_keys) {
   constexpr int KBY = (int)sizeof(KT);       // bytes per key
   constexpr int EH = E / KH;                 // experts per K part
   constexpr int KBH = 2 * EH;                // K bytes per step row per part: [lo | hi16]
@@ -347,7 +438,13 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
   };
   uint32_t mma_phase = 0;
   load_rows(0, 0);
+  const int2* fl_l = SKIP ? floor_tab + l * T : nullptr;
   for (int i = 0; i < ntiles; ++i) {
+    int2 fl = make_int2(INT32_MAX, 0);  // this lane's step (TMEM lane): {skip level, floor key}
+    if constexpr (SKIP) {
+      const int64_t ts = (int64_t)i * 128 + lg * 32 + lane;
+      if (ts < T) fl = __ldg(fl_l + ts);
+    }
 #pragma unroll
     for (int part = 0; part < KH; ++part) {
       write_a();
@@ -376,37 +473,51 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
         tc::tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
-          uint32_t m = 0;
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
+          auto gather = [&](int g) -> uint32_t {
             uint32_t key;
             const int32_t rel = max((int32_t)v[j * G + g] * KBY + kr.koff[g], kr.kbase[g]);
             const uint32_t sak = sk_addr + (uint32_t)rel;
             if (!SPLIT) {
               if constexpr (KBY == 2) {
                 uint16_t k16;
-                asm("ld.shared.u16 %0, [%1];" : "=h"(k16) : "r"(sak));
+                GEM_KEY_LD("ld.shared.u16 %0, [%1];" : "=h"(k16) : "r"(sak));
                 key = k16;
               } else {
-                asm("ld.shared.u32 %0, [%1];" : "=r"(key) : "r"(sak));
+                GEM_KEY_LD("ld.shared.u32 %0, [%1];" : "=r"(key) : "r"(sak));
               }
             } else {
               const char* ga = gk_bytes + (rel + kr.goff[g]);
               if constexpr (KBY == 2) {
                 uint16_t k16;
-                asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t"
+                GEM_KEY_LD("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t"
                     "@p ld.shared.u16 %0, [%3];\n\t@!p ld.global.nc.u16 %0, [%4];\n\t}"
                     : "=h"(k16)
                     : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga));
                 key = k16;
               } else {
-                asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t"
+                GEM_KEY_LD("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t"
                     "@p ld.shared.u32 %0, [%3];\n\t@!p ld.global.nc.u32 %0, [%4];\n\t}"
                     : "=r"(key)
                     : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga));
               }
             }
-            m = max(m, key);
+            return key;
+          };
+          uint32_t m = 0u;
+          if constexpr (SKIP) {
+            // warp-uniform set of the GPU columns with a load above the skip
+            // level in any of the warp's 32 steps; their gathers are issued
+            // back to back (the maximum is taken after the last one)
+            uint32_t kx[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+              kx[g] = __any_sync(0xffffffffu, (int32_t)v[j * G + g] > fl.x) ? gather(g) : 0u;
+            m = (uint32_t)fl.y;
+#pragma unroll
+            for (int g = 0; g < G; ++g) m = max(m, kx[g]);
+          } else {
+#pragma unroll
+            for (int g = 0; g < G; ++g) m = max(m, gather(g));
           }
           kk[ch * CPL + j] = m;
         }
@@ -485,21 +596,29 @@ template <> struct Key4<uint32_t> {
 template <typename KT>
 __global__ void __launch_bounds__(kSumThreads, 3)
 keysum_kernel(const KT* __restrict__ keys, int64_t T, int64_t C, int64_t Cp, int64_t L, int64_t layer0,
-              const double* __restrict__ vals, const int32_t* __restrict__ nvals, double* __restrict__ layer_scores) {
+              const double* __restrict__ vals, const int32_t* __restrict__ nvals, const int32_t* __restrict__ vbase,
+              double* __restrict__ layer_scores) {
   using K4 = Key4<KT>;
   using V = typename K4::V;
   extern __shared__ double s_vals[];  // [kSumSmemVals]
-  const int K = min(*nvals, kSumSmemVals);
-  for (int i = threadIdx.x; i < K; i += blockDim.x) s_vals[i] = vals[i];
+  // vals[base, base + K) in shared memory: base = the smallest step-floor key
+  // when the floors ran (G >= 16: the keys a maximum can take start there), else 0
+  const int base = vbase ? *vbase : 0;
+  const int K = max(0, min(*nvals - base, kSumSmemVals));
+  for (int i = threadIdx.x; i < K; i += blockDim.x) s_vals[i] = vals[base + i];
   __syncthreads();
   const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int64_t lb = blockIdx.y;
   if (c0 >= C) return;
   const V* p = reinterpret_cast<const V*>(keys + lb * T * Cp + c0);
   const int64_t stride = Cp / 4;  // V per step
-  auto val = [&](uint32_t k) -> double { return k < (uint32_t)kSumSmemVals ? s_vals[k] : __ldg(vals + k); };
-  // keys 8 steps ahead of the serial fp64 chains (which stay in t order)
-  constexpr int D = 8;
+  auto val = [&](uint32_t k) -> double {
+    const uint32_t r = k - (uint32_t)base;
+    return r < (uint32_t)K ? s_vals[r] : __ldg(vals + k);
+  };
+  // keys 64 bytes ahead of the serial fp64 chains (which stay in t order):
+  // 8 steps of u16 keys, 4 of u32 (8 x 16 bytes spilled under 3 CTAs/SM)
+  constexpr int D = sizeof(KT) == 2 ? 8 : 4;
   V q[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) q[d] = d < T ? __ldcs(p + (int64_t)d * stride) : K4::zero();
@@ -537,34 +656,43 @@ constexpr bool maxkey_fits() {
 }
 
 template <int E, typename KT>
-static int launch_maxkey(int G, bool split, dim3 grid, size_t smem, cudaStream_t st, const int32_t* hist,
+static int launch_maxkey(int G, bool split, bool skip, dim3 grid, size_t smem, cudaStream_t st, const int32_t* hist,
                          int64_t T, const int8_t* cand, int64_t C, int64_t L, int64_t l0, int64_t Cp,
-                         const KT* keys, int keys_total, const KeyRowConsts& kr, int WS, int WG, KT* out) {
+                         const KT* keys, int keys_total, const KeyRowConsts& kr, int WS, int WG, const int2* fl,
+                         KT* out) {
   constexpr int KH = E == 256 ? 2 : 1;
-  constexpr int NW = kLtWarps;
+  constexpr int NW = kLtWarps, NWS = kLtWarpsSkip;
   auto pick = [&](auto kern) -> int {
     GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, NW * 32, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, keys_total, kr, WS, WG, out);
+    kern<<<grid, (skip ? NWS : NW) * 32, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, keys_total, kr, WS, WG, fl,
+                                                     out);
     GEM_CHECK_LAUNCH("maxkey_tc_kernel");
     return GEM_OK;
   };
   auto pick2 = [&](auto k_full, auto k_split) -> int { return split ? pick(k_split) : pick(k_full); };
+  // step floors only where a GPU holds few experts (G >= 16): most GPU columns
+  // of a warp's 32 steps then sit below the floor and are skipped
+  auto pick4 = [&](auto k_full, auto k_split, auto k_full_skip, auto k_split_skip) -> int {
+    return skip ? pick2(k_full_skip, k_split_skip) : pick2(k_full, k_split);
+  };
   switch (G) {
     case 4:
       if constexpr (maxkey_fits<E, 4, KT, NW>())
-        return pick2(maxkey_tc_kernel<E, 4, KH, false, KT, NW>, maxkey_tc_kernel<E, 4, KH, true, KT, NW>);
+        return pick2(maxkey_tc_kernel<E, 4, KH, false, KT, NW, false>, maxkey_tc_kernel<E, 4, KH, true, KT, NW, false>);
       else return 1;
     case 8:
       if constexpr (maxkey_fits<E, 8, KT, NW>())
-        return pick2(maxkey_tc_kernel<E, 8, KH, false, KT, NW>, maxkey_tc_kernel<E, 8, KH, true, KT, NW>);
+        return pick2(maxkey_tc_kernel<E, 8, KH, false, KT, NW, false>, maxkey_tc_kernel<E, 8, KH, true, KT, NW, false>);
       else return 1;
     case 16:
-      if constexpr (maxkey_fits<E, 16, KT, NW>())
-        return pick2(maxkey_tc_kernel<E, 16, KH, false, KT, NW>, maxkey_tc_kernel<E, 16, KH, true, KT, NW>);
+      if constexpr (maxkey_fits<E, 16, KT, NW>() && maxkey_fits<E, 16, KT, NWS>())
+        return pick4(maxkey_tc_kernel<E, 16, KH, false, KT, NW, false>, maxkey_tc_kernel<E, 16, KH, true, KT, NW, false>,
+                     maxkey_tc_kernel<E, 16, KH, false, KT, NWS, true>, maxkey_tc_kernel<E, 16, KH, true, KT, NWS, true>);
       else return 1;
     default:
-      if constexpr (maxkey_fits<E, 32, KT, NW>())
-        return pick2(maxkey_tc_kernel<E, 32, KH, false, KT, NW>, maxkey_tc_kernel<E, 32, KH, true, KT, NW>);
+      if constexpr (maxkey_fits<E, 32, KT, NW>() && maxkey_fits<E, 32, KT, NWS>())
+        return pick4(maxkey_tc_kernel<E, 32, KH, false, KT, NW, false>, maxkey_tc_kernel<E, 32, KH, true, KT, NW, false>,
+                     maxkey_tc_kernel<E, 32, KH, false, KT, NWS, true>, maxkey_tc_kernel<E, 32, KH, true, KT, NWS, true>);
       else return 1;
   }
 }
@@ -740,6 +868,28 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   if (P < 1) return 1;
   void* kbuf = alloc(per_layer * P);
   if (!kbuf) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc key buffer");
+  // step floors (G >= 16; GEM_SCORE_NOSKIP turns them off): {skip level, floor
+  // key} per load level h in [0, W), then per step of every layer
+  const bool skip = G >= 16 && !std::getenv("GEM_SCORE_NOSKIP");
+  int2* floors = nullptr;
+  int32_t* kmin = nullptr;
+  if (skip) {
+    int2* ftab = static_cast<int2*>(alloc((size_t)W * 8));
+    floors = static_cast<int2*>(alloc((size_t)L * T * 8));
+    kmin = static_cast<int32_t*>(alloc(4));
+    if (!ftab || !floors || !kmin) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc step floors");
+    GEM_CHECK_CUDA(cudaMemsetAsync(kmin, 0x7f, 4, st));
+    if (wide)
+      floor_table_kernel<uint32_t><<<(W + 127) / 128, 128, 0, st>>>(lut, nmax + 1, G, W, bnd_d + 3 + 2 * L,
+                                                                   static_cast<const uint32_t*>(keys), kr, ftab);
+    else
+      floor_table_kernel<uint16_t><<<(W + 127) / 128, 128, 0, st>>>(lut, nmax + 1, G, W, bnd_d + 3 + 2 * L,
+                                                                   static_cast<const uint16_t*>(keys), kr, ftab);
+    GEM_CHECK_LAUNCH("floor_table_kernel");
+    step_floor_kernel<<<(unsigned)imin64((L * T + 7) / 8, 32 * num_sms()), 256, 0, st>>>(hist, L * T, E, W, ftab,
+                                                                                         floors, kmin);
+    GEM_CHECK_LAUNCH("step_floor_kernel");
+  }
   auto run = [&](auto kt) -> int {
     using KT = decltype(kt);
     auto ks = keysum_kernel<KT>;
@@ -752,15 +902,15 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
       const int64_t nb = imin64(P, L - l0);
       const dim3 g1((unsigned)ntile, (unsigned)nb);
       const int rc =
-          E == 256 ? launch_maxkey<256, KT>(G, split, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
-                                            keys_total, kr, WS, WG, kt_buf)
-          : E == 128 ? launch_maxkey<128, KT>(G, split, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
-                                              keys_total, kr, WS, WG, kt_buf)
-                     : launch_maxkey<64, KT>(G, split, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
-                                             keys_total, kr, WS, WG, kt_buf);
+          E == 256 ? launch_maxkey<256, KT>(G, split, skip, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
+                                            keys_total, kr, WS, WG, floors, kt_buf)
+          : E == 128 ? launch_maxkey<128, KT>(G, split, skip, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
+                                              keys_total, kr, WS, WG, floors, kt_buf)
+                     : launch_maxkey<64, KT>(G, split, skip, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
+                                             keys_total, kr, WS, WG, floors, kt_buf);
       if (rc) return rc;
       ks<<<dim3((unsigned)((C + 4 * kSumThreads - 1) / (4 * kSumThreads)), (unsigned)nb), kSumThreads,
-           (size_t)kSumSmemVals * 8, st>>>(kt_buf, T, C, Cp, L, l0, vals, nu, layer_scores);
+           (size_t)kSumSmemVals * 8, st>>>(kt_buf, T, C, Cp, L, l0, vals, nu, kmin, layer_scores);
       GEM_CHECK_LAUNCH("keysum_kernel");
     }
     return GEM_OK;

@@ -633,3 +633,63 @@ def test_fullsize_layer_matches_reference_build(oracle):
     assert got.best_mapping.assignment.tolist() == want.best_mapping.assignment.tolist()
     assert [(r.provenance, tuple(r.trajectory)) for r in got.per_restart] == [
         (r.provenance, tuple(r.trajectory)) for r in want.per_restart]
+
+
+def _skewed_counts(rng, T, E, high):
+    """Zipf-like rows: a few heavy experts (identity changing over t) over a
+    light background -- the DeepSeek-V3 regime where the step floor skips most
+    GPU columns."""
+    tok = rng.integers(0, max(2, high // 8), (T, E))
+    for t in range(T):
+        heavy = rng.choice(E, 3, replace=False)
+        tok[t, heavy] += rng.integers(high // 2, high, 3)
+    return tok
+
+
+@pytest.mark.parametrize("E,G,split,key32,tied", [(256, 32, True, True, False), (256, 32, False, False, False),
+                                                  (128, 16, False, False, False), (64, 32, True, False, False),
+                                                  (256, 32, True, True, True), (128, 16, True, True, True)])
+def test_score_batch_step_floors(oracle, monkeypatch, E, G, split, key32, tied):
+    """K5 step floors (G >= 16): columns whose loads stay at or below the step's
+    skip level are not gathered and the maximum starts at the floor key. Must
+    equal the no-skip kernel, the CUDA-core scorer and the oracle bit for bit,
+    on skewed counts (most columns skipped) and on identical GPU curves (every
+    maximum tied with the floor value)."""
+    from paper_2605_19945_b200 import _device, _lib
+
+    if split:
+        monkeypatch.setenv("GEM_SCORE_SPLIT", "1")
+    if key32:
+        monkeypatch.setenv("GEM_SCORE_KEY32", "1")
+    rng = np.random.default_rng(E * 7 + G + 3 * split + 5 * tied)
+    L, T, C = 2, 300, 24
+    tok = np.stack([_skewed_counts(rng, T, E, high=900) for _ in range(L)])
+    if tied:
+        one = staircase_profile(gem, rng, 1, tile=16, tiles=200).curves[0]
+        p = gem.VariabilityProfile(tuple(one for _ in range(G)))
+    else:
+        p = mixed_profile(gem, rng, G)
+    cand = np.stack([[balanced_assignment(rng, E, G) for _ in range(L)] for _ in range(C)])
+    hist, nmax = _device.counts_to_device_int32(tok)
+    dc = _device.DeviceCurves.from_profile(p)
+    lut = dc.lut(nmax)
+    cd = torch.from_numpy(cand.astype(np.int8)).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    out = {}
+    for name, fn, noskip in (("skip", "gem_score_batch_tc", False), ("noskip", "gem_score_batch_tc", True),
+                             ("v1", "gem_score_batch_v1", False)):
+        if noskip:
+            monkeypatch.setenv("GEM_SCORE_NOSKIP", "1")
+        else:
+            monkeypatch.delenv("GEM_SCORE_NOSKIP", raising=False)
+        ls = torch.zeros((C, L), dtype=torch.float64, device="cuda")
+        err = torch.zeros((1,), dtype=torch.int32, device="cuda")
+        rc = getattr(_lib.lib(), fn)(hist.data_ptr(), L, T, E, G, cd.data_ptr(), C, lut.data_ptr(), dc.lut_nmax,
+                                     ls.data_ptr(), err.data_ptr(), st)
+        assert rc == 0, (name, rc, _lib.lib().gem_last_error())
+        out[name] = ls.cpu().numpy()
+    assert np.array_equal(out["skip"], out["noskip"])
+    assert np.array_equal(out["skip"], out["v1"])
+    cv = oracle.Curves.from_profile(p)
+    for c in range(0, C, 5):
+        assert out["skip"][c].tolist() == [oracle.score(tok[l], cand[c, l], cv) for l in range(L)]
