@@ -294,6 +294,31 @@ __global__ void row_bits_kernel(const double* __restrict__ lut, int64_t width, i
 //   offset rel + goff[g].  (KeyRowConsts above.)
 
 // KT: u16 keys, or u32 when the window holds more than 65,536 distinct latencies.
+// K5 A operand, once per call: counts h < 4096 as u8 limbs [lo | 16*hi] per K
+// part of EH = E/KH experts, rows padded with zeros to a multiple of 128 steps
+// (limbs[(l*Tpad + t)*2E + p*2EH + {0, EH} + e - p*EH]); every candidate tile
+// of a layer then moves 16-byte chunks instead of converting counts
+__global__ void limbs_kernel(const int32_t* __restrict__ hist, int64_t L, int64_t T, int64_t Tpad, int E, int EH,
+                             uint8_t* __restrict__ limbs) {
+  const int E4 = E / 4;
+  const int64_t n = L * Tpad * E4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / E4;
+    const int e = (int)(i - r * E4) * 4;
+    const int64_t l = r / Tpad, t = r - l * Tpad;
+    int4 h = make_int4(0, 0, 0, 0);
+    if (t < T) h = __ldg(reinterpret_cast<const int4*>(hist + (l * T + t) * E + e));
+    const uint32_t lo = (uint32_t)(h.x & 255) | ((uint32_t)(h.y & 255) << 8) | ((uint32_t)(h.z & 255) << 16) |
+                        ((uint32_t)(h.w & 255) << 24);
+    const uint32_t hi = (uint32_t)((h.x >> 8) << 4) | ((uint32_t)((h.y >> 8) << 4) << 8) |
+                        ((uint32_t)((h.z >> 8) << 4) << 16) | ((uint32_t)((h.w >> 8) << 4) << 24);
+    const int p = e / EH, eo = e - p * EH;
+    uint8_t* row = limbs + r * (2 * E) + p * 2 * EH;
+    *reinterpret_cast<uint32_t*>(row + eo) = lo;
+    *reinterpret_cast<uint32_t*>(row + EH + eo) = hi;
+  }
+}
+
 // key gathers: volatile under SKIP so they stay inside their warp-uniform
 // branch (not speculated above it); free to schedule otherwise
 #define GEM_KEY_LD(...)                 \
@@ -309,7 +334,7 @@ __global__ void row_bits_kernel(const double* __restrict__ lut, int64_t width, i
 // steps has its load above the step's skip level.
 template <int E, int G, int KH, bool SPLIT, typename KT, int NW, bool SKIP>
 __global__ void __launch_bounds__(NW * 32, 1)
-maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __restrict__ cand, int64_t C,
+maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __restrict__ cand, int64_t C,
                  int64_t L, int64_t layer0, int64_t Cp, const KT* __restrict__ gkeys, int keys_total,
                  const __grid_constant__ KeyRowConsts kr, int WS, int WG, const int2* __restrict__ floor_tab,
                  KT* __restrict__ out_keys) {
@@ -343,7 +368,8 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
   const int64_t c0 = (int64_t)blockIdx.x * CT;
   const int64_t lb = blockIdx.y;  // layer within the batch
   const int64_t l = layer0 + lb;
-  const int32_t* hl = hist + l * T * E;
+  const int64_t Tpad = (T + 127) / 128 * 128;
+  const uint8_t* al = limbs + l * Tpad * (2 * E);  // this layer's A rows
   KT* out = out_keys + lb * T * Cp;
 
   if (tid == 0) {
@@ -393,34 +419,30 @@ maxkey_tc_kernel(const int32_t* __restrict__ hist, int64_t T, const int8_t* __re
   const uint32_t sk_addr = tc::smem_u32(skeys);
   const char* gk_bytes = reinterpret_cast<const char*>(gkeys);
 
-  // H rows of one K part: each warp reads whole rows (coalesced); the next
-  // part's rows are in flight during the current part's MMA (and epilogue)
+  // A rows of one K part come precomputed as u8 limbs (limbs_kernel: [L][Tpad][2E],
+  // part p = bytes [p*KBH, (p+1)*KBH) of a row, zero rows past T): each lane
+  // moves 16-byte K chunks (coalesced rows in, conflict-free padded K slices
+  // out); the next part's rows are in flight during the current part's MMA
+  // (and epilogue)
   constexpr int RPW = 128 / NW;                  // rows per warp
-  constexpr int LPR = EH / 4;                    // lanes per row (4 experts each)
+  constexpr int LPR = KCH;                       // lanes per row (one 16-byte K chunk each)
   constexpr int RPI = 32 / LPR;                  // rows per warp instruction
   constexpr int NX = RPW / RPI;
+  static_assert(RPW % RPI == 0, "rows per warp");
   int4 x[NX];
   auto load_rows = [&](int i, int part) {
 #pragma unroll
     for (int v = 0; v < NX; ++v) {
       const int row = warp * RPW + v * RPI + lane / LPR;
-      const int64_t t = (int64_t)i * 128 + row;
-      x[v] = t < T ? __ldg(reinterpret_cast<const int4*>(hl + t * E + part * EH) + (lane % LPR))
-                   : make_int4(0, 0, 0, 0);
+      x[v] = __ldg(reinterpret_cast<const int4*>(al + ((int64_t)i * 128 + row) * (2 * E) + part * KBH) +
+                   (lane % LPR));
     }
   };
-  auto write_a = [&]() {  // u8 limbs, lo bytes at K = e, 16*hi at K = EH + e (h < 4096)
+  auto write_a = [&]() {
 #pragma unroll
     for (int v = 0; v < NX; ++v) {
       const int row = warp * RPW + v * RPI + lane / LPR;
-      const int e4 = lane % LPR;  // experts 4*e4 .. 4*e4+3 of the part
-      const uint32_t lo = __byte_perm(__byte_perm((uint32_t)x[v].x, (uint32_t)x[v].y, 0x0040),
-                                      __byte_perm((uint32_t)x[v].z, (uint32_t)x[v].w, 0x0040), 0x5410);
-      const uint32_t hi = __byte_perm(__byte_perm((uint32_t)x[v].x, (uint32_t)x[v].y, 0x0051),
-                                      __byte_perm((uint32_t)x[v].z, (uint32_t)x[v].w, 0x0051), 0x5410) << 4;
-      unsigned char* rowp = sa + (size_t)row * 16 + (e4 & 3) * 4;
-      *reinterpret_cast<uint32_t*>(rowp + (size_t)(e4 >> 2) * LBO_A) = lo;
-      *reinterpret_cast<uint32_t*>(rowp + (size_t)(EH / 16 + (e4 >> 2)) * LBO_A) = hi;
+      *reinterpret_cast<int4*>(sa + (size_t)(lane % LPR) * LBO_A + (size_t)row * 16) = x[v];
     }
     tc::fence_async_smem();
   };
@@ -656,7 +678,7 @@ constexpr bool maxkey_fits() {
 }
 
 template <int E, typename KT>
-static int launch_maxkey(int G, bool split, bool skip, dim3 grid, size_t smem, cudaStream_t st, const int32_t* hist,
+static int launch_maxkey(int G, bool split, bool skip, dim3 grid, size_t smem, cudaStream_t st, const uint8_t* limbs,
                          int64_t T, const int8_t* cand, int64_t C, int64_t L, int64_t l0, int64_t Cp,
                          const KT* keys, int keys_total, const KeyRowConsts& kr, int WS, int WG, const int2* fl,
                          KT* out) {
@@ -664,7 +686,7 @@ static int launch_maxkey(int G, bool split, bool skip, dim3 grid, size_t smem, c
   constexpr int NW = kLtWarps, NWS = kLtWarpsSkip;
   auto pick = [&](auto kern) -> int {
     GEM_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, (skip ? NWS : NW) * 32, smem, st>>>(hist, T, cand, C, L, l0, Cp, keys, keys_total, kr, WS, WG, fl,
+    kern<<<grid, (skip ? NWS : NW) * 32, smem, st>>>(limbs, T, cand, C, L, l0, Cp, keys, keys_total, kr, WS, WG, fl,
                                                      out);
     GEM_CHECK_LAUNCH("maxkey_tc_kernel");
     return GEM_OK;
@@ -868,6 +890,13 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   if (P < 1) return 1;
   void* kbuf = alloc(per_layer * P);
   if (!kbuf) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc key buffer");
+  // A rows as u8 limbs, once for all candidate tiles
+  const int64_t Tpad = (T + 127) / 128 * 128;
+  uint8_t* limbs = static_cast<uint8_t*>(alloc((size_t)L * Tpad * 2 * E));
+  if (!limbs) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc limbs");
+  limbs_kernel<<<(unsigned)imin64((L * Tpad * (E / 4) + 255) / 256, 32 * num_sms()), 256, 0, st>>>(
+      hist, L, T, Tpad, E, E == 256 ? 128 : E, limbs);
+  GEM_CHECK_LAUNCH("limbs_kernel");
   // step floors (G >= 16; GEM_SCORE_NOSKIP turns them off): {skip level, floor
   // key} per load level h in [0, W), then per step of every layer
   const bool skip = G >= 16 && !std::getenv("GEM_SCORE_NOSKIP");
@@ -902,11 +931,11 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
       const int64_t nb = imin64(P, L - l0);
       const dim3 g1((unsigned)ntile, (unsigned)nb);
       const int rc =
-          E == 256 ? launch_maxkey<256, KT>(G, split, skip, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
+          E == 256 ? launch_maxkey<256, KT>(G, split, skip, g1, lt_smem, st, limbs, T, cand, C, L, l0, Cp, kt_keys,
                                             keys_total, kr, WS, WG, floors, kt_buf)
-          : E == 128 ? launch_maxkey<128, KT>(G, split, skip, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
+          : E == 128 ? launch_maxkey<128, KT>(G, split, skip, g1, lt_smem, st, limbs, T, cand, C, L, l0, Cp, kt_keys,
                                               keys_total, kr, WS, WG, floors, kt_buf)
-                     : launch_maxkey<64, KT>(G, split, skip, g1, lt_smem, st, hist, T, cand, C, L, l0, Cp, kt_keys,
+                     : launch_maxkey<64, KT>(G, split, skip, g1, lt_smem, st, limbs, T, cand, C, L, l0, Cp, kt_keys,
                                              keys_total, kr, WS, WG, floors, kt_buf);
       if (rc) return rc;
       ks<<<dim3((unsigned)((C + 4 * kSumThreads - 1) / (4 * kSumThreads)), (unsigned)nb), kSumThreads,
