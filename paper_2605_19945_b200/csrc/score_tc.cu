@@ -29,6 +29,7 @@
 // Bit-exact with score_layers_kernel and the oracle by construction.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -938,8 +939,17 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
                      : launch_maxkey<64, KT>(G, split, skip, g1, lt_smem, st, limbs, T, cand, C, L, l0, Cp, kt_keys,
                                              keys_total, kr, WS, WG, floors, kt_buf);
       if (rc) return rc;
-      ks<<<dim3((unsigned)((C + 4 * kSumThreads - 1) / (4 * kSumThreads)), (unsigned)nb), kSumThreads,
-           (size_t)kSumSmemVals * 8, st>>>(kt_buf, T, C, Cp, L, l0, vals, nu, kmin, layer_scores);
+      // CTA size with the fullest last wave (3 CTAs per SM, shared-memory
+      // limited): at C4 940 CTAs of 256 = 2.12 waves, 1316 of 192 = 2.96
+      int bs = kSumThreads;
+      double best = -1.0;
+      for (int cand_bs = kSumThreads; cand_bs >= 128; cand_bs -= 64) {
+        const double waves = (double)(((C + 4 * cand_bs - 1) / (4 * cand_bs)) * nb) / (3.0 * num_sms());
+        const double eff = waves / std::ceil(waves);
+        if (eff > best + 0.02) best = eff, bs = cand_bs;
+      }
+      ks<<<dim3((unsigned)((C + 4 * bs - 1) / (4 * bs)), (unsigned)nb), bs, (size_t)kSumSmemVals * 8, st>>>(
+          kt_buf, T, C, Cp, L, l0, vals, nu, kmin, layer_scores);
       GEM_CHECK_LAUNCH("keysum_kernel");
     }
     return GEM_OK;
