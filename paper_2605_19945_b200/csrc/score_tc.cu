@@ -500,13 +500,46 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
             uint32_t key;
             const int32_t rel = max((int32_t)v[j * G + g] * KBY + kr.koff[g], kr.kbase[g]);
             const uint32_t sak = sk_addr + (uint32_t)rel;
-            if (!SPLIT) {
+            if (!SPLIT && SKIP) {  // lanes at or below their step's skip level load nothing (key 0)
+              const uint32_t need = (int32_t)v[j * G + g] > fl.x ? 1u : 0u;
+              if constexpr (KBY == 2) {
+                uint16_t k16;
+                GEM_KEY_LD("{\n\t.reg .pred pn;\n\tsetp.ne.u32 pn, %2, 0;\n\tmov.u16 %0, 0;\n\t"
+                           "@pn ld.shared.u16 %0, [%1];\n\t}" : "=h"(k16) : "r"(sak), "r"(need));
+                key = k16;
+              } else {
+                GEM_KEY_LD("{\n\t.reg .pred pn;\n\tsetp.ne.u32 pn, %2, 0;\n\tmov.u32 %0, 0;\n\t"
+                           "@pn ld.shared.u32 %0, [%1];\n\t}" : "=r"(key) : "r"(sak), "r"(need));
+              }
+            } else if (!SPLIT) {
               if constexpr (KBY == 2) {
                 uint16_t k16;
                 GEM_KEY_LD("ld.shared.u16 %0, [%1];" : "=h"(k16) : "r"(sak));
                 key = k16;
               } else {
                 GEM_KEY_LD("ld.shared.u32 %0, [%1];" : "=r"(key) : "r"(sak));
+              }
+            } else if constexpr (SKIP) {
+              // a lane whose own load is at or below its step's skip level
+              // cannot raise the maximum and loads nothing (key 0): most lanes
+              // of a gathered column, whose load would often miss the shared
+              // rows and go to L2
+              const char* ga = gk_bytes + (rel + kr.goff[g]);
+              const uint32_t need = (int32_t)v[j * G + g] > fl.x ? 1u : 0u;
+              if constexpr (KBY == 2) {
+                uint16_t k16;
+                GEM_KEY_LD("{\n\t.reg .pred pw, pn, ps, pg;\n\tsetp.lt.s32 pw, %1, %2;\n\t"
+                    "setp.ne.u32 pn, %5, 0;\n\tand.pred ps, pw, pn;\n\tand.pred pg, !pw, pn;\n\t"
+                    "mov.u16 %0, 0;\n\t@ps ld.shared.u16 %0, [%3];\n\t@pg ld.global.nc.u16 %0, [%4];\n\t}"
+                    : "=h"(k16)
+                    : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga), "r"(need));
+                key = k16;
+              } else {
+                GEM_KEY_LD("{\n\t.reg .pred pw, pn, ps, pg;\n\tsetp.lt.s32 pw, %1, %2;\n\t"
+                    "setp.ne.u32 pn, %5, 0;\n\tand.pred ps, pw, pn;\n\tand.pred pg, !pw, pn;\n\t"
+                    "mov.u32 %0, 0;\n\t@ps ld.shared.u32 %0, [%3];\n\t@pg ld.global.nc.u32 %0, [%4];\n\t}"
+                    : "=r"(key)
+                    : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga), "r"(need));
               }
             } else {
               const char* ga = gk_bytes + (rel + kr.goff[g]);
