@@ -363,7 +363,11 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
   unsigned char* sb = lt_smem + A_BYTES;
   LoadsTcShared* sh = reinterpret_cast<LoadsTcShared*>(sb + B_BYTES);
   KT* skeys = reinterpret_cast<KT*>(sb + B_BYTES + 64 + 256);  // packed key rows (SPLIT: [G][WS])
-  unsigned char* stg = sa;  // the A tile's space, free once the tile's MMAs completed
+  // key staging: the A tile's space, free once the tile's MMAs completed; under
+  // step floors (next tile's MMAs in flight) the bytes after the key rows
+  unsigned char* stg = SKIP ? reinterpret_cast<unsigned char*>(skeys) +
+                                  (SPLIT ? (size_t)G * WS * KBY : (((size_t)keys_total * KBY + 15) & ~size_t(15)))
+                            : sa;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * CT;
@@ -377,7 +381,7 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
     tc::mbar_init(&sh->mma_bar, 1);
     tc::fence_mbar_init();
   }
-  if (warp == 0) tc::tmem_alloc<kLtN>(&sh->tmem_base);
+  if (warp == 0) tc::tmem_alloc<SKIP ? 2 * kLtN : kLtN>(&sh->tmem_base);
   if (!SPLIT) {  // key rows -> shared memory (16-byte pieces; the global copy is padded to 16 bytes)
     const int pieces = (keys_total * KBY + 15) / 16;
     for (int i = tid; i < pieces; i += NT)
@@ -447,14 +451,14 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
     }
     tc::fence_async_smem();
   };
-  auto issue_mma = [&](int part) {
+  auto issue_mma = [&](int part, uint32_t col) {
     if (tid == 0) {
       tc::tc_fence_after();
 #pragma unroll
       for (int k = 0; k < KBH / 32; ++k) {
         const uint64_t ad = tc::smem_desc(sa_addr + k * 2 * LBO_A, LBO_A, 128);
         const uint64_t bd = tc::smem_desc(sb_addr + (part * KCH + k * 2) * LBO_B, LBO_B, 128);
-        tc::mma_i8(tmem, ad, bd, idesc, (part > 0 || k > 0) ? 1u : 0u);
+        tc::mma_i8(tmem + col, ad, bd, idesc, (part > 0 || k > 0) ? 1u : 0u);
       }
       tc::mma_commit(&sh->mma_bar);
     }
@@ -462,169 +466,227 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
   uint32_t mma_phase = 0;
   load_rows(0, 0);
   const int2* fl_l = SKIP ? floor_tab + l * T : nullptr;
-  for (int i = 0; i < ntiles; ++i) {
-    int2 fl = make_int2(INT32_MAX, 0);  // this lane's step (TMEM lane): {skip level, floor key}
+  auto step_floor = [&](int i) {  // this lane's step (TMEM lane): {skip level, floor key}
+    int2 fl = make_int2(INT32_MAX, 0);
     if constexpr (SKIP) {
       const int64_t ts = (int64_t)i * 128 + lg * 32 + lane;
       if (ts < T) fl = __ldg(fl_l + ts);
     }
+    return fl;
+  };
+  auto mma_wait = [&]() {
+    tc::mbar_wait(&sh->mma_bar, mma_phase);
+    mma_phase ^= 1u;
+    tc::tc_fence_after();
+  };
+  // ---- epilogue of tile i from TMEM columns [tcol, tcol + kLtN): warp w drains
+  // TMEM lanes 32(w%4).. (one step per lane) and column group w/4 in 32-column
+  // chunks; load n of GPU g -> key; the maximum over a candidate's G columns is
+  // its step key. mid() runs after the first chunk.
+  auto epilogue = [&](int i, uint32_t tcol, const int2 fl, auto&& mid) {
+      {
+        const uint32_t trow = tmem + tcol + ((uint32_t)(lg * 32) << 16);
+        uint32_t kk[KPT];
+  #pragma unroll
+        for (int ch = 0; ch < kLtN / NQ / 32; ++ch) {
+          uint32_t v[32];
+          tc::tmem_ld32(trow + cg * (kLtN / NQ) + ch * 32, v);
+          tc::tmem_ld_wait();
+  #pragma unroll
+          for (int j = 0; j < CPL; ++j) {
+            auto gather = [&](int g) -> uint32_t {
+              uint32_t key;
+              const int32_t rel = max((int32_t)v[j * G + g] * KBY + kr.koff[g], kr.kbase[g]);
+              const uint32_t sak = sk_addr + (uint32_t)rel;
+              if (!SPLIT && SKIP) {  // lanes at or below their step's skip level load nothing (key 0)
+                const uint32_t need = (int32_t)v[j * G + g] > fl.x ? 1u : 0u;
+                if constexpr (KBY == 2) {
+                  uint16_t k16;
+                  GEM_KEY_LD("{\n\t.reg .pred pn;\n\tsetp.ne.u32 pn, %2, 0;\n\tmov.u16 %0, 0;\n\t"
+                             "@pn ld.shared.u16 %0, [%1];\n\t}" : "=h"(k16) : "r"(sak), "r"(need));
+                  key = k16;
+                } else {
+                  GEM_KEY_LD("{\n\t.reg .pred pn;\n\tsetp.ne.u32 pn, %2, 0;\n\tmov.u32 %0, 0;\n\t"
+                             "@pn ld.shared.u32 %0, [%1];\n\t}" : "=r"(key) : "r"(sak), "r"(need));
+                }
+              } else if (!SPLIT) {
+                if constexpr (KBY == 2) {
+                  uint16_t k16;
+                  GEM_KEY_LD("ld.shared.u16 %0, [%1];" : "=h"(k16) : "r"(sak));
+                  key = k16;
+                } else {
+                  GEM_KEY_LD("ld.shared.u32 %0, [%1];" : "=r"(key) : "r"(sak));
+                }
+              } else if constexpr (SKIP) {
+                // a lane whose own load is at or below its step's skip level
+                // cannot raise the maximum and loads nothing (key 0): most lanes
+                // of a gathered column, whose load would often miss the shared
+                // rows and go to L2
+                const char* ga = gk_bytes + (rel + kr.goff[g]);
+                const uint32_t need = (int32_t)v[j * G + g] > fl.x ? 1u : 0u;
+                if constexpr (KBY == 2) {
+                  uint16_t k16;
+                  GEM_KEY_LD("{\n\t.reg .pred pw, pn, ps, pg;\n\tsetp.lt.s32 pw, %1, %2;\n\t"
+                      "setp.ne.u32 pn, %5, 0;\n\tand.pred ps, pw, pn;\n\tand.pred pg, !pw, pn;\n\t"
+                      "mov.u16 %0, 0;\n\t@ps ld.shared.u16 %0, [%3];\n\t@pg ld.global.nc.u16 %0, [%4];\n\t}"
+                      : "=h"(k16)
+                      : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga), "r"(need));
+                  key = k16;
+                } else {
+                  GEM_KEY_LD("{\n\t.reg .pred pw, pn, ps, pg;\n\tsetp.lt.s32 pw, %1, %2;\n\t"
+                      "setp.ne.u32 pn, %5, 0;\n\tand.pred ps, pw, pn;\n\tand.pred pg, !pw, pn;\n\t"
+                      "mov.u32 %0, 0;\n\t@ps ld.shared.u32 %0, [%3];\n\t@pg ld.global.nc.u32 %0, [%4];\n\t}"
+                      : "=r"(key)
+                      : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga), "r"(need));
+                }
+              } else {
+                const char* ga = gk_bytes + (rel + kr.goff[g]);
+                if constexpr (KBY == 2) {
+                  uint16_t k16;
+                  GEM_KEY_LD("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t"
+                      "@p ld.shared.u16 %0, [%3];\n\t@!p ld.global.nc.u16 %0, [%4];\n\t}"
+                      : "=h"(k16)
+                      : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga));
+                  key = k16;
+                } else {
+                  GEM_KEY_LD("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t"
+                      "@p ld.shared.u32 %0, [%3];\n\t@!p ld.global.nc.u32 %0, [%4];\n\t}"
+                      : "=r"(key)
+                      : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga));
+                }
+              }
+              return key;
+            };
+            uint32_t m = 0u;
+            if constexpr (SKIP) {
+              // warp-uniform set of the GPU columns with a load above the skip
+              // level in any of the warp's 32 steps; their gathers are issued
+              // back to back (the maximum is taken after the last one)
+              uint32_t kx[G];
+  #pragma unroll
+              for (int g = 0; g < G; ++g)
+                kx[g] = __any_sync(0xffffffffu, (int32_t)v[j * G + g] > fl.x) ? gather(g) : 0u;
+              m = (uint32_t)fl.y;
+  #pragma unroll
+              for (int g = 0; g < G; ++g) m = max(m, kx[g]);
+            } else {
+  #pragma unroll
+              for (int g = 0; g < G; ++g) m = max(m, gather(g));
+            }
+            kk[ch * CPL + j] = m;
+          }
+          if (ch == 0) mid();
+        }
+        // stage the keys (the A tile's space once its MMAs completed; a separate
+        // buffer when the next tile's MMAs run under this epilogue), then store rows
+        // of KPT keys per step, 16-byte pieces
+        unsigned char* wst = stg + warp * 32 * STG_ROW;
+        if constexpr (KBY == 2) {
+  #pragma unroll
+          for (int x8 = 0; x8 < KPT / 8; ++x8)
+            *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x8 * 16) =
+                make_uint4(kk[8 * x8] | (kk[8 * x8 + 1] << 16), kk[8 * x8 + 2] | (kk[8 * x8 + 3] << 16),
+                           kk[8 * x8 + 4] | (kk[8 * x8 + 5] << 16), kk[8 * x8 + 6] | (kk[8 * x8 + 7] << 16));
+          if (KPT % 8 == 4)
+            *reinterpret_cast<uint2*>(wst + lane * STG_ROW + (KPT / 8) * 16) =
+                make_uint2(kk[KPT - 4] | (kk[KPT - 3] << 16), kk[KPT - 2] | (kk[KPT - 1] << 16));
+          if (KPT == 2) *reinterpret_cast<uint32_t*>(wst + lane * STG_ROW) = kk[0] | (kk[1] << 16);
+        } else {
+  #pragma unroll
+          for (int x4 = 0; x4 < KPT / 4; ++x4)
+            *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x4 * 16) =
+                make_uint4(kk[4 * x4], kk[4 * x4 + 1], kk[4 * x4 + 2], kk[4 * x4 + 3]);
+          if (KPT == 2) *reinterpret_cast<uint2*>(wst + lane * STG_ROW) = make_uint2(kk[0], kk[1]);
+        }
+        __syncwarp();
+        const int64_t tbase = (int64_t)i * 128 + lg * 32;
+        const int64_t cbase = c0 + cg * KPT;
+        if constexpr (KPT >= KPP) {
+          constexpr int PPR = KPT / KPP;  // 16-byte pieces per row
+          for (int q = lane; q < 32 * PPR; q += 32) {
+            const int r = q / PPR, piece = q % PPR;
+            const int64_t t = tbase + r;
+            if (t < T)
+              *reinterpret_cast<uint4*>(out + t * Cp + cbase + piece * KPP) =
+                  *reinterpret_cast<const uint4*>(wst + r * STG_ROW + piece * 16);
+          }
+        } else if constexpr (KPT * KBY == 8) {  // one 8-byte piece per row
+          const int64_t t = tbase + lane;
+          if (t < T)
+            *reinterpret_cast<uint2*>(out + t * Cp + cbase) = *reinterpret_cast<const uint2*>(wst + lane * STG_ROW);
+        } else {  // u16, KPT == 2: one 4-byte piece per row
+          static_assert(KPT * KBY == 4, "key row pieces of 4, 8 or 16k bytes");
+          const int64_t t = tbase + lane;
+          if (t < T)
+            *reinterpret_cast<uint32_t*>(out + t * Cp + cbase) = *reinterpret_cast<const uint32_t*>(wst + lane * STG_ROW);
+        }
+      }
+  };
+  if constexpr (!SKIP) {
+    for (int i = 0; i < ntiles; ++i) {
+      const int2 fl = step_floor(i);
 #pragma unroll
-    for (int part = 0; part < KH; ++part) {
+      for (int part = 0; part < KH; ++part) {
+        write_a();
+        __syncthreads();
+        issue_mma(part, 0);
+        if (part + 1 < KH) load_rows(i, part + 1);
+        else if (i + 1 < ntiles) load_rows(i + 1, 0);
+        mma_wait();
+        if (part + 1 < KH) {
+          tc::tc_fence_before();
+          __syncthreads();  // the A buffer is free for the next part
+        }
+      }
+      epilogue(i, 0u, fl, [] {});
+      tc::tc_fence_before();
+      __syncthreads();  // TMEM and the A tile are free for tile i+1
+    }
+  } else {
+    // step floors: the epilogue is latency-bound and long, so tile i+1's MMAs run
+    // under tile i's epilogue -- TMEM double-buffered (2 x kLtN columns), part 0
+    // issued before it, part 1 (E = 256) after its first chunk; keys staged in a
+    // separate buffer (the A tile is busy)
+#pragma unroll
+    for (int part = 0; part < KH; ++part) {  // tile 0 into columns [0, kLtN)
       write_a();
       __syncthreads();
-      issue_mma(part);
-      if (part + 1 < KH) load_rows(i, part + 1);
-      else if (i + 1 < ntiles) load_rows(i + 1, 0);
-      tc::mbar_wait(&sh->mma_bar, mma_phase);
-      mma_phase ^= 1u;
-      tc::tc_fence_after();
+      issue_mma(part, 0);
+      if (part + 1 < KH) load_rows(0, part + 1);
+      else if (ntiles > 1) load_rows(1, 0);
+      mma_wait();
       if (part + 1 < KH) {
         tc::tc_fence_before();
-        __syncthreads();  // the A buffer is free for the next part
+        __syncthreads();
       }
     }
-    // ---- epilogue: warp w drains TMEM lanes 32(w%4).. (one step per lane) and
-    // column group w/4 in 32-column chunks; load n of GPU g -> key; the maximum
-    // over a candidate's G columns is its step key
-    {
-      const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16);
-      uint32_t kk[KPT];
-#pragma unroll
-      for (int ch = 0; ch < kLtN / NQ / 32; ++ch) {
-        uint32_t v[32];
-        tc::tmem_ld32(trow + cg * (kLtN / NQ) + ch * 32, v);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) {
-          auto gather = [&](int g) -> uint32_t {
-            uint32_t key;
-            const int32_t rel = max((int32_t)v[j * G + g] * KBY + kr.koff[g], kr.kbase[g]);
-            const uint32_t sak = sk_addr + (uint32_t)rel;
-            if (!SPLIT && SKIP) {  // lanes at or below their step's skip level load nothing (key 0)
-              const uint32_t need = (int32_t)v[j * G + g] > fl.x ? 1u : 0u;
-              if constexpr (KBY == 2) {
-                uint16_t k16;
-                GEM_KEY_LD("{\n\t.reg .pred pn;\n\tsetp.ne.u32 pn, %2, 0;\n\tmov.u16 %0, 0;\n\t"
-                           "@pn ld.shared.u16 %0, [%1];\n\t}" : "=h"(k16) : "r"(sak), "r"(need));
-                key = k16;
-              } else {
-                GEM_KEY_LD("{\n\t.reg .pred pn;\n\tsetp.ne.u32 pn, %2, 0;\n\tmov.u32 %0, 0;\n\t"
-                           "@pn ld.shared.u32 %0, [%1];\n\t}" : "=r"(key) : "r"(sak), "r"(need));
-              }
-            } else if (!SPLIT) {
-              if constexpr (KBY == 2) {
-                uint16_t k16;
-                GEM_KEY_LD("ld.shared.u16 %0, [%1];" : "=h"(k16) : "r"(sak));
-                key = k16;
-              } else {
-                GEM_KEY_LD("ld.shared.u32 %0, [%1];" : "=r"(key) : "r"(sak));
-              }
-            } else if constexpr (SKIP) {
-              // a lane whose own load is at or below its step's skip level
-              // cannot raise the maximum and loads nothing (key 0): most lanes
-              // of a gathered column, whose load would often miss the shared
-              // rows and go to L2
-              const char* ga = gk_bytes + (rel + kr.goff[g]);
-              const uint32_t need = (int32_t)v[j * G + g] > fl.x ? 1u : 0u;
-              if constexpr (KBY == 2) {
-                uint16_t k16;
-                GEM_KEY_LD("{\n\t.reg .pred pw, pn, ps, pg;\n\tsetp.lt.s32 pw, %1, %2;\n\t"
-                    "setp.ne.u32 pn, %5, 0;\n\tand.pred ps, pw, pn;\n\tand.pred pg, !pw, pn;\n\t"
-                    "mov.u16 %0, 0;\n\t@ps ld.shared.u16 %0, [%3];\n\t@pg ld.global.nc.u16 %0, [%4];\n\t}"
-                    : "=h"(k16)
-                    : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga), "r"(need));
-                key = k16;
-              } else {
-                GEM_KEY_LD("{\n\t.reg .pred pw, pn, ps, pg;\n\tsetp.lt.s32 pw, %1, %2;\n\t"
-                    "setp.ne.u32 pn, %5, 0;\n\tand.pred ps, pw, pn;\n\tand.pred pg, !pw, pn;\n\t"
-                    "mov.u32 %0, 0;\n\t@ps ld.shared.u32 %0, [%3];\n\t@pg ld.global.nc.u32 %0, [%4];\n\t}"
-                    : "=r"(key)
-                    : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga), "r"(need));
-              }
-            } else {
-              const char* ga = gk_bytes + (rel + kr.goff[g]);
-              if constexpr (KBY == 2) {
-                uint16_t k16;
-                GEM_KEY_LD("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t"
-                    "@p ld.shared.u16 %0, [%3];\n\t@!p ld.global.nc.u16 %0, [%4];\n\t}"
-                    : "=h"(k16)
-                    : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga));
-                key = k16;
-              } else {
-                GEM_KEY_LD("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t"
-                    "@p ld.shared.u32 %0, [%3];\n\t@!p ld.global.nc.u32 %0, [%4];\n\t}"
-                    : "=r"(key)
-                    : "r"(rel), "r"(kr.kend[g]), "r"(sak), "l"(ga));
-              }
-            }
-            return key;
-          };
-          uint32_t m = 0u;
-          if constexpr (SKIP) {
-            // warp-uniform set of the GPU columns with a load above the skip
-            // level in any of the warp's 32 steps; their gathers are issued
-            // back to back (the maximum is taken after the last one)
-            uint32_t kx[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g)
-              kx[g] = __any_sync(0xffffffffu, (int32_t)v[j * G + g] > fl.x) ? gather(g) : 0u;
-            m = (uint32_t)fl.y;
-#pragma unroll
-            for (int g = 0; g < G; ++g) m = max(m, kx[g]);
-          } else {
-#pragma unroll
-            for (int g = 0; g < G; ++g) m = max(m, gather(g));
-          }
-          kk[ch * CPL + j] = m;
+    for (int i = 0; i < ntiles; ++i) {
+      const int2 fl = step_floor(i);
+      const uint32_t cur = (uint32_t)(i & 1) * kLtN, nxt = cur ^ (uint32_t)kLtN;
+      const bool more = i + 1 < ntiles;
+      if (more) {
+        write_a();  // rows (i+1, part 0); the A buffer's last MMA completed
+        __syncthreads();
+        issue_mma(0, nxt);
+        if (KH == 2) load_rows(i + 1, 1);
+        else if (i + 2 < ntiles) load_rows(i + 2, 0);
+      }
+      epilogue(i, cur, fl, [&] {
+        if (KH == 2 && more) {
+          mma_wait();  // part 0 of tile i+1: the A buffer is free
+          tc::tc_fence_before();
+          write_a();
+          __syncthreads();
+          issue_mma(1, nxt);
+          if (i + 2 < ntiles) load_rows(i + 2, 0);
         }
-      }
-      // the A tile is free (its MMAs completed): stage the keys, then store rows
-      // of KPT keys per step, 16-byte pieces
-      unsigned char* wst = stg + warp * 32 * STG_ROW;
-      if constexpr (KBY == 2) {
-#pragma unroll
-        for (int x8 = 0; x8 < KPT / 8; ++x8)
-          *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x8 * 16) =
-              make_uint4(kk[8 * x8] | (kk[8 * x8 + 1] << 16), kk[8 * x8 + 2] | (kk[8 * x8 + 3] << 16),
-                         kk[8 * x8 + 4] | (kk[8 * x8 + 5] << 16), kk[8 * x8 + 6] | (kk[8 * x8 + 7] << 16));
-        if (KPT % 8 == 4)
-          *reinterpret_cast<uint2*>(wst + lane * STG_ROW + (KPT / 8) * 16) =
-              make_uint2(kk[KPT - 4] | (kk[KPT - 3] << 16), kk[KPT - 2] | (kk[KPT - 1] << 16));
-        if (KPT == 2) *reinterpret_cast<uint32_t*>(wst + lane * STG_ROW) = kk[0] | (kk[1] << 16);
-      } else {
-#pragma unroll
-        for (int x4 = 0; x4 < KPT / 4; ++x4)
-          *reinterpret_cast<uint4*>(wst + lane * STG_ROW + x4 * 16) =
-              make_uint4(kk[4 * x4], kk[4 * x4 + 1], kk[4 * x4 + 2], kk[4 * x4 + 3]);
-        if (KPT == 2) *reinterpret_cast<uint2*>(wst + lane * STG_ROW) = make_uint2(kk[0], kk[1]);
-      }
-      __syncwarp();
-      const int64_t tbase = (int64_t)i * 128 + lg * 32;
-      const int64_t cbase = c0 + cg * KPT;
-      if constexpr (KPT >= KPP) {
-        constexpr int PPR = KPT / KPP;  // 16-byte pieces per row
-        for (int q = lane; q < 32 * PPR; q += 32) {
-          const int r = q / PPR, piece = q % PPR;
-          const int64_t t = tbase + r;
-          if (t < T)
-            *reinterpret_cast<uint4*>(out + t * Cp + cbase + piece * KPP) =
-                *reinterpret_cast<const uint4*>(wst + r * STG_ROW + piece * 16);
-        }
-      } else if constexpr (KPT * KBY == 8) {  // one 8-byte piece per row
-        const int64_t t = tbase + lane;
-        if (t < T)
-          *reinterpret_cast<uint2*>(out + t * Cp + cbase) = *reinterpret_cast<const uint2*>(wst + lane * STG_ROW);
-      } else {  // u16, KPT == 2: one 4-byte piece per row
-        static_assert(KPT * KBY == 4, "key row pieces of 4, 8 or 16k bytes");
-        const int64_t t = tbase + lane;
-        if (t < T)
-          *reinterpret_cast<uint32_t*>(out + t * Cp + cbase) = *reinterpret_cast<const uint32_t*>(wst + lane * STG_ROW);
-      }
+      });
+      if (more) mma_wait();  // the last part of tile i+1
+      tc::tc_fence_before();
+      __syncthreads();  // TMEM columns cur are free for tile i+2
     }
-    tc::tc_fence_before();
-    __syncthreads();  // TMEM and the A tile are free for tile i+1
   }
-  if (warp == 0) tc::tmem_dealloc<kLtN>(tmem);
+  if (warp == 0) tc::tmem_dealloc<SKIP ? 2 * kLtN : kLtN>(tmem);
 }
 
 // ---------------------------------------------------------------------------
@@ -864,7 +926,13 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
 
   // ---- shared memory: A (one K part of E/KH experts), B (K = 2E), barriers, row info, key rows
   const int KH = E == 256 ? 2 : 1;
-  const size_t fixed = (size_t)(128 * 16 + 16) * (2 * (E / KH) / 16) + (size_t)kLtN * 2 * E + 64 + 256;
+  // step floors (G >= 16; GEM_SCORE_NOSKIP turns them off); their kernel stages
+  // the step keys in a buffer of its own (the next tile's MMAs use the A tile)
+  const bool skip = G >= 16 && !std::getenv("GEM_SCORE_NOSKIP");
+  const size_t stg_bytes =
+      skip ? (size_t)kLtWarpsSkip * 32 * ((kLtN / G) / (kLtWarpsSkip / 4) * KBY + 16) : 0;
+  const size_t fixed =
+      (size_t)(128 * 16 + 16) * (2 * (E / KH) / 16) + (size_t)kLtN * 2 * E + 64 + 256 + stg_bytes;
   std::vector<int32_t> rowinfo = packed;
   int keys_total = npacked;
   size_t key_smem = (((size_t)keys_total * KBY) + 15) & ~size_t(15);
@@ -931,9 +999,8 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   limbs_kernel<<<(unsigned)imin64((L * Tpad * (E / 4) + 255) / 256, 32 * num_sms()), 256, 0, st>>>(
       hist, L, T, Tpad, E, E == 256 ? 128 : E, limbs);
   GEM_CHECK_LAUNCH("limbs_kernel");
-  // step floors (G >= 16; GEM_SCORE_NOSKIP turns them off): {skip level, floor
-  // key} per load level h in [0, W), then per step of every layer
-  const bool skip = G >= 16 && !std::getenv("GEM_SCORE_NOSKIP");
+  // step floors: {skip level, floor key} per load level h in [0, W), then per
+  // step of every layer
   int2* floors = nullptr;
   int32_t* kmin = nullptr;
   if (skip) {
