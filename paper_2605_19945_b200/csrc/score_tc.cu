@@ -682,8 +682,10 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
         }
       });
       if (more) mma_wait();  // the last part of tile i+1
+      // no barrier here: the next iteration's first __syncthreads (before tile
+      // i+2's MMA into columns cur) follows every warp's reads of them, and each
+      // warp's key staging area is its own
       tc::tc_fence_before();
-      __syncthreads();  // TMEM columns cur are free for tile i+2
     }
   }
   if (warp == 0) tc::tmem_dealloc<SKIP ? 2 * kLtN : kLtN>(tmem);
