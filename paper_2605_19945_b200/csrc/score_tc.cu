@@ -354,7 +354,7 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
   constexpr int CPL = 32 / G;                // candidates per 32-column TMEM load
   constexpr int STG_ROW = KPT * KBY + 16;    // staging row: the thread's keys + 16 B pad
   constexpr int STG_BYTES = NW * 32 * STG_ROW;
-  static_assert(STG_BYTES <= A_BYTES, "key staging must fit the A tile");
+  static_assert(STG_BYTES <= A_BYTES, "key staging size (the host reserves it after the key rows)");
   static_assert(G >= 4 && G <= 32 && (kLtN % G) == 0, "G in {4, 8, 16, 32}");
   static_assert(EH == 64 || EH == 128, "K parts of 64 or 128 experts");
   constexpr int KPP = 16 / KBY;              // keys per 16-byte piece
@@ -363,11 +363,9 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
   unsigned char* sb = lt_smem + A_BYTES;
   LoadsTcShared* sh = reinterpret_cast<LoadsTcShared*>(sb + B_BYTES);
   KT* skeys = reinterpret_cast<KT*>(sb + B_BYTES + 64 + 256);  // packed key rows (SPLIT: [G][WS])
-  // key staging: the A tile's space, free once the tile's MMAs completed; under
-  // step floors (next tile's MMAs in flight) the bytes after the key rows
-  unsigned char* stg = SKIP ? reinterpret_cast<unsigned char*>(skeys) +
-                                  (SPLIT ? (size_t)G * WS * KBY : (((size_t)keys_total * KBY + 15) & ~size_t(15)))
-                            : sa;
+  // key staging: the bytes after the key rows (the next tile's MMAs use the A tile)
+  unsigned char* stg = reinterpret_cast<unsigned char*>(skeys) +
+                       (SPLIT ? (size_t)G * WS * KBY : (((size_t)keys_total * KBY + 15) & ~size_t(15)));
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * CT;
@@ -381,7 +379,7 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
     tc::mbar_init(&sh->mma_bar, 1);
     tc::fence_mbar_init();
   }
-  if (warp == 0) tc::tmem_alloc<SKIP ? 2 * kLtN : kLtN>(&sh->tmem_base);
+  if (warp == 0) tc::tmem_alloc<2 * kLtN>(&sh->tmem_base);  // two accumulators (MMA/epilogue overlap)
   if (!SPLIT) {  // key rows -> shared memory (16-byte pieces; the global copy is padded to 16 bytes)
     const int pieces = (keys_total * KBY + 15) / 16;
     for (int i = tid; i < pieces; i += NT)
@@ -581,6 +579,7 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
         // buffer when the next tile's MMAs run under this epilogue), then store rows
         // of KPT keys per step, 16-byte pieces
         unsigned char* wst = stg + warp * 32 * STG_ROW;
+        __syncwarp();  // the warp's reads of its staging rows (previous tile) are done
         if constexpr (KBY == 2) {
   #pragma unroll
           for (int x8 = 0; x8 < KPT / 8; ++x8)
@@ -622,31 +621,11 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
         }
       }
   };
-  if constexpr (!SKIP) {
-    for (int i = 0; i < ntiles; ++i) {
-      const int2 fl = step_floor(i);
-#pragma unroll
-      for (int part = 0; part < KH; ++part) {
-        write_a();
-        __syncthreads();
-        issue_mma(part, 0);
-        if (part + 1 < KH) load_rows(i, part + 1);
-        else if (i + 1 < ntiles) load_rows(i + 1, 0);
-        mma_wait();
-        if (part + 1 < KH) {
-          tc::tc_fence_before();
-          __syncthreads();  // the A buffer is free for the next part
-        }
-      }
-      epilogue(i, 0u, fl, [] {});
-      tc::tc_fence_before();
-      __syncthreads();  // TMEM and the A tile are free for tile i+1
-    }
-  } else {
-    // step floors: the epilogue is latency-bound and long, so tile i+1's MMAs run
-    // under tile i's epilogue -- TMEM double-buffered (2 x kLtN columns), part 0
-    // issued before it, part 1 (E = 256) after its first chunk; keys staged in a
-    // separate buffer (the A tile is busy)
+  // tile i+1's MMAs run under tile i's epilogue (the epilogue's gathers are the
+  // long part): TMEM double-buffered (2 x kLtN columns), part 0 issued before
+  // it, part 1 (E = 256) after its first chunk; keys staged in a buffer of their
+  // own (the A tile is busy)
+  {
 #pragma unroll
     for (int part = 0; part < KH; ++part) {  // tile 0 into columns [0, kLtN)
       write_a();
@@ -688,7 +667,9 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
       tc::tc_fence_before();
     }
   }
-  if (warp == 0) tc::tmem_dealloc<SKIP ? 2 * kLtN : kLtN>(tmem);
+  __syncthreads();  // every warp's last TMEM reads precede the dealloc
+  tc::tc_fence_after();
+  if (warp == 0) tc::tmem_dealloc<2 * kLtN>(tmem);
 }
 
 // ---------------------------------------------------------------------------
@@ -928,11 +909,11 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
 
   // ---- shared memory: A (one K part of E/KH experts), B (K = 2E), barriers, row info, key rows
   const int KH = E == 256 ? 2 : 1;
-  // step floors (G >= 16; GEM_SCORE_NOSKIP turns them off); their kernel stages
-  // the step keys in a buffer of its own (the next tile's MMAs use the A tile)
+  // step floors (G >= 16; GEM_SCORE_NOSKIP turns them off); the kernels stage
+  // the step keys in a buffer of their own (the next tile's MMAs use the A tile)
   const bool skip = G >= 16 && !std::getenv("GEM_SCORE_NOSKIP");
-  const size_t stg_bytes =
-      skip ? (size_t)kLtWarpsSkip * 32 * ((kLtN / G) / (kLtWarpsSkip / 4) * KBY + 16) : 0;
+  const int nw_launch = skip ? kLtWarpsSkip : kLtWarps;
+  const size_t stg_bytes = (size_t)nw_launch * 32 * ((kLtN / G) / (nw_launch / 4) * KBY + 16);
   const size_t fixed =
       (size_t)(128 * 16 + 16) * (2 * (E / KH) / 16) + (size_t)kLtN * 2 * E + 64 + 256 + stg_bytes;
   std::vector<int32_t> rowinfo = packed;
