@@ -84,10 +84,10 @@ struct SearchWs {
 };
 
 #ifndef GEM_LOCK
-#define GEM_LOCK 16
+#define GEM_LOCK 64
 #endif
 #ifndef GEM_CANDK
-#define GEM_CANDK 64
+#define GEM_CANDK 256
 #endif
 constexpr int kLocK = GEM_LOCK;
 constexpr int kCandK = GEM_CANDK;
