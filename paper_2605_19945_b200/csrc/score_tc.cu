@@ -295,9 +295,9 @@ __global__ void row_bits_kernel(const double* __restrict__ lut, int64_t width, i
 //   offset rel + goff[g].  (KeyRowConsts above.)
 
 // KT: u16 keys, or u32 when the window holds more than 65,536 distinct latencies.
-// K5 A operand, once per call: counts h < 4096 as u8 limbs [lo | 16*hi] per K
-// part of EH = E/KH experts, rows padded with zeros to a multiple of 128 steps
-// (limbs[(l*Tpad + t)*2E + p*2EH + {0, EH} + e - p*EH]); every candidate tile
+// K5 A operand, once per layer batch: counts h < 4096 as u8 limbs [lo | 16*hi]
+// per K part of EH = E/KH experts, rows padded with zeros to a multiple of 128
+// steps (limbs[(lb*Tpad + t)*2E + p*2EH + {0, EH} + e - p*EH]); every candidate tile
 // of a layer then moves 16-byte chunks instead of converting counts
 __global__ void limbs_kernel(const int32_t* __restrict__ hist, int64_t L, int64_t T, int64_t Tpad, int E, int EH,
                              uint8_t* __restrict__ limbs) {
@@ -372,7 +372,7 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
   const int64_t lb = blockIdx.y;  // layer within the batch
   const int64_t l = layer0 + lb;
   const int64_t Tpad = (T + 127) / 128 * 128;
-  const uint8_t* al = limbs + l * Tpad * (2 * E);  // this layer's A rows
+  const uint8_t* al = limbs + lb * Tpad * (2 * E);  // this layer's A rows (limbs of the batch)
   KT* out = out_keys + lb * T * Cp;
 
   if (tid == 0) {
@@ -422,7 +422,7 @@ maxkey_tc_kernel(const uint8_t* __restrict__ limbs, int64_t T, const int8_t* __r
   const uint32_t sk_addr = tc::smem_u32(skeys);
   const char* gk_bytes = reinterpret_cast<const char*>(gkeys);
 
-  // A rows of one K part come precomputed as u8 limbs (limbs_kernel: [L][Tpad][2E],
+  // A rows of one K part come precomputed as u8 limbs (limbs_kernel: [batch layers][Tpad][2E],
   // part p = bytes [p*KBH, (p+1)*KBH) of a row, zero rows past T): each lane
   // moves 16-byte K chunks (coalesced rows in, conflict-free padded K slices
   // out); the next part's rows are in flight during the current part's MMA
@@ -975,13 +975,11 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
   if (P < 1) return 1;
   void* kbuf = alloc(per_layer * P);
   if (!kbuf) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc key buffer");
-  // A rows as u8 limbs, once for all candidate tiles
+  // A rows as u8 limbs, per layer batch (half the batch's histogram bytes),
+  // once for all candidate tiles
   const int64_t Tpad = (T + 127) / 128 * 128;
-  uint8_t* limbs = static_cast<uint8_t*>(alloc((size_t)L * Tpad * 2 * E));
+  uint8_t* limbs = static_cast<uint8_t*>(alloc((size_t)P * Tpad * 2 * E));
   if (!limbs) return fail_cuda(cudaErrorMemoryAllocation, "gem_score_batch_tc limbs");
-  limbs_kernel<<<(unsigned)imin64((L * Tpad * (E / 4) + 255) / 256, 32 * num_sms()), 256, 0, st>>>(
-      hist, L, T, Tpad, E, E == 256 ? 128 : E, limbs);
-  GEM_CHECK_LAUNCH("limbs_kernel");
   // step floors: {skip level, floor key} per load level h in [0, W), then per
   // step of every layer
   int2* floors = nullptr;
@@ -1014,6 +1012,9 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
     for (int64_t l0 = 0; l0 < L; l0 += P) {
       const int64_t nb = imin64(P, L - l0);
       const dim3 g1((unsigned)ntile, (unsigned)nb);
+      limbs_kernel<<<(unsigned)imin64((nb * Tpad * (E / 4) + 255) / 256, 32 * num_sms()), 256, 0, st>>>(
+          hist + l0 * T * E, nb, T, Tpad, E, E == 256 ? 128 : E, limbs);
+      GEM_CHECK_LAUNCH("limbs_kernel");
       const int rc =
           E == 256 ? launch_maxkey<256, KT>(G, split, skip, g1, lt_smem, st, limbs, T, cand, C, L, l0, Cp, kt_keys,
                                             keys_total, kr, WS, WG, floors, kt_buf)
