@@ -57,7 +57,11 @@ constexpr int kLtWarpsSkip = GEM_LT_WARPS_SKIP;
 constexpr int kLtN = 256;        // MMA N (candidate x GPU columns per CTA)
 constexpr int kMaxKeys = 65536;  // u16 keys
 constexpr int kSumThreads = 256;
-constexpr int kSumSmemVals = 8192;  // vals[0, 8192) in shared memory (64 KB)
+#ifndef GEM_SUM_VALS
+#define GEM_SUM_VALS 8192
+#endif
+constexpr int kSumSmemVals = GEM_SUM_VALS;  // vals[base, base + 8192) in shared memory (64 KB)
+constexpr int kSumCtasPerSm = (227 * 1024) / (kSumSmemVals * 8 + 1024);  // shared-memory limited
 
 struct LoadsTcShared {
   uint64_t mma_bar;
@@ -695,7 +699,7 @@ template <> struct Key4<uint32_t> {
 };
 
 template <typename KT>
-__global__ void __launch_bounds__(kSumThreads, 3)
+__global__ void __launch_bounds__(kSumThreads, kSumCtasPerSm)
 keysum_kernel(const KT* __restrict__ keys, int64_t T, int64_t C, int64_t Cp, int64_t L, int64_t layer0,
               const double* __restrict__ vals, const int32_t* __restrict__ nvals, const int32_t* __restrict__ vbase,
               double* __restrict__ layer_scores) {
@@ -1028,7 +1032,7 @@ extern "C" int gem_score_batch_tc(const int32_t* hist, int64_t L, int64_t T, int
       int bs = kSumThreads;
       double best = -1.0;
       for (int cand_bs = kSumThreads; cand_bs >= 128; cand_bs -= 64) {
-        const double waves = (double)(((C + 4 * cand_bs - 1) / (4 * cand_bs)) * nb) / (3.0 * num_sms());
+        const double waves = (double)(((C + 4 * cand_bs - 1) / (4 * cand_bs)) * nb) / ((double)kSumCtasPerSm * num_sms());
         const double eff = waves / std::ceil(waves);
         if (eff > best + 0.02) best = eff, bs = cand_bs;
       }
